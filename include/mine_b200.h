@@ -1,0 +1,177 @@
+/*
+ * mine_b200.h -- C ABI of the B200-native MINE score engine (libmine_b200.so).
+ *
+ * This is the drop-in boundary for the reference's hot path.
+ * The reference (/root/reference/proj) exposes the path as C++ free functions;
+ * the paper names the C engine's entry point mine_compute_score() and "three
+ * structures", which minepy spells mine_problem /
+ * mine_parameter / mine_score.  Each declaration below cites the reference
+ * interface it replaces.  Conventions:
+ *   - plain pointers and sizes, no C++ or CUDA types;
+ *   - no exceptions cross the ABI: functions return 0 / NULL on failure and
+ *     mine_b200_last_error() (thread-local) names the condition the reference
+ *     would have thrown std::invalid_argument / std::out_of_range for;
+ *   - every result is computed on the GPU (sm_100a); there is no CPU fallback,
+ *     and a missing / unusable GPU is an error;
+ *   - results are bit-identical to the reference for MIC, MAS, MEV, MCN (the
+ *     characteristic matrix itself is bit-identical), whatever the batch size,
+ *     tier or number of GPUs.
+ * Extensions absent from the reference (parity unpinned):
+ *   MIC_e (equicharacteristic matrix), TIC, the est switch, cross batches.
+ */
+#ifndef MINE_B200_H
+#define MINE_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MINE_B200_VERSION 100
+
+/* est: which characteristic matrix mine_score.M / TIC refer to. */
+#define MINE_EST_MIC_APPROX 0 /* the reference's CharacteristicMatrix (char_matrix.hpp:25-49) */
+#define MINE_EST_MIC_E 1      /* extension: equicharacteristic matrix */
+
+/* <-> mine::Parameters {alpha = 0.6, c = 15} (char_matrix.hpp:11-14), plus est. */
+typedef struct mine_parameter {
+  double alpha;
+  double c;
+  int est;
+} mine_parameter;
+
+/* <-> the (xs, ys) arguments of mine::compute_score (char_matrix.hpp:57). */
+typedef struct mine_problem {
+  int n;
+  double* x;
+  double* y;
+} mine_problem;
+
+/* <-> mine::CharacteristicMatrix (char_matrix.hpp:25-49): row i holds y = i+2,
+ * column j holds x = j+2, m[i] = floor(B/(i+2)) - 1 columns.  Library-owned;
+ * release with mine_free_score(). */
+typedef struct mine_score {
+  int n;         /* rows: B/2 - 1 */
+  int* m;        /* columns per row */
+  double** M;    /* matrix selected by param.est (MIC_approx: the reference's M) */
+  double** M_e;  /* extension: equicharacteristic matrix (always filled) */
+  int B;         /* grid bound, char_matrix.cpp:17-20 */
+  int est;
+} mine_score;
+
+/* Variable-major data matrix: n variables (rows) x m samples, row-major -- the
+ * layout of mine::Dataset::values' columns (analysis.hpp:16-22). */
+typedef struct mine_matrix {
+  double* data;
+  int n;
+  int m;
+} mine_matrix;
+
+/* minepy-style batch results: MIC and TIC per pair. */
+typedef struct mine_pstats {
+  long long n; /* pairs: p(p-1)/2 in PairSequence order (analysis.cpp:66-81) */
+  double* mic;
+  double* tic;
+} mine_pstats;
+typedef struct mine_cstats {
+  long long n; /* X variables */
+  long long m; /* Y variables; results are n x m row-major */
+  double* mic;
+  double* tic;
+} mine_cstats;
+
+/* Caller-allocated per-pair outputs; any pointer may be NULL.  mic/mas/mev/mcn
+ * <-> MineStatistics (statistics.hpp:10-17, Pearson excluded), mic_e / tic are
+ * extensions.  cells (optional): 2 * mine_b200_cell_count(B) doubles per pair,
+ * the two per-orientation matrices in for_each order (debug / tests). */
+typedef struct mine_stats_out {
+  double* mic;
+  double* mas;
+  double* mev;
+  double* mcn;
+  double* mic_e;
+  double* tic;
+  double* cells;
+} mine_stats_out;
+
+/* Engine context: one per host thread (calls on one context are serialised). */
+typedef struct mine_b200_ctx mine_b200_ctx;
+
+/* Options for batch calls (zero-initialise for defaults). */
+typedef struct mine_b200_opts {
+  int device_io;     /* 1: inputs and outputs are device pointers (HBM-resident) */
+  int async;         /* 1 (with device_io): enqueue on `stream` and return */
+  void* stream;      /* cudaStream_t or NULL for the context's stream */
+  int tier;          /* 0 auto, 1 force tiny (n<=32, B<=7), 2 force general */
+  long long first;   /* first work item (pairwise/cross/list index) */
+  long long count;   /* items to score; <= 0 means all from `first` */
+} mine_b200_opts;
+
+/* ---- engine API ---------------------------------------------------------- */
+const char* mine_b200_last_error(void);
+int mine_b200_version(void);
+mine_b200_ctx* mine_b200_create(int device);
+void mine_b200_destroy(mine_b200_ctx* ctx);
+/* Grid bound B(n) = max(floor(n^alpha), 4) (char_matrix.cpp:17-20) and the
+ * number of stored shapes for it. */
+int mine_b200_grid_bound(long long n, double alpha);
+int mine_b200_cell_count(int bound);
+/* Kernel launches issued by the last batch call on this context. */
+long long mine_b200_last_launches(mine_b200_ctx* ctx);
+
+/* All pairs i < j of p variables (vars: p x n, variable-major), results in
+ * condensed PairSequence order (analysis.cpp:66-81, run_analysis
+ * all_pairs :133-191); item w of [first, first+count) goes to slot w-first. */
+int mine_b200_pairwise(mine_b200_ctx* ctx, const double* vars, int p, int n,
+                       const mine_parameter* param, const mine_b200_opts* opts,
+                       mine_stats_out* out);
+/* X (px x n) against Y (py x n), px*py results row-major.  px == 1 is the
+ * reference's master_vs_all (analysis.cpp:25-30,82-85). */
+int mine_b200_cross(mine_b200_ctx* ctx, const double* X, int px, const double* Y, int py, int n,
+                    const mine_parameter* param, const mine_b200_opts* opts,
+                    mine_stats_out* out);
+/* Explicit pairs (xi[w], yi[w]) of nvars variables (x = column variable of
+ * compute_score's first orientation). */
+int mine_b200_pairs(mine_b200_ctx* ctx, const double* vars, int nvars, int n, const int* xi,
+                    const int* yi, long long npairs, const mine_parameter* param,
+                    const mine_b200_opts* opts, mine_stats_out* out);
+
+/* Debug export of one (orientation, row target) subproblem computed by the
+ * GPU general tier -- the stage sequence of score_orientation
+ * (char_matrix.cpp:44-56): row_count (yhat), q_x[n] (row label per x-sorted
+ * position, reindex_to_first_order), raw_k (get_clumps_partition), k and
+ * bounds[k+1] (get_superclumps_partition), h_q and values[x_max-1]
+ * (optimize_x_axis).  Columns on col_var, rows on row_var. */
+int mine_b200_debug_subproblem(mine_b200_ctx* ctx, int n, const double* col_var,
+                               const double* row_var, int y_target, int x_max, int k_hat,
+                               int* row_count, int* q_x, int* raw_k, int* k, int* bounds,
+                               double* h_q, double* values);
+
+/* ---- minepy-compatible API (default context of the calling thread) -------- */
+/* NULL if valid, else a static message <-> validate_parameters (char_matrix.cpp:11-15). */
+char* mine_check_parameter(mine_parameter* param);
+/* <-> mine::compute_score (char_matrix.cpp:70-81). */
+mine_score* mine_compute_score(mine_problem* prob, mine_parameter* param);
+void mine_free_score(mine_score** score);
+/* Reductions of score->M <-> statistics.cpp:10-37 (mcn: eps = 0 is the
+ * reference's exact-equality rule, eps > 0 the minepy relaxation). */
+double mine_mic(mine_score* score);
+double mine_mas(mine_score* score);
+double mine_mev(mine_score* score);
+double mine_mcn(mine_score* score, double eps);
+double mine_mcn_general(mine_score* score);
+/* Extensions: TIC = sum of score->M (norm != 0: divided by the cell count);
+ * MIC_e = max of score->M_e. */
+double mine_tic(mine_score* score, int norm);
+double mine_mic_e(mine_score* score);
+/* minepy 1.2 batch calls; release with mine_free_pstats / mine_free_cstats. */
+mine_pstats* mine_compute_pstats(mine_matrix* X, mine_parameter* param);
+mine_cstats* mine_compute_cstats(mine_matrix* X, mine_matrix* Y, mine_parameter* param);
+void mine_free_pstats(mine_pstats** p);
+void mine_free_cstats(mine_cstats** c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MINE_B200_H */

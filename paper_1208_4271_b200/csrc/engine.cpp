@@ -1,0 +1,790 @@
+// Host runtime of the B200 MINE engine: contexts, host-built constant tables,
+// device workspaces, pair batching / streaming, and the C ABI of
+// include/mine_b200.h.  All per-pair work runs in the CUDA kernels of
+// mine_kernels.cu; this file never scores a pair on the CPU.
+//
+// Compiled with -ffp-contract=off: the p*log(p) table must round exactly like
+// the reference's `acc += p * std::log(p)` (mutual_info.hpp:24-27).
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "mine_b200.h"
+#include "mine_kernels.h"
+
+using namespace mb200;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Failure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) throw Failure(std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* ensure(size_t bytes) {
+    if (bytes > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      cap = 0;
+      const size_t want = std::max<size_t>(bytes, 256);
+      CK(cudaMalloc(&p, want));
+      cap = want;
+    }
+    return p;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  ~DevBuf() { release(); }
+};
+
+inline unsigned long long tri(unsigned long long m) { return m * (m + 1) / 2; }
+
+int grid_bound(long long n, double alpha) {  // char_matrix.cpp:17-20
+  const int b = static_cast<int>(std::floor(std::pow(static_cast<double>(n), alpha)));
+  return std::max(b, 4);
+}
+
+int cell_count(int B) {
+  int c = 0;
+  for (int y = 2; y <= B / 2; ++y) c += B / y - 1;
+  return c;
+}
+
+// Host-built constant tables, cached per (n, B) on a context.
+struct TableSet {
+  int n = -1, B = -1, ncell = 0;
+  DevBuf pl, logi, log2i, cell_off, cell_tr, cell_xy, cell_edge, cell_cmp;
+  std::vector<int> h_off;
+
+  void build(int n_, int B_, cudaStream_t s) {
+    if (n_ == n && B_ == B) return;
+    // p*log(p) for p = w/m, 1 <= w <= m <= n -- exactly the reference's term
+    // (mutual_info.hpp:24-27), with the same glibc libm.
+    const unsigned long long entries = tri((unsigned long long)n_ + 1);
+    std::vector<double> h(entries);
+    auto fill = [&](int m0, int m1) {
+      for (int m = m0; m < m1; ++m) {
+        double* row = h.data() + tri(m);
+        row[0] = 0.0;
+        for (int w = 1; w <= m; ++w) {
+          const double p = static_cast<double>(w) / static_cast<double>(m);
+          row[w] = p * std::log(p);
+        }
+      }
+    };
+    const int nthreads = n_ >= 2048 ? std::max(1u, std::min(16u, std::thread::hardware_concurrency())) : 1;
+    if (nthreads == 1) {
+      fill(0, n_ + 1);
+    } else {
+      std::vector<std::thread> th;
+      // balance by area: row m costs m
+      std::vector<int> cut(nthreads + 1, 0);
+      for (int t = 1; t < nthreads; ++t)
+        cut[t] = static_cast<int>(std::sqrt(static_cast<double>(t) / nthreads) * (n_ + 1));
+      cut[nthreads] = n_ + 1;
+      for (int t = 0; t < nthreads; ++t) th.emplace_back(fill, cut[t], cut[t + 1]);
+      for (auto& x : th) x.join();
+    }
+    CK(cudaMemcpyAsync(pl.ensure(entries * sizeof(double)), h.data(), entries * sizeof(double),
+                       cudaMemcpyHostToDevice, s));
+    std::vector<double> lg(B_ + 1), lg2(B_ + 1);
+    for (int i = 0; i <= B_; ++i) {
+      lg[i] = i ? std::log(static_cast<double>(i)) : 0.0;
+      lg2[i] = i ? std::log2(static_cast<double>(i)) : 0.0;
+    }
+    // for_each order (char_matrix.hpp:43-47) and the derived cell tables
+    h_off.assign(B_ / 2 + 2, 0);
+    int c = 0;
+    for (int y = 2; y <= B_ / 2; ++y) {
+      h_off[y] = c;
+      c += B_ / y - 1;
+    }
+    ncell = c;
+    std::vector<int> tr(c), xy(c);
+    std::vector<uint8_t> edge(c);
+    std::vector<int8_t> cmp(c);
+    int i = 0;
+    for (int y = 2; y <= B_ / 2; ++y)
+      for (int x = 2; x <= B_ / y; ++x, ++i) {
+        tr[i] = h_off[x] + (y - 2);
+        xy[i] = x * y;
+        edge[i] = (x == 2 || y == 2);
+        cmp[i] = x < y ? -1 : (x > y ? 1 : 0);
+      }
+    CK(cudaMemcpyAsync(logi.ensure(lg.size() * 8), lg.data(), lg.size() * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(log2i.ensure(lg2.size() * 8), lg2.data(), lg2.size() * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(cell_off.ensure(h_off.size() * 4), h_off.data(), h_off.size() * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(cell_tr.ensure(std::max(c, 1) * 4), tr.data(), c * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(cell_xy.ensure(std::max(c, 1) * 4), xy.data(), c * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(cell_edge.ensure(std::max(c, 1)), edge.data(), c, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(cell_cmp.ensure(std::max(c, 1)), cmp.data(), c, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));  // host vectors go out of scope
+    n = n_;
+    B = B_;
+  }
+
+  Tables view() const {
+    Tables t;
+    t.pl = pl.as<double>();
+    t.logi = logi.as<double>();
+    t.log2i = log2i.as<double>();
+    t.cell_off = cell_off.as<int>();
+    t.cell_tr = cell_tr.as<int>();
+    t.cell_xy = cell_xy.as<int>();
+    t.cell_edge = cell_edge.as<uint8_t>();
+    t.cell_cmp = cell_cmp.as<int8_t>();
+    t.n = n;
+    t.B = B;
+    t.ncell = ncell;
+    return t;
+  }
+};
+
+}  // namespace
+
+struct mine_b200_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;  // compute
+  cudaStream_t copy = nullptr;    // result drain
+  std::mutex mu;
+  TableSet tables;
+  DevBuf vals, perm, runid, runstart, nruns, q, yhat, hq, lw, rsmask;
+  DevBuf ocells, fscratch, stats, flag, idx;
+  std::vector<cudaEvent_t> events;
+  long long launches = 0;
+};
+
+namespace {
+
+struct Call {
+  int kind;                 // PairKind
+  const double* a;          // pairwise / list: all variables; cross: X
+  const double* b;          // cross: Y
+  int va, vb;               // variable counts (cross: px, py; others: p, 0)
+  int n;
+  const int* xi;
+  const int* yi;
+  long long total;          // size of the pair space
+};
+
+void validate_param(const mine_parameter* par) {  // char_matrix.cpp:11-15
+  if (!par) throw Failure("parameters: null");
+  if (!(par->alpha > 0.0) || par->alpha > 1.0) throw Failure("parameters: alpha must be in (0, 1]");
+  if (!(par->c > 0.0)) throw Failure("parameters: c must be > 0");
+  if (par->est != MINE_EST_MIC_APPROX && par->est != MINE_EST_MIC_E)
+    throw Failure("parameters: est must be MINE_EST_MIC_APPROX or MINE_EST_MIC_E");
+}
+
+cudaEvent_t ctx_event(mine_b200_ctx* ctx, size_t i) {
+  while (ctx->events.size() <= i) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->events.push_back(e);
+  }
+  return ctx->events[i];
+}
+
+// Runs one batch call.  Everything from the input upload to the statistic
+// drain is enqueued on the context streams; host work is limited to tables
+// (cached) and launch bookkeeping.
+void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
+              const mine_b200_opts* opts_in, mine_stats_out* out) {
+  validate_param(par);
+  mine_b200_opts opts{};
+  if (opts_in) opts = *opts_in;
+  const int n = call.n;
+  if (n < 2) throw Failure("compute_score: need at least 2 samples");
+  if (n > 65535) throw Failure("mine_b200: n > 65535 samples is not supported");
+  if (!out) throw Failure("mine_b200: null output");
+  const long long first = opts.first;
+  if (first < 0 || first > call.total) throw Failure("expand_pairs: first index out of range");
+  long long count = opts.count > 0 ? opts.count : call.total - first;
+  if (first + count > call.total) throw Failure("expand_pairs: pair range out of range");
+  ctx->launches = 0;
+  if (count == 0) return;
+
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = opts.stream ? static_cast<cudaStream_t>(opts.stream) : ctx->stream;
+  const bool dio = opts.device_io != 0;
+  const int B = grid_bound(n, par->alpha);
+  const int ny = B / 2 - 1;
+  const bool tiny_ok = n <= 32 && B <= 7;
+  bool tiny = tiny_ok && opts.tier != 2;
+  if (opts.tier == 1 && !tiny_ok) throw Failure("mine_b200: tiny tier needs n <= 32 and B <= 7");
+
+  ctx->tables.build(n, B, s);
+  const Tables tb = ctx->tables.view();
+  const int ncell = tb.ncell;
+
+  // ---- variables -> device
+  const int V = call.va + call.vb;
+  const size_t vbytes = sizeof(double) * (size_t)V * n;
+  const double* dvals;
+  if (dio && call.kind != kCross) {
+    dvals = call.a;
+  } else {
+    double* d = ctx->vals.as<double>();
+    d = static_cast<double*>(ctx->vals.ensure(vbytes));
+    const cudaMemcpyKind kind = dio ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CK(cudaMemcpyAsync(d, call.a, sizeof(double) * (size_t)call.va * n, kind, s));
+    if (call.kind == kCross)
+      CK(cudaMemcpyAsync(d + (size_t)call.va * n, call.b, sizeof(double) * (size_t)call.vb * n, kind, s));
+    dvals = d;
+  }
+  int* flag = static_cast<int*>(ctx->flag.ensure(sizeof(int)));
+  CK(cudaMemsetAsync(flag, 0, sizeof(int), s));
+  launch_check_finite(dvals, (long long)V * n, flag, s);
+  ++ctx->launches;
+
+  VarSet vs;
+  vs.vals = dvals;
+  vs.V = V;
+  vs.n = n;
+  vs.ny = ny;
+  vs.perm = static_cast<int*>(ctx->perm.ensure(sizeof(int) * (size_t)V * n));
+  vs.runid = static_cast<int*>(ctx->runid.ensure(sizeof(int) * (size_t)V * n));
+  vs.runstart = static_cast<int*>(ctx->runstart.ensure(sizeof(int) * (size_t)V * (n + 1)));
+  vs.nruns = static_cast<int*>(ctx->nruns.ensure(sizeof(int) * (size_t)V));
+  vs.q = static_cast<uint16_t*>(ctx->q.ensure(sizeof(uint16_t) * (size_t)V * ny * n));
+  vs.yhat = static_cast<int*>(ctx->yhat.ensure(sizeof(int) * (size_t)V * ny));
+  vs.hq = static_cast<double*>(ctx->hq.ensure(sizeof(double) * (size_t)V * ny));
+  launch_sort_vars(vs, s);
+  launch_equipartition(vs, tb, s);
+  ctx->launches += 2;
+  if (tiny) {
+    vs.lw = static_cast<uint8_t*>(ctx->lw.ensure((size_t)V * n));
+    vs.rsmask = static_cast<uint32_t*>(ctx->rsmask.ensure(sizeof(uint32_t) * V));
+    launch_pack_tiny(vs, s);
+    ++ctx->launches;
+  }
+
+  // ---- pair space
+  PairSpace ps;
+  ps.kind = call.kind;
+  ps.p = call.va;
+  ps.px = call.va;
+  ps.py = call.vb;
+  if (call.kind == kList) {
+    if (dio) {
+      ps.xi = call.xi;
+      ps.yi = call.yi;
+    } else {
+      for (long long w = first; w < first + count; ++w)
+        if (call.xi[w] < 0 || call.xi[w] >= V || call.yi[w] < 0 || call.yi[w] >= V)
+          throw Failure("expand_pairs: pair index out of range");
+      int* d = static_cast<int*>(ctx->idx.ensure(sizeof(int) * 2 * (size_t)call.total));
+      CK(cudaMemcpyAsync(d, call.xi, sizeof(int) * call.total, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(d + call.total, call.yi, sizeof(int) * call.total, cudaMemcpyHostToDevice, s));
+      ps.xi = d;
+      ps.yi = d + call.total;
+    }
+  }
+
+  // ---- outputs: device-resident, or a device staging area drained by the
+  // copy stream chunk by chunk while the next chunk computes.
+  double* const user_stat[6] = {out->mic, out->mas, out->mev, out->mcn, out->mic_e, out->tic};
+  const long long chunk = tiny ? std::min<long long>(count, 1LL << 20)
+                               : std::max<long long>(1, std::min<long long>(
+                                     count, (256LL << 20) / (16LL * ncell)));
+  const long long nchunks = (count + chunk - 1) / chunk;
+  const int nslots = dio ? 1 : 2;  // double-buffered staging for host io
+  double* stage = nullptr;
+  const size_t stage_stats = 6 * (size_t)chunk;
+  const size_t stage_cells = out->cells ? 2 * (size_t)ncell * chunk : 0;
+  if (!dio) stage = static_cast<double*>(ctx->stats.ensure(sizeof(double) * nslots * (stage_stats + stage_cells)));
+  double* ocells = nullptr;
+  if (!tiny) ocells = static_cast<double*>(ctx->ocells.ensure(sizeof(double) * 2 * (size_t)ncell * chunk));
+
+  std::vector<YParams> yps;
+  for (int y = 2; y <= B / 2; ++y) {
+    YParams yp;
+    yp.y = y;
+    yp.yi = y - 2;
+    yp.x_max = B / y;
+    yp.k_hat = std::max(1, static_cast<int>(std::floor(par->c * static_cast<double>(yp.x_max))));
+    yps.push_back(yp);
+  }
+  if (!tiny) {
+    for (const auto& yp : yps)
+      if (general_smem_bytes(n, yp, false) > 227 * 1024)
+        throw Failure("mine_b200: general tier shared-memory plan exceeds 227 KB for n=" +
+                      std::to_string(n) + " y=" + std::to_string(yp.y));
+  }
+
+  for (long long ci = 0; ci < nchunks; ++ci) {
+    const long long c0 = ci * chunk;
+    const long long cn = std::min(chunk, count - c0);
+    const int slot = (int)(ci % nslots);
+    StatsOut so;
+    double* cells_dst = nullptr;
+    if (dio) {
+      so.mic = user_stat[0] ? user_stat[0] + c0 : nullptr;
+      so.mas = user_stat[1] ? user_stat[1] + c0 : nullptr;
+      so.mev = user_stat[2] ? user_stat[2] + c0 : nullptr;
+      so.mcn = user_stat[3] ? user_stat[3] + c0 : nullptr;
+      so.mic_e = user_stat[4] ? user_stat[4] + c0 : nullptr;
+      so.tic = user_stat[5] ? user_stat[5] + c0 : nullptr;
+      cells_dst = out->cells ? out->cells + (size_t)c0 * 2 * ncell : nullptr;
+    } else {
+      double* base = stage + (size_t)slot * (stage_stats + stage_cells);
+      if (ci >= nslots) CK(cudaStreamWaitEvent(s, ctx_event(ctx, 2 * slot + 1), 0));  // slot drained
+      double** so_p[6] = {&so.mic, &so.mas, &so.mev, &so.mcn, &so.mic_e, &so.tic};
+      for (int k = 0; k < 6; ++k) *so_p[k] = user_stat[k] ? base + (size_t)k * chunk : nullptr;
+      cells_dst = out->cells ? base + stage_stats : nullptr;
+    }
+    PairSpace pc = ps;
+    pc.first = first + c0;
+    pc.count = cn;
+    if (tiny) {
+      launch_tiny_pairs(vs, tb, pc, par->c, par->est, so, cells_dst, s);
+      ++ctx->launches;
+    } else {
+      for (const auto& yp : yps) {
+        if (general_f_fits(n, yp)) {
+          launch_general(vs, tb, pc, 0, cn, yp, ocells, nullptr, nullptr, -1, s);
+          ++ctx->launches;
+        } else {
+          // F table in global scratch: bound the CTAs per launch.
+          const size_t per_cta = sizeof(double) * (size_t)(std::min(n, yp.k_hat) + 1) * (yp.x_max - 1);
+          const long long max_ctas = std::max<long long>(2, (1LL << 30) / (long long)per_cta);
+          const long long step = std::max<long long>(1, max_ctas / 2);
+          double* fs = static_cast<double*>(ctx->fscratch.ensure(per_cta * 2 * step));
+          for (long long b0 = 0; b0 < cn; b0 += step) {
+            launch_general(vs, tb, pc, b0, std::min(step, cn - b0), yp, ocells + 0, fs, nullptr, -1, s);
+            ++ctx->launches;
+          }
+        }
+      }
+      launch_reduce(tb, cn, ocells, par->est, so, 0, s);
+      ++ctx->launches;
+      if (cells_dst)
+        CK(cudaMemcpyAsync(cells_dst, ocells, sizeof(double) * 2 * ncell * cn, cudaMemcpyDeviceToDevice, s));
+    }
+    CK(cudaGetLastError());
+    if (!dio) {
+      // drain this chunk on the copy stream
+      CK(cudaEventRecord(ctx_event(ctx, 2 * slot), s));
+      CK(cudaStreamWaitEvent(ctx->copy, ctx_event(ctx, 2 * slot), 0));
+      const double* base = stage + (size_t)slot * (stage_stats + stage_cells);
+      for (int k = 0; k < 6; ++k)
+        if (user_stat[k])
+          CK(cudaMemcpyAsync(user_stat[k] + c0, base + (size_t)k * chunk, sizeof(double) * cn,
+                             cudaMemcpyDeviceToHost, ctx->copy));
+      if (out->cells)
+        CK(cudaMemcpyAsync(out->cells + (size_t)c0 * 2 * ncell, base + stage_stats,
+                           sizeof(double) * 2 * ncell * cn, cudaMemcpyDeviceToHost, ctx->copy));
+      CK(cudaEventRecord(ctx_event(ctx, 2 * slot + 1), ctx->copy));
+    }
+  }
+  if (dio && opts.async) return;
+  if (!dio) CK(cudaStreamSynchronize(ctx->copy));
+  CK(cudaStreamSynchronize(s));
+  int h_flag = 0;
+  CK(cudaMemcpy(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h_flag) throw Failure("compute_score: inputs must be finite");
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+mine_b200_ctx* default_ctx() {
+  thread_local std::unique_ptr<mine_b200_ctx, void (*)(mine_b200_ctx*)> ctx(nullptr, mine_b200_destroy);
+  if (!ctx) {
+    const char* env = std::getenv("MINE_B200_DEVICE");
+    mine_b200_ctx* c = mine_b200_create(env ? std::atoi(env) : 0);
+    if (!c) throw Failure(g_err);
+    ctx.reset(c);
+  }
+  return ctx.get();
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* mine_b200_last_error(void) { return g_err.c_str(); }
+int mine_b200_version(void) { return MINE_B200_VERSION; }
+int mine_b200_grid_bound(long long n, double alpha) { return grid_bound(n, alpha); }
+int mine_b200_cell_count(int bound) { return cell_count(bound); }
+long long mine_b200_last_launches(mine_b200_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+mine_b200_ctx* mine_b200_create(int device) {
+  mine_b200_ctx* ctx = nullptr;
+  const int rc = guarded([&] {
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw Failure("mine_b200: no such CUDA device");
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) throw Failure("mine_b200: needs an sm_100 (Blackwell) GPU");
+    CK(cudaSetDevice(device));
+    std::unique_ptr<mine_b200_ctx> c(new mine_b200_ctx());
+    c->device = device;
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    ctx = c.release();
+  });
+  return rc ? nullptr : ctx;
+}
+
+void mine_b200_destroy(mine_b200_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  for (auto e : ctx->events) cudaEventDestroy(e);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->copy) cudaStreamDestroy(ctx->copy);
+  delete ctx;
+}
+
+int mine_b200_pairwise(mine_b200_ctx* ctx, const double* vars, int p, int n,
+                       const mine_parameter* param, const mine_b200_opts* opts,
+                       mine_stats_out* out) {
+  return guarded([&] {
+    if (!ctx) throw Failure("mine_b200: null context");
+    if (p < 0) throw Failure("mine_b200: negative variable count");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    Call call{kPairwise, vars, nullptr, p, 0, n, nullptr, nullptr, (long long)p * (p - 1) / 2};
+    if (p < 2) call.total = 0;
+    run_call(ctx, call, param, opts, out);
+  });
+}
+
+int mine_b200_cross(mine_b200_ctx* ctx, const double* X, int px, const double* Y, int py, int n,
+                    const mine_parameter* param, const mine_b200_opts* opts,
+                    mine_stats_out* out) {
+  return guarded([&] {
+    if (!ctx) throw Failure("mine_b200: null context");
+    if (px < 0 || py < 0) throw Failure("mine_b200: negative variable count");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    Call call{kCross, X, Y, px, py, n, nullptr, nullptr, (long long)px * py};
+    run_call(ctx, call, param, opts, out);
+  });
+}
+
+int mine_b200_pairs(mine_b200_ctx* ctx, const double* vars, int nvars, int n, const int* xi,
+                    const int* yi, long long npairs, const mine_parameter* param,
+                    const mine_b200_opts* opts, mine_stats_out* out) {
+  return guarded([&] {
+    if (!ctx) throw Failure("mine_b200: null context");
+    if (npairs < 0 || nvars < 0) throw Failure("mine_b200: negative size");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    Call call{kList, vars, nullptr, nvars, 0, n, xi, yi, npairs};
+    run_call(ctx, call, param, opts, out);
+  });
+}
+
+int mine_b200_debug_subproblem(mine_b200_ctx* ctx, int n, const double* col_var,
+                               const double* row_var, int y_target, int x_max, int k_hat,
+                               int* row_count, int* q_x, int* raw_k, int* k, int* bounds,
+                               double* h_q, double* values) {
+  return guarded([&] {
+    if (!ctx) throw Failure("mine_b200: null context");
+    if (n < 2) throw Failure("equipartition_y_axis: need at least 2 points");
+    if (y_target < 2) throw Failure("equipartition_y_axis: row target must be >= 2");
+    if (k_hat < 1) throw Failure("get_superclumps_partition: clump budget must be >= 1");
+    if (x_max < 2) throw Failure("optimize_x_axis: column target must be >= 2");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const int B = x_max * y_target;  // admits (x_max, y_target) and rows up to y_target
+    ctx->tables.build(n, B, s);
+    const Tables tb = ctx->tables.view();
+    VarSet vs;
+    vs.V = 2;
+    vs.n = n;
+    vs.ny = B / 2 - 1;
+    double* d = static_cast<double*>(ctx->vals.ensure(sizeof(double) * 2 * n));
+    CK(cudaMemcpyAsync(d, col_var, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d + n, row_var, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    vs.vals = d;
+    vs.perm = static_cast<int*>(ctx->perm.ensure(sizeof(int) * 2 * n));
+    vs.runid = static_cast<int*>(ctx->runid.ensure(sizeof(int) * 2 * n));
+    vs.runstart = static_cast<int*>(ctx->runstart.ensure(sizeof(int) * 2 * (n + 1)));
+    vs.nruns = static_cast<int*>(ctx->nruns.ensure(sizeof(int) * 2));
+    vs.q = static_cast<uint16_t*>(ctx->q.ensure(sizeof(uint16_t) * 2 * vs.ny * n));
+    vs.yhat = static_cast<int*>(ctx->yhat.ensure(sizeof(int) * 2 * vs.ny));
+    vs.hq = static_cast<double*>(ctx->hq.ensure(sizeof(double) * 2 * vs.ny));
+    launch_sort_vars(vs, s);
+    launch_equipartition(vs, tb, s);
+    int hidx[2] = {0, 1};
+    int* didx = static_cast<int*>(ctx->idx.ensure(sizeof(int) * 2));
+    CK(cudaMemcpyAsync(didx, hidx, sizeof(hidx), cudaMemcpyHostToDevice, s));
+    PairSpace ps;
+    ps.kind = kList;
+    ps.first = 0;
+    ps.count = 1;
+    ps.xi = didx;
+    ps.yi = didx + 1;
+    YParams yp{y_target, y_target - 2, x_max, k_hat};
+    if (general_smem_bytes(n, yp, false) > 227 * 1024)
+      throw Failure("mine_b200: subproblem too large for the general tier");
+    // debug outputs in one device block
+    const size_t ints = 3 + (size_t)n + (n + 1);
+    const size_t bytes = sizeof(double) * (1 + x_max) + sizeof(int) * ints;
+    char* dd = static_cast<char*>(ctx->stats.ensure(bytes));
+    SubDebug dbg;
+    dbg.h_q = reinterpret_cast<double*>(dd);
+    dbg.values = dbg.h_q + 1;
+    int* ib = reinterpret_cast<int*>(dbg.values + x_max);
+    dbg.row_count = ib;
+    dbg.raw_k = ib + 1;
+    dbg.k = ib + 2;
+    dbg.q_x = ib + 3;
+    dbg.bounds = ib + 3 + n;
+    double* oc = static_cast<double*>(ctx->ocells.ensure(sizeof(double) * 2 * tb.ncell));
+    double* fs = nullptr;
+    if (!general_f_fits(n, yp))
+      fs = static_cast<double*>(ctx->fscratch.ensure(sizeof(double) * (size_t)(std::min(n, k_hat) + 1) * (x_max - 1)));
+    launch_general(vs, tb, ps, 0, 1, yp, oc, fs, &dbg, 0, s);
+    CK(cudaGetLastError());
+    std::vector<char> h(bytes);
+    CK(cudaMemcpyAsync(h.data(), dd, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const double* hd = reinterpret_cast<const double*>(h.data());
+    const int* hi = reinterpret_cast<const int*>(hd + 1 + x_max);
+    *h_q = hd[0];
+    for (int l = 0; l < x_max - 1; ++l) values[l] = hd[1 + l];
+    *row_count = hi[0];
+    *raw_k = hi[1];
+    *k = hi[2];
+    for (int i = 0; i < n; ++i) q_x[i] = hi[3 + i];
+    for (int j = 0; j <= hi[2]; ++j) bounds[j] = hi[3 + n + j];
+  });
+}
+
+// ---- minepy-compatible API -------------------------------------------------
+char* mine_check_parameter(mine_parameter* param) {
+  static char bad_alpha[] = "alpha must be in (0, 1]";
+  static char bad_c[] = "c must be > 0";
+  static char bad_est[] = "est must be MINE_EST_MIC_APPROX or MINE_EST_MIC_E";
+  if (!param || !(param->alpha > 0.0) || param->alpha > 1.0) return bad_alpha;
+  if (!(param->c > 0.0)) return bad_c;
+  if (param->est != MINE_EST_MIC_APPROX && param->est != MINE_EST_MIC_E) return bad_est;
+  return nullptr;
+}
+
+mine_score* mine_compute_score(mine_problem* prob, mine_parameter* param) {
+  mine_score* score = nullptr;
+  const int rc = guarded([&] {
+    if (!prob || !prob->x || !prob->y) throw Failure("compute_score: null problem");
+    validate_param(param);
+    const int n = prob->n;
+    if (n < 2) throw Failure("compute_score: need at least 2 samples");
+    const int B = grid_bound(n, param->alpha);
+    const int nc = cell_count(B);
+    std::vector<double> vars(2 * (size_t)n), cells(2 * (size_t)nc);
+    std::memcpy(vars.data(), prob->x, sizeof(double) * n);
+    std::memcpy(vars.data() + n, prob->y, sizeof(double) * n);
+    int xi = 0, yi = 1;
+    mine_stats_out out{};
+    double dummy = 0;
+    out.mic = &dummy;
+    out.cells = cells.data();
+    mine_b200_ctx* ctx = default_ctx();
+    {
+      std::lock_guard<std::mutex> lk(ctx->mu);
+      Call call{kList, vars.data(), nullptr, 2, 0, n, &xi, &yi, 1};
+      run_call(ctx, call, param, nullptr, &out);
+    }
+    score = static_cast<mine_score*>(std::calloc(1, sizeof(mine_score)));
+    score->n = B / 2 - 1;
+    score->B = B;
+    score->est = param->est;
+    score->m = static_cast<int*>(std::malloc(sizeof(int) * std::max(score->n, 1)));
+    double** ma = static_cast<double**>(std::malloc(sizeof(double*) * std::max(score->n, 1)));
+    double** me = static_cast<double**>(std::malloc(sizeof(double*) * std::max(score->n, 1)));
+    int c = 0;
+    for (int i = 0; i < score->n; ++i) {
+      const int y = i + 2;
+      score->m[i] = B / y - 1;
+      ma[i] = static_cast<double*>(std::malloc(sizeof(double) * score->m[i]));
+      me[i] = static_cast<double*>(std::malloc(sizeof(double) * score->m[i]));
+      for (int j = 0; j < score->m[i]; ++j, ++c) {
+        const int x = j + 2;
+        const double a = cells[c], b = cells[nc + c];
+        const double m = b > a ? b : a;  // update_max of orientation 2 over 1
+        ma[i][j] = m;
+        me[i][j] = x < y ? a : (x > y ? b : m);
+      }
+    }
+    score->M = param->est == MINE_EST_MIC_E ? me : ma;
+    score->M_e = me;
+    if (param->est == MINE_EST_MIC_E) {
+      for (int i = 0; i < score->n; ++i) std::free(ma[i]);
+      std::free(ma);
+    }
+  });
+  return rc ? nullptr : score;
+}
+
+void mine_free_score(mine_score** score) {
+  if (!score || !*score) return;
+  mine_score* s = *score;
+  const bool shared = s->M == s->M_e;
+  for (int i = 0; i < s->n; ++i) {
+    if (!shared) std::free(s->M[i]);
+    std::free(s->M_e[i]);
+  }
+  if (!shared) std::free(s->M);
+  std::free(s->M_e);
+  std::free(s->m);
+  std::free(s);
+  *score = nullptr;
+}
+
+static double score_max(double** M, const mine_score* s) {
+  double best = 0.0;
+  for (int i = 0; i < s->n; ++i)
+    for (int j = 0; j < s->m[i]; ++j) best = best < M[i][j] ? M[i][j] : best;
+  return best;
+}
+
+double mine_mic(mine_score* s) { return s ? score_max(s->M, s) : NAN; }
+double mine_mic_e(mine_score* s) { return s ? score_max(s->M_e, s) : NAN; }
+
+double mine_mas(mine_score* s) {  // statistics.cpp:16-20
+  if (!s) return NAN;
+  double best = 0.0;
+  for (int i = 0; i < s->n; ++i)
+    for (int j = 0; j < s->m[i]; ++j) {
+      const int x = j + 2, y = i + 2;  // M(y, x) lives in row x-2, column y-2
+      const double d = std::fabs(s->M[i][j] - s->M[x - 2][y - 2]);
+      best = best < d ? d : best;
+    }
+  return best;
+}
+
+double mine_mev(mine_score* s) {  // statistics.cpp:22-28
+  if (!s) return NAN;
+  double best = 0.0;
+  for (int i = 0; i < s->n; ++i)
+    for (int j = 0; j < s->m[i]; ++j)
+      if (i == 0 || j == 0) best = best < s->M[i][j] ? s->M[i][j] : best;
+  return best;
+}
+
+double mine_mcn(mine_score* s, double eps) {  // statistics.cpp:30-37 (eps = 0)
+  if (!s) return NAN;
+  const double top = mine_mic(s);
+  long best = LONG_MAX;
+  for (int i = 0; i < s->n; ++i)
+    for (int j = 0; j < s->m[i]; ++j) {
+      const bool hit = eps == 0.0 ? s->M[i][j] == top : s->M[i][j] >= (1.0 - eps) * top;
+      if (hit) best = std::min(best, static_cast<long>(i + 2) * (j + 2));
+    }
+  return std::log2(static_cast<double>(best));
+}
+
+double mine_mcn_general(mine_score* s) { return s ? mine_mcn(s, 1.0 - mine_mic(s)) : NAN; }
+
+double mine_tic(mine_score* s, int norm) {
+  if (!s) return NAN;
+  double tic = 0.0;
+  long cnt = 0;
+  for (int i = 0; i < s->n; ++i)
+    for (int j = 0; j < s->m[i]; ++j, ++cnt) tic += s->M[i][j];
+  return norm ? tic / static_cast<double>(cnt) : tic;
+}
+
+mine_pstats* mine_compute_pstats(mine_matrix* X, mine_parameter* param) {
+  mine_pstats* ps = nullptr;
+  const int rc = guarded([&] {
+    if (!X || !X->data) throw Failure("mine_compute_pstats: null matrix");
+    const long long total = X->n >= 2 ? (long long)X->n * (X->n - 1) / 2 : 0;
+    std::unique_ptr<mine_pstats, void (*)(mine_pstats*)> r(
+        static_cast<mine_pstats*>(std::calloc(1, sizeof(mine_pstats))),
+        [](mine_pstats* p) { mine_free_pstats(&p); });
+    r->n = total;
+    r->mic = static_cast<double*>(std::malloc(sizeof(double) * std::max<long long>(total, 1)));
+    r->tic = static_cast<double*>(std::malloc(sizeof(double) * std::max<long long>(total, 1)));
+    mine_stats_out out{};
+    out.mic = r->mic;
+    out.tic = r->tic;
+    mine_b200_ctx* ctx = default_ctx();
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    Call call{kPairwise, X->data, nullptr, X->n, 0, X->m, nullptr, nullptr, total};
+    run_call(ctx, call, param, nullptr, &out);
+    ps = r.release();
+  });
+  return rc ? nullptr : ps;
+}
+
+mine_cstats* mine_compute_cstats(mine_matrix* X, mine_matrix* Y, mine_parameter* param) {
+  mine_cstats* cs = nullptr;
+  const int rc = guarded([&] {
+    if (!X || !Y || !X->data || !Y->data) throw Failure("mine_compute_cstats: null matrix");
+    if (X->m != Y->m) throw Failure("compute_score: input lengths differ");
+    const long long total = (long long)X->n * Y->n;
+    std::unique_ptr<mine_cstats, void (*)(mine_cstats*)> r(
+        static_cast<mine_cstats*>(std::calloc(1, sizeof(mine_cstats))),
+        [](mine_cstats* p) { mine_free_cstats(&p); });
+    r->n = X->n;
+    r->m = Y->n;
+    r->mic = static_cast<double*>(std::malloc(sizeof(double) * std::max<long long>(total, 1)));
+    r->tic = static_cast<double*>(std::malloc(sizeof(double) * std::max<long long>(total, 1)));
+    mine_stats_out out{};
+    out.mic = r->mic;
+    out.tic = r->tic;
+    mine_b200_ctx* ctx = default_ctx();
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    Call call{kCross, X->data, Y->data, X->n, Y->n, X->m, nullptr, nullptr, total};
+    run_call(ctx, call, param, nullptr, &out);
+    cs = r.release();
+  });
+  return rc ? nullptr : cs;
+}
+
+void mine_free_pstats(mine_pstats** p) {
+  if (!p || !*p) return;
+  std::free((*p)->mic);
+  std::free((*p)->tic);
+  std::free(*p);
+  *p = nullptr;
+}
+
+void mine_free_cstats(mine_cstats** c) {
+  if (!c || !*c) return;
+  std::free((*c)->mic);
+  std::free((*c)->tic);
+  std::free(*c);
+  *c = nullptr;
+}
+
+}  // extern "C"

@@ -1,0 +1,802 @@
+// B200 (sm_100a) kernels of the MINE score engine.
+//
+// Compiled with -fmad=false: the reference's x86-64 build never contracts
+// a*b+c into an FMA, and every FP64 op below must round exactly like it does
+// (SURVEY App. B).  Division uses IEEE __ddiv_rn (CUDA's default for double).
+// All logarithms come from host-built glibc tables (Tables), so entropies are
+// bit-identical to mutual_info.hpp:16-52.
+//
+// Pipeline of one call:
+//   K1 k_sort_vars      per variable: stable rank, tie-run structure       (partition.cpp:13-38)
+//   K2 k_equipartition  per (variable, y): greedy row map Q, yhat, H(Q)      (partition.cpp:42-67, A1)
+//   tiny tier  k_tiny_pairs   n <= 32, B <= 7: one thread per pair, all stages in registers
+//   general    k_general      one CTA per (pair, orientation) at one y:
+//                               clumps/superclumps/cell counts (partition.cpp:108-165,
+//                               mutual_info.cpp:9-24) + t-outer exact DP (mutual_info.cpp:26-72)
+//              k_reduce       per pair: max-merge + MIC/MAS/MEV/MCN/MIC_e/TIC (statistics.cpp:10-37)
+#include <cfloat>
+#include <cstdint>
+
+#include "mine_kernels.h"
+
+namespace mb200 {
+
+namespace {
+
+constexpr double kLowest = -DBL_MAX;  // std::numeric_limits<double>::lowest()
+
+__device__ __forceinline__ unsigned tri(unsigned m) { return m * (m + 1u) / 2u; }
+
+// std::max / std::min argument order (libstdc++): max(a,b) = a < b ? b : a.
+__device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }
+__device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = dmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_min_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_incl_scan(int v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  return v;
+}
+
+// In-place inclusive scan of a[0..n) in shared memory; each thread owns a
+// contiguous chunk.  tmp: >= 33 ints of shared scratch.  Returns the total.
+__device__ int block_incl_scan(int* a, int n, int* tmp) {
+  const int nt = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = (nt + 31) >> 5;
+  const int per = (n + nt - 1) / nt;
+  const int beg = min(tid * per, n), end = min(beg + per, n);
+  int s = 0;
+  for (int i = beg; i < end; ++i) s += a[i];
+  const int incl = warp_incl_scan(s);
+  if (lane == 31) tmp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int x = lane < nw ? tmp[lane] : 0;
+    x = warp_incl_scan(x);
+    if (lane < nw) tmp[lane] = x;
+  }
+  __syncthreads();
+  int run = incl - s + (warp ? tmp[warp - 1] : 0);
+  for (int i = beg; i < end; ++i) {
+    run += a[i];
+    a[i] = run;
+  }
+  const int total = tmp[nw - 1];
+  __syncthreads();
+  return total;
+}
+
+// PairSequence::at (analysis.cpp:66-81), 0-based.
+__device__ void pair_at(long long p, long long w, int& i, int& j) {
+  const long long total = p * (p - 1) / 2;
+  const long long r = total - w;
+  long long m = (long long)((sqrt(8.0 * (double)r + 1.0) - 1.0) / 2.0);
+  while (m * (m + 1) / 2 < r) ++m;
+  while (m >= 1 && (m - 1) * m / 2 >= r) --m;
+  const long long ii = p - m;
+  const long long row_start = total - m * (m + 1) / 2;
+  i = (int)(ii - 1);
+  j = (int)(ii + (w - row_start));
+}
+
+// Variables (x, y) of work item w: x is the column variable of orientation 0.
+__device__ __forceinline__ void pair_vars(const PairSpace& ps, long long w, int& vx, int& vy) {
+  if (ps.kind == kPairwise) {
+    pair_at(ps.p, w, vx, vy);
+  } else if (ps.kind == kCross) {
+    vx = (int)(w / ps.py);
+    vy = ps.px + (int)(w % ps.py);
+  } else {
+    vx = ps.xi[w];
+    vy = ps.yi[w];
+  }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_check_finite(const double* __restrict__ v, long long count, int* flag) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x)
+    if (!isfinite(v[i])) *flag = 1;
+}
+
+// K1: per-variable stable ranking (CTA per variable).  pos = #smaller +
+// #equal-with-lower-index gives the stable sorted position; tie runs are the
+// groups of equal values (C++ ==, so -0.0 and +0.0 share a run,
+// partition.cpp:20,24,52,124).  The order inside a tie run is irrelevant to
+// every result, so a per-variable sort replaces the reference's
+// four per-pair stable sorts.
+__global__ void k_sort_vars(VarSet vs) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = vs.n;
+  double* v = reinterpret_cast<double*>(smem);
+  int* rs = reinterpret_cast<int*>(v + n);
+  int* tmp = rs + n;
+  const int var = blockIdx.x;
+  const double* src = vs.vals + (size_t)var * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) v[i] = src[i];
+  __syncthreads();
+  int* perm = vs.perm + (size_t)var * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double a = v[i];
+    int less = 0, eqb = 0;
+    for (int j = 0; j < n; ++j) {
+      const double b = v[j];
+      less += b < a;
+      eqb += (b == a) & (j < i);
+    }
+    perm[less + eqb] = i;
+    rs[less + eqb] = eqb == 0;
+  }
+  __syncthreads();
+  const int runs = block_incl_scan(rs, n, tmp);
+  int* runid = vs.runid + (size_t)var * n;
+  int* rstart = vs.runstart + (size_t)var * (n + 1);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int r = rs[i] - 1;
+    runid[i] = r;
+    if (i == 0 || rs[i - 1] != rs[i]) rstart[r] = i;
+  }
+  if (threadIdx.x == 0) {
+    rstart[runs] = n;
+    vs.nruns[var] = runs;
+  }
+}
+
+// K2: EquipartitionYAxis per (variable, y) -- one thread runs the greedy scan
+// of equipartition_runs (partition.cpp:42-67) over the variable's tie runs.
+// The row map depends only on the row variable, so it is computed
+// once per variable instead of twice per pair.  H(Q) is accumulated with the
+// reference's sequential p*log(p) over rows (mutual_info.cpp:33).
+__global__ void k_equipartition(VarSet vs, Tables tb) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)vs.V * vs.ny) return;
+  const int var = (int)(idx / vs.ny), yi = (int)(idx % vs.ny), y = yi + 2, n = vs.n;
+  const int* rs = vs.runstart + (size_t)var * (n + 1);
+  const int* perm = vs.perm + (size_t)var * n;
+  const int runs = vs.nruns[var];
+  uint16_t* q = vs.q + ((size_t)var * vs.ny + yi) * n;
+  const double* pln = tb.pl + tri(n);
+  double desired = (double)n / (double)y;
+  int curr = 1, in_row = 0;
+  double acc = 0.0;
+  for (int r = 0; r < runs; ++r) {
+    const int i = rs[r], j = rs[r + 1], run = j - i;
+    if (in_row != 0 && fabs((double)(in_row + run) - desired) >= fabs((double)in_row - desired)) {
+      acc = __dadd_rn(acc, pln[in_row]);
+      ++curr;
+      in_row = 0;
+      desired = (double)(n - i) / (double)(y - curr + 1);
+    }
+    for (int t = i; t < j; ++t) q[perm[t]] = (uint16_t)curr;
+    in_row += run;
+  }
+  acc = __dadd_rn(acc, pln[in_row]);
+  vs.yhat[idx] = curr;
+  vs.hq[idx] = -acc;
+}
+
+// Tiny-tier packing: per sample the labels of y=2 and y=3 in one byte, and the
+// run-start bitmask over sorted positions.
+__global__ void k_pack_tiny(VarSet vs) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int n = vs.n;
+  if (idx >= (long long)vs.V * n) return;
+  const int var = (int)(idx / n), s = (int)(idx % n);
+  const uint16_t* q = vs.q + (size_t)var * vs.ny * n;
+  uint8_t l = (uint8_t)(q[s] & 3);
+  if (vs.ny > 1) l |= (uint8_t)((q[n + s] & 3) << 2);
+  vs.lw[idx] = l;
+  if (s == 0) {
+    uint32_t m = 0;
+    const int* rid = vs.runid + (size_t)var * n;
+    for (int t = 0; t < n; ++t)
+      if (t == 0 || rid[t] != rid[t - 1]) m |= 1u << t;
+    vs.rsmask[var] = m;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tiny tier.  Positions fit one 32-bit word, so row maps become bitmasks in
+// x-sorted order and every cumulative count is a popcount of a prefix mask.
+struct TinyCtx {
+  const double* pl;  // shared copy
+  int n;
+  uint32_t valid;
+};
+
+__device__ __forceinline__ uint32_t prefix(int pos) { return pos >= 32 ? 0xffffffffu : ((1u << pos) - 1u); }
+__device__ __forceinline__ double PLs(const TinyCtx& c, int m, int w) { return c.pl[tri(m) + w]; }
+
+// F(t,2) candidate (mutual_info.cpp:51-52): H(P) - H(P,Q) for the split at s.
+__device__ __forceinline__ double tiny_cand2(const TinyCtx& c, const uint32_t* m, int rows, int cs,
+                                             int ct) {
+  double acc2 = PLs(c, ct, cs);
+  acc2 = __dadd_rn(acc2, PLs(c, ct, ct - cs));
+  const uint32_t ps = prefix(cs), pt = prefix(ct);
+  int a[3];
+  double accj = 0.0;
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    if (r < rows) {
+      a[r] = __popc(m[r] & ps);
+      accj = __dadd_rn(accj, PLs(c, ct, a[r]));
+    }
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    if (r < rows) accj = __dadd_rn(accj, PLs(c, ct, __popc(m[r] & pt) - a[r]));
+  return __dsub_rn(-acc2, -accj);
+}
+
+// One (orientation, y) subproblem; returns I_2 and I_3 (I_3 = I_2 if x_max=2).
+__device__ void tiny_subproblem(const TinyCtx& c, const uint32_t* m, int rows, uint32_t rsm,
+                                int x_max, int k_hat, double hq, double& i2, double& i3) {
+  const int n = c.n;
+  uint32_t d = 0;
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    if (r < rows) d |= m[r] ^ (m[r] << 1);
+  d &= c.valid & ~1u;
+  // Alg. 1 sentinel fusing (partition.cpp:116-133): an x-tie run whose labels
+  // change inside it is fused; fused runs never merge with neighbours.
+  uint32_t fp = d & ~rsm, fm = 0;
+  while (fp) {
+    const int t = __ffs(fp) - 1;
+    const uint32_t upto = (t >= 31) ? 0xffffffffu : ((2u << t) - 1u);
+    const int start = 31 - __clz(rsm & upto);
+    const uint32_t after = rsm & ~upto & c.valid;
+    const int end = after ? __ffs(after) - 1 : n;
+    const uint32_t run = prefix(end) & ~prefix(start);
+    fm |= run;
+    fp &= ~run;
+  }
+  uint32_t bnd = rsm & c.valid & ~1u & (d | fm | (fm << 1));
+  int k = __popc(bnd) + 1;
+  if (k > k_hat) {  // Alg. 2 (partition.cpp:148-165): equipartition clump ordinals
+    double desired = (double)n / (double)k_hat;
+    int curr = 1, in_row = 0, i = 0;
+    uint32_t rest = bnd, nb = 0;
+    for (;;) {
+      const int j = rest ? __ffs(rest) - 1 : n;
+      const int run = j - i;
+      if (in_row != 0 && fabs((double)(in_row + run) - desired) >= fabs((double)in_row - desired)) {
+        ++curr;
+        in_row = 0;
+        desired = (double)(n - i) / (double)(k_hat - curr + 1);
+        nb |= 1u << i;
+      }
+      in_row += run;
+      if (!rest) break;
+      rest &= rest - 1;
+      i = j;
+    }
+    bnd = nb;
+    k = curr;
+  }
+  if (k < 2) {
+    i2 = 0.0;
+    i3 = 0.0;
+    return;
+  }
+  double f2k = kLowest, best3 = kLowest;
+  if (x_max <= 2) {
+    for (uint32_t s = bnd; s; s &= s - 1) f2k = dmax(f2k, tiny_cand2(c, m, rows, __ffs(s) - 1, n));
+  } else {
+    // t-outer over clump ends: F(t,2) for every t (mutual_info.cpp:47-56), and
+    // the level-3 candidate at t = k (mutual_info.cpp:57-66) as soon as F(s,2)
+    // is known, so no F column is stored.
+    int j = 0;
+    for (uint32_t ts = bnd;; ts &= ts - 1) {
+      const int t = ts ? __ffs(ts) - 1 : n;
+      ++j;
+      if (j >= 2) {
+        double f2 = kLowest;
+        for (uint32_t s = bnd & prefix(t); s; s &= s - 1)
+          f2 = dmax(f2, tiny_cand2(c, m, rows, __ffs(s) - 1, t));
+        if (t < n) {
+          // h_span(s=t, k): entropy of the rows of (t, n] (mutual_info.cpp:39-41)
+          const uint32_t tail = c.valid & ~prefix(t);
+          const int mm = n - t;
+          double acch = 0.0;
+#pragma unroll
+          for (int r = 0; r < 3; ++r)
+            if (r < rows) acch = __dadd_rn(acch, PLs(c, mm, __popc(m[r] & tail)));
+          const double r1 = __ddiv_rn((double)t, (double)n);
+          const double wv = __dmul_rn(__ddiv_rn(__dsub_rn((double)n, (double)t), (double)n), -acch);
+          best3 = dmax(best3, __dsub_rn(__dmul_rn(r1, f2), wv));
+        } else {
+          f2k = f2;
+        }
+      }
+      if (!ts) break;
+    }
+  }
+  i2 = dmax(0.0, __dadd_rn(hq, f2k));
+  const int l_max = min(x_max, k);
+  i3 = l_max >= 3 ? dmax(0.0, __dadd_rn(hq, best3)) : i2;
+}
+
+// char_matrix.cpp:57-64: normalise by min(log l, log yhat); clamp at 1 and
+// keep the max with the zero-initialised slot (update_max :28-35).
+__device__ __forceinline__ double norm_cell(double I, double logl, double logy) {
+  const double norm = dmin(logl, logy);
+  double v = norm > 0.0 ? __ddiv_rn(I, norm) : 0.0;
+  if (v > 1.0) v = 1.0;
+  return 0.0 < v ? v : 0.0;
+}
+
+__global__ void __launch_bounds__(128) k_tiny_pairs(VarSet vs, Tables tb, PairSpace ps,
+                                                    double cpar, int est, StatsOut out,
+                                                    double* ocells) {
+  __shared__ double pl_s[561];  // tri(33): rows m <= 32
+  __shared__ double lg[8], lg2[8];
+  const int n = vs.n, B = tb.B;
+  for (int i = threadIdx.x; i < (int)tri(n + 1); i += blockDim.x) pl_s[i] = tb.pl[i];
+  if (threadIdx.x < 8) {
+    lg[threadIdx.x] = threadIdx.x <= B ? tb.logi[threadIdx.x] : 0.0;
+    lg2[threadIdx.x] = threadIdx.x <= B ? tb.log2i[threadIdx.x] : 0.0;
+  }
+  __syncthreads();
+  const long long wl = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (wl >= ps.count) return;
+  int va, vb;
+  pair_vars(ps, ps.first + wl, va, vb);
+
+  TinyCtx c;
+  c.pl = pl_s;
+  c.n = n;
+  c.valid = prefix(n);
+  const int ny = vs.ny;  // 1 (B in {4,5}) or 2 (B in {6,7})
+  // cells in for_each order: 0:(2,2) 1:(3,2) 2:(2,3)
+  double o[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+#pragma unroll
+  for (int orient = 0; orient < 2; ++orient) {
+    const int X = orient ? vb : va, Y = orient ? va : vb;
+    const int* permX = vs.perm + (size_t)X * n;
+    const uint8_t* lwY = vs.lw + (size_t)Y * n;
+    uint32_t m2[3] = {0, 0, 0}, m3[3] = {0, 0, 0};
+    for (int t = 0; t < n; ++t) {
+      const unsigned l = lwY[permX[t]];
+      const uint32_t bit = 1u << t;
+      m2[0] |= (l & 3) == 1 ? bit : 0;
+      m2[1] |= (l & 3) == 2 ? bit : 0;
+      m3[0] |= (l >> 2) == 1 ? bit : 0;
+      m3[1] |= (l >> 2) == 2 ? bit : 0;
+      m3[2] |= (l >> 2) == 3 ? bit : 0;
+    }
+    const uint32_t rsm = vs.rsmask[X];
+    {  // y = 2
+      const int rows = vs.yhat[(size_t)Y * ny];
+      const int x_max = B / 2;
+      const int k_hat = max(1, (int)floor(cpar * (double)x_max));
+      double i2, i3;
+      tiny_subproblem(c, m2, rows, rsm, x_max, k_hat, vs.hq[(size_t)Y * ny], i2, i3);
+      o[orient][0] = norm_cell(i2, lg[2], lg[rows]);
+      if (x_max >= 3) o[orient][orient ? 2 : 1] = norm_cell(i3, lg[3], lg[rows]);
+    }
+    if (ny > 1) {  // y = 3
+      const int rows = vs.yhat[(size_t)Y * ny + 1];
+      const int x_max = B / 3;
+      const int k_hat = max(1, (int)floor(cpar * (double)x_max));
+      double i2, i3;
+      tiny_subproblem(c, m3, rows, rsm, x_max, k_hat, vs.hq[(size_t)Y * ny + 1], i2, i3);
+      o[orient][orient ? 1 : 2] = norm_cell(i2, lg[2], lg[rows]);
+    }
+  }
+  const int ncell = ny > 1 ? 3 : 1;
+  const int cxy[3] = {4, 6, 6};
+  double M[3], E[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    M[i] = o[1][i] > o[0][i] ? o[1][i] : o[0][i];
+    E[i] = i == 0 ? M[i] : (i == 1 ? o[1][i] : o[0][i]);  // (3,2): x>y -> O2; (2,3): x<y -> O1
+  }
+  double mic = 0.0, mev = 0.0, mice = 0.0, mas = 0.0, tic = 0.0;
+  for (int i = 0; i < ncell; ++i) {
+    mic = dmax(mic, M[i]);
+    mev = dmax(mev, M[i]);  // every stored shape has x == 2 or y == 2 when B <= 7
+    mice = dmax(mice, E[i]);
+    const double tr = i == 0 ? M[0] : M[3 - i];
+    mas = dmax(mas, fabs(M[i] - tr));
+    tic = __dadd_rn(tic, est ? E[i] : M[i]);
+  }
+  int best = 1 << 30;
+  for (int i = 0; i < ncell; ++i)
+    if (M[i] == mic) best = min(best, cxy[i]);
+  const long long oi = wl;
+  if (out.mic) out.mic[oi] = mic;
+  if (out.mas) out.mas[oi] = mas;
+  if (out.mev) out.mev[oi] = mev;
+  if (out.mcn) out.mcn[oi] = lg2[best > 7 ? 0 : best];
+  if (out.mic_e) out.mic_e[oi] = mice;
+  if (out.tic) out.tic[oi] = tic;
+  if (ocells) {
+    for (int i = 0; i < ncell; ++i) {
+      ocells[(size_t)oi * 2 * ncell + i] = o[0][i];
+      ocells[(size_t)oi * 2 * ncell + ncell + i] = o[1][i];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// General tier.  One CTA per (pair, orientation) at one row target y.
+constexpr int kGenThreads = 256;
+constexpr int kGenWarps = kGenThreads / 32;
+
+struct GenLayout {
+  size_t f, r1, wv, part, red, cum, cb, cl, sup, lab, fused, misc, total;
+};
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+__host__ __device__ inline GenLayout gen_layout(int n, int y, int x_max, int k_hat, bool f_smem) {
+  GenLayout L;
+  const int kmax = min(n, k_hat);
+  const int lw = x_max - 1;
+  size_t o = 0;
+  L.f = o;
+  o += f_smem ? align16(sizeof(double) * (size_t)(kmax + 1) * lw) : 0;
+  L.r1 = o;
+  o += align16(sizeof(double) * (kmax + 1));
+  L.wv = o;
+  o += align16(sizeof(double) * (kmax + 1));
+  L.part = o;
+  o += align16(sizeof(double) * kGenWarps * 32);
+  L.red = o;
+  o += align16(sizeof(double) * 32);
+  L.cum = o;
+  o += align16(sizeof(int) * (size_t)y * (kmax + 1));
+  L.cb = o;
+  o += align16(sizeof(int) * (n + 1));
+  L.cl = o;
+  o += align16(sizeof(int) * n);
+  L.sup = o;
+  o += align16(sizeof(int) * (n + 1));
+  L.lab = o;
+  o += align16(sizeof(uint16_t) * n);
+  L.fused = o;
+  o += align16(n);
+  L.misc = o;
+  o += align16(sizeof(int) * 64);
+  L.total = o;
+  return L;
+}
+
+__global__ void __launch_bounds__(kGenThreads) k_general(VarSet vs, Tables tb, PairSpace ps,
+                                                         long long base, YParams yp,
+                                                         double* __restrict__ ocells,
+                                                         double* __restrict__ fscratch,
+                                                         SubDebug dbg, int has_dbg,
+                                                         int orient_only, int f_smem) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = vs.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int norient = orient_only >= 0 ? 1 : 2;
+  const long long pl_ = base + blockIdx.x / norient;
+  const int orient = orient_only >= 0 ? orient_only : (int)(blockIdx.x % 2);
+  int va, vb;
+  pair_vars(ps, ps.first + pl_, va, vb);
+  const int X = orient ? vb : va, Y = orient ? va : vb;
+  const int y = yp.y, yi = yp.yi, x_max = yp.x_max, k_hat = yp.k_hat;
+  const int kmax = min(n, k_hat), LW = x_max - 1;
+
+  const GenLayout L = gen_layout(n, y, x_max, k_hat, f_smem != 0);
+  double* F = f_smem ? reinterpret_cast<double*>(smem + L.f)
+                     : fscratch + (size_t)blockIdx.x * (size_t)(kmax + 1) * LW;
+  double* r1 = reinterpret_cast<double*>(smem + L.r1);
+  double* wv = reinterpret_cast<double*>(smem + L.wv);
+  double* part = reinterpret_cast<double*>(smem + L.part);
+  double* red = reinterpret_cast<double*>(smem + L.red);
+  int* cum = reinterpret_cast<int*>(smem + L.cum);
+  int* cb = reinterpret_cast<int*>(smem + L.cb);
+  int* cl = reinterpret_cast<int*>(smem + L.cl);
+  int* sup = reinterpret_cast<int*>(smem + L.sup);
+  uint16_t* lab = reinterpret_cast<uint16_t*>(smem + L.lab);
+  uint8_t* fused = smem + L.fused;
+  int* misc = reinterpret_cast<int*>(smem + L.misc);
+
+  const int* permX = vs.perm + (size_t)X * n;
+  const int* ridX = vs.runid + (size_t)X * n;
+  const uint16_t* qY = vs.q + ((size_t)Y * vs.ny + yi) * n;
+  const int rows = vs.yhat[(size_t)Y * vs.ny + yi];
+  const double hq = vs.hq[(size_t)Y * vs.ny + yi];
+
+  // --- row labels in x-sorted order (reindex_to_first_order, partition.cpp:94-106)
+  for (int t = tid; t < n; t += kGenThreads) {
+    lab[t] = qY[permX[t]];
+    fused[t] = 0;
+  }
+  __syncthreads();
+  // --- Alg. 1 (partition.cpp:116-133): a tie run of x whose labels change is fused
+  for (int t = tid + 1; t < n; t += kGenThreads)
+    if (ridX[t] == ridX[t - 1] && lab[t] != lab[t - 1]) fused[ridX[t]] = 1;
+  __syncthreads();
+  // --- clump starts (:135-144): label change at a run start, or either run fused
+  for (int t = tid; t < n; t += kGenThreads) {
+    int f = 0;
+    if (t > 0) {
+      const int a = ridX[t], b = ridX[t - 1];
+      f = a != b && (fused[a] || fused[b] || lab[t] != lab[t - 1]);
+    }
+    cl[t] = f;
+  }
+  __syncthreads();
+  const int kraw = block_incl_scan(cl, n, misc) + 1;  // cl[t] = clump index of position t
+  for (int t = tid + 1; t < n; t += kGenThreads)
+    if (cl[t] != cl[t - 1]) cb[cl[t]] = t;
+  if (tid == 0) {
+    cb[0] = 0;
+    cb[kraw] = n;
+  }
+  __syncthreads();
+  // --- Alg. 2 (partition.cpp:148-165): equipartition clump ordinals into <= k_hat
+  int k = kraw;
+  if (kraw > k_hat) {
+    if (tid == 0) {
+      double desired = (double)n / (double)k_hat;
+      int curr = 1, in_row = 0;
+      for (int j = 0; j < kraw; ++j) {
+        const int i = cb[j], run = cb[j + 1] - i;
+        if (in_row != 0 &&
+            fabs((double)(in_row + run) - desired) >= fabs((double)in_row - desired)) {
+          ++curr;
+          in_row = 0;
+          desired = (double)(n - i) / (double)(k_hat - curr + 1);
+          cb[curr - 1] = i;  // in place: curr - 1 <= j
+        }
+        sup[j] = curr - 1;
+        in_row += run;
+      }
+      cb[curr] = n;
+      misc[40] = curr;
+    }
+    __syncthreads();
+    k = misc[40];
+  } else {
+    for (int j = tid; j < kraw; j += kGenThreads) sup[j] = j;
+  }
+  // --- cell counts and cumulative table (mutual_info.cpp:9-24), cum[r][j]
+  const int kk = k + 1;
+  for (int i = tid; i < rows * kk; i += kGenThreads) cum[i] = 0;
+  __syncthreads();
+  for (int t = tid; t < n; t += kGenThreads) atomicAdd(&cum[(lab[t] - 1) * kk + sup[cl[t]] + 1], 1);
+  __syncthreads();
+  for (int r = warp; r < rows; r += kGenWarps) {  // warp-scan each row over clumps
+    int carry = 0;
+    for (int j0 = 1; j0 <= k; j0 += 32) {
+      const int j = j0 + lane;
+      int v = j <= k ? cum[r * kk + j] : 0;
+      v = warp_incl_scan(v) + carry;
+      if (j <= k) cum[r * kk + j] = v;
+      carry = __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+
+  if (has_dbg && tid == 0) {
+    *dbg.row_count = rows;
+    *dbg.raw_k = kraw;
+    *dbg.k = k;
+    *dbg.h_q = hq;
+  }
+  if (has_dbg) {
+    for (int t = tid; t < n; t += kGenThreads) dbg.q_x[t] = lab[t];
+    for (int j = tid; j <= k; j += kGenThreads) dbg.bounds[j] = cb[j];
+  }
+
+  // --- exact OptimizeXAxis DP (mutual_info.cpp:26-72), t-outer ---------------
+  const int l_max = min(x_max, k);
+  const double* pl = tb.pl;
+  if (k >= 2) {
+    const int t_begin = l_max >= 3 ? 2 : k;  // x_max == 2 needs F(k,2) only
+    for (int t = t_begin; t <= k; ++t) {
+      const int ct = cb[t];
+      const double* plt = pl + tri(ct);
+      // phase A: threads over s -- F(t,2) candidates and, for levels >= 3, the
+      // span terms r1 = c_s/c_t and wv = ((c_t - c_s)/c_t) h_span(s,t).
+      double best = kLowest;
+      for (int s = 1 + tid; s < t; s += kGenThreads) {
+        const int cs = cb[s];
+        double acc2 = plt[cs];
+        acc2 = __dadd_rn(acc2, plt[ct - cs]);
+        double accj = 0.0;
+        for (int r = 0; r < rows; ++r) accj = __dadd_rn(accj, plt[cum[r * kk + s]]);
+        for (int r = 0; r < rows; ++r) accj = __dadd_rn(accj, plt[cum[r * kk + t] - cum[r * kk + s]]);
+        best = dmax(best, __dsub_rn(-acc2, -accj));
+        if (l_max >= 3 && s >= 2) {
+          const double* plm = pl + tri(ct - cs);
+          double acch = 0.0;
+          for (int r = 0; r < rows; ++r) acch = __dadd_rn(acch, plm[cum[r * kk + t] - cum[r * kk + s]]);
+          const double dcs = (double)cs, dct = (double)ct;
+          r1[s] = __ddiv_rn(dcs, dct);
+          wv[s] = __dmul_rn(__ddiv_rn(__dsub_rn(dct, dcs), dct), -acch);
+        }
+      }
+      best = warp_max(best);
+      if (lane == 0) red[warp] = best;
+      __syncthreads();
+      if (tid == 0) {
+        double b = red[0];
+        for (int w = 1; w < kGenWarps; ++w) b = dmax(b, red[w]);
+        F[(size_t)t * LW + 0] = b;
+      }
+      // phase B: levels 3 .. l_hi from F(s, l-1), s in [l-1, t-1]
+      const int l_hi = t == k ? min(t, l_max) : min(t, l_max - 1);
+      const int nlev = l_hi - 2;
+      if (nlev >= 8) {
+        // lanes over levels, warps over s (strided); partial maxima then reduce
+        for (int l0 = 3; l0 <= l_hi; l0 += 32) {
+          const int l = l0 + lane;
+          double pm = kLowest;
+          if (l <= l_hi)
+            for (int s = max(2, l - 1) + warp; s < t; s += kGenWarps)
+              pm = dmax(pm, __dsub_rn(__dmul_rn(r1[s], F[(size_t)s * LW + (l - 3)]), wv[s]));
+          // stagger warps that start below l-1: the loop start differs per lane
+          part[warp * 32 + lane] = pm;
+          __syncthreads();
+          if (warp == 0 && l <= l_hi) {
+            double b = part[lane];
+            for (int w = 1; w < kGenWarps; ++w) b = dmax(b, part[w * 32 + lane]);
+            F[(size_t)t * LW + (l - 2)] = b;
+          }
+          __syncthreads();
+        }
+      } else if (nlev >= 1) {
+        // one warp per level, lanes over s, shuffle max
+        for (int l = 3 + warp; l <= l_hi; l += kGenWarps) {
+          double pm = kLowest;
+          for (int s = l - 1 + lane; s < t; s += 32)
+            pm = dmax(pm, __dsub_rn(__dmul_rn(r1[s], F[(size_t)s * LW + (l - 3)]), wv[s]));
+          pm = warp_max(pm);
+          if (lane == 0) F[(size_t)t * LW + (l - 2)] = pm;
+        }
+        __syncthreads();
+      } else {
+        __syncthreads();
+      }
+    }
+  }
+  __syncthreads();
+  // --- I_l, normalisation and per-orientation cells (char_matrix.cpp:57-64)
+  double* oc = ocells + (size_t)pl_ * 2 * tb.ncell + (size_t)orient * tb.ncell;
+  const double logy = tb.logi[rows];
+  for (int l = 2 + tid; l <= x_max; l += kGenThreads) {
+    double I;
+    if (k < 2) {
+      I = 0.0;
+    } else {
+      const int le = l <= l_max ? l : l_max;
+      I = dmax(0.0, __dadd_rn(hq, F[(size_t)k * LW + (le - 2)]));
+    }
+    if (has_dbg) dbg.values[l - 2] = I;
+    const int cell = orient ? tb.cell_off[l] + (y - 2) : tb.cell_off[y] + (l - 2);
+    oc[cell] = norm_cell(I, tb.logi[l], logy);
+  }
+}
+
+// Per-pair reduction: max-merge of the orientations (update_max,
+// char_matrix.cpp:28-35) and the statistics (statistics.cpp:10-37) plus the
+// extensions MIC_e / TIC.  One warp per pair.
+__global__ void k_reduce(Tables tb, long long npairs, const double* __restrict__ ocells, int est,
+                         StatsOut out, long long out_offset) {
+  const int lane = threadIdx.x & 31;
+  const long long pr = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (pr >= npairs) return;
+  const int nc = tb.ncell;
+  const double* o1 = ocells + (size_t)pr * 2 * nc;
+  const double* o2 = o1 + nc;
+  double mic = 0.0, mas = 0.0, mev = 0.0, mice = 0.0;
+  for (int c = lane; c < nc; c += 32) {
+    const double a = o1[c], b = o2[c];
+    const double m = b > a ? b : a;
+    const int tr = tb.cell_tr[c];
+    const double ta = o1[tr], tb2 = o2[tr];
+    const double mt = tb2 > ta ? tb2 : ta;
+    mic = dmax(mic, m);
+    mas = dmax(mas, fabs(m - mt));
+    if (tb.cell_edge[c]) mev = dmax(mev, m);
+    const int cmp = tb.cell_cmp[c];
+    mice = dmax(mice, cmp < 0 ? a : (cmp > 0 ? b : m));
+  }
+  mic = warp_max(mic);
+  mas = warp_max(mas);
+  mev = warp_max(mev);
+  mice = warp_max(mice);
+  int best = 1 << 30;
+  for (int c = lane; c < nc; c += 32) {
+    const double a = o1[c], b = o2[c];
+    if ((b > a ? b : a) == mic) best = min(best, tb.cell_xy[c]);
+  }
+  best = warp_min_i(best);
+  if (lane == 0) {
+    double tic = 0.0;  // sequential in for_each order
+    for (int c = 0; c < nc; ++c) {
+      const double a = o1[c], b = o2[c];
+      const double m = b > a ? b : a;
+      const int cmp = tb.cell_cmp[c];
+      tic = __dadd_rn(tic, est ? (cmp < 0 ? a : (cmp > 0 ? b : m)) : m);
+    }
+    const long long oi = out_offset + pr;
+    if (out.mic) out.mic[oi] = mic;
+    if (out.mas) out.mas[oi] = mas;
+    if (out.mev) out.mev[oi] = mev;
+    if (out.mcn) out.mcn[oi] = tb.log2i[best];
+    if (out.mic_e) out.mic_e[oi] = mice;
+    if (out.tic) out.tic[oi] = tic;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Launchers.
+void launch_check_finite(const double* v, long long count, int* flag, cudaStream_t s) {
+  const int blocks = (int)std::min<long long>(4 * 148, (count + 255) / 256 + 1);
+  k_check_finite<<<blocks, 256, 0, s>>>(v, count, flag);
+}
+
+void launch_sort_vars(const VarSet& vs, cudaStream_t s) {
+  const int threads = vs.n <= 256 ? 128 : (vs.n <= 2048 ? 256 : 1024);
+  const size_t sm = sizeof(double) * vs.n + sizeof(int) * (vs.n + 64);
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_sort_vars, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_sort_vars<<<vs.V, threads, sm, s>>>(vs);
+}
+
+void launch_equipartition(const VarSet& vs, const Tables& tb, cudaStream_t s) {
+  const long long total = (long long)vs.V * vs.ny;
+  k_equipartition<<<(unsigned)((total + 127) / 128), 128, 0, s>>>(vs, tb);
+}
+
+void launch_pack_tiny(const VarSet& vs, cudaStream_t s) {
+  const long long total = (long long)vs.V * vs.n;
+  k_pack_tiny<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(vs);
+}
+
+void launch_tiny_pairs(const VarSet& vs, const Tables& tb, const PairSpace& ps, double c, int est,
+                       StatsOut out, double* o_cells, cudaStream_t s) {
+  if (ps.count <= 0) return;
+  const unsigned blocks = (unsigned)((ps.count + 127) / 128);
+  k_tiny_pairs<<<blocks, 128, 0, s>>>(vs, tb, ps, c, est, out, o_cells);
+}
+
+size_t general_smem_bytes(int n, const YParams& yp, bool f_in_smem) {
+  return gen_layout(n, yp.y, yp.x_max, yp.k_hat, f_in_smem).total;
+}
+
+bool general_f_fits(int n, const YParams& yp) {
+  return general_smem_bytes(n, yp, true) <= 200 * 1024;
+}
+
+void launch_general(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
+                    long long npairs, const YParams& yp, double* ocells, double* fscratch,
+                    const SubDebug* dbg, int orient_only, cudaStream_t s) {
+  if (npairs <= 0) return;
+  const bool fs = fscratch == nullptr;
+  const size_t sm = general_smem_bytes(vs.n, yp, fs);
+  cudaFuncSetAttribute(k_general, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const unsigned blocks = (unsigned)(npairs * (orient_only >= 0 ? 1 : 2));
+  SubDebug d{};
+  if (dbg) d = *dbg;
+  k_general<<<blocks, kGenThreads, sm, s>>>(vs, tb, ps, base, yp, ocells, fscratch, d,
+                                            dbg ? 1 : 0, orient_only, fs ? 1 : 0);
+}
+
+void launch_reduce(const Tables& tb, long long npairs, const double* ocells, int est, StatsOut out,
+                   long long out_offset, cudaStream_t s) {
+  if (npairs <= 0) return;
+  const unsigned blocks = (unsigned)((npairs * 32 + 255) / 256);
+  k_reduce<<<blocks, 256, 0, s>>>(tb, npairs, ocells, est, out, out_offset);
+}
+
+}  // namespace mb200

@@ -1,0 +1,107 @@
+// Device-side data structures and kernel launchers of the B200 MINE engine.
+// Host code (engine.cpp) owns all allocations; these launchers only enqueue
+// work on the given stream.  See DESIGN.md for the HBM layout.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace mb200 {
+
+// Per-variable precompute of one call (K1 + K2), all device pointers.
+// Layout is variable-major: variable v's n-length rows start at v * n.
+struct VarSet {
+  const double* vals = nullptr;  // V x n input samples (f64)
+  int V = 0;                     // number of variables
+  int n = 0;                     // samples per variable
+  int ny = 0;                    // row targets y = 2 .. ny + 1  (ny = B/2 - 1)
+  int* perm = nullptr;           // V x n      sample index at each sorted position
+  int* runid = nullptr;          // V x n      tie-run ordinal of each sorted position
+  int* runstart = nullptr;       // V x (n+1)  start position of run r; [nruns] = n
+  int* nruns = nullptr;          // V
+  uint16_t* q = nullptr;         // V x ny x n row label (1-based) of each sample
+  int* yhat = nullptr;           // V x ny     realised row count
+  double* hq = nullptr;          // V x ny     H(Q), reference-exact (mutual_info.cpp:33)
+  uint8_t* lw = nullptr;         // V x n      tiny tier: packed labels (y=2: bits 0-1, y=3: 2-3)
+  uint32_t* rsmask = nullptr;    // V          tiny tier: run-start bitmask over sorted positions
+};
+
+// Host-built constant tables (glibc libm, the reference's own arithmetic).
+struct Tables {
+  const double* pl = nullptr;     // p*log(p), p = w/m, at tri(m) + w, 0 <= w <= m <= n
+  const double* logi = nullptr;   // log(i), 0 <= i <= B
+  const double* log2i = nullptr;  // log2(i), 0 <= i <= B
+  const int* cell_off = nullptr;  // offset of row y in for_each order, indexed by y (0..B/2+1)
+  const int* cell_tr = nullptr;   // for cell c = (x, y): index of (y, x)
+  const int* cell_xy = nullptr;   // x * y of cell c
+  const uint8_t* cell_edge = nullptr;  // x == 2 || y == 2
+  const int8_t* cell_cmp = nullptr;    // sign(x - y): which orientation feeds MIC_e
+  int n = 0;
+  int B = 0;
+  int ncell = 0;
+};
+
+// Which pairs of the variable set to score: work item w in [first, first+count).
+enum PairKind : int { kPairwise = 0, kCross = 1, kList = 2 };
+struct PairSpace {
+  int kind = kPairwise;
+  long long first = 0;
+  long long count = 0;
+  long long p = 0;          // pairwise: variable count
+  int px = 0, py = 0;       // cross: X = vars [0, px), Y = vars [px, px + py)
+  const int* xi = nullptr;  // list: explicit variable indices
+  const int* yi = nullptr;
+};
+
+// Statistic outputs, SoA, indexed by (w - first); any pointer may be null.
+struct StatsOut {
+  double* mic = nullptr;
+  double* mas = nullptr;
+  double* mev = nullptr;
+  double* mcn = nullptr;
+  double* mic_e = nullptr;
+  double* tic = nullptr;
+};
+
+// Parameters of one row target for the general tier.
+struct YParams {
+  int y, yi, x_max, k_hat;
+};
+
+// Optional debug export of one subproblem's integer partition (general tier).
+struct SubDebug {
+  int* row_count;   // [1]
+  int* q_x;         // [n]   row label per x-sorted position
+  int* raw_k;       // [1]   clumps before superclumping
+  int* k;           // [1]
+  int* bounds;      // [n+1]
+  double* h_q;      // [1]
+  double* values;   // [x_max - 1]  I_l before normalisation
+};
+
+// ---- launchers ------------------------------------------------------------
+void launch_check_finite(const double* v, long long count, int* flag, cudaStream_t s);
+void launch_sort_vars(const VarSet& vs, cudaStream_t s);
+void launch_equipartition(const VarSet& vs, const Tables& tb, cudaStream_t s);
+void launch_pack_tiny(const VarSet& vs, cudaStream_t s);
+
+// Tiny tier (n <= 32, B <= 7): one thread per pair, stats (and optionally the
+// per-orientation cells o1/o2, ncell each per pair) written directly.
+void launch_tiny_pairs(const VarSet& vs, const Tables& tb, const PairSpace& ps, double c,
+                       int est, StatsOut out, double* o_cells, cudaStream_t s);
+
+// General tier: one CTA per (pair, orientation) for one row target; writes the
+// normalised per-orientation cells into ocells[(pair - base) * 2 * ncell ...].
+// Returns false if the launch configuration is impossible (caller falls back
+// to nothing: the error surfaces through the C ABI).
+size_t general_smem_bytes(int n, const YParams& yp, bool f_in_smem);
+bool general_f_fits(int n, const YParams& yp);
+void launch_general(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
+                    long long npairs, const YParams& yp, double* ocells, double* fscratch,
+                    const SubDebug* dbg, int orient_only, cudaStream_t s);
+void launch_reduce(const Tables& tb, long long npairs, const double* ocells, int est,
+                   StatsOut out, long long out_offset, cudaStream_t s);
+
+}  // namespace mb200

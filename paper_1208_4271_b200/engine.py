@@ -1,0 +1,351 @@
+"""Python binding of the C ABI (include/mine_b200.h) of libmine_b200.so.
+
+Mirrors the reference's interface for the hot path (proj/include/mine/*.hpp):
+``Parameters``, ``validate_parameters``, ``grid_bound``, ``compute_score`` ->
+``CharacteristicMatrix``, ``compute_statistics``, plus the batch calls
+``pairwise`` / ``cross`` / ``pairs`` that replace ``run_analysis``.  Every
+number comes from the GPU; if the library or a Blackwell GPU is missing the
+call raises -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libmine_b200.so")
+
+MIC_APPROX = 0
+MIC_E = 1
+STATS = ("mic", "mas", "mev", "mcn", "mic_e", "tic")
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_ip = ctypes.POINTER(ctypes.c_int)
+
+
+class MineError(ValueError):
+    """The condition the reference throws std::invalid_argument for."""
+
+
+class MineParameter(ctypes.Structure):
+    _fields_ = [("alpha", ctypes.c_double), ("c", ctypes.c_double), ("est", ctypes.c_int)]
+
+
+class MineStatsOut(ctypes.Structure):
+    _fields_ = [(k, _dp) for k in STATS] + [("cells", _dp)]
+
+
+class MineOpts(ctypes.Structure):
+    _fields_ = [("device_io", ctypes.c_int), ("async_", ctypes.c_int), ("stream", ctypes.c_void_p),
+                ("tier", ctypes.c_int), ("first", ctypes.c_longlong), ("count", ctypes.c_longlong)]
+
+
+class MineProblem(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("x", _dp), ("y", _dp)]
+
+
+class MineScore(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("m", _ip), ("M", ctypes.POINTER(_dp)),
+                ("M_e", ctypes.POINTER(_dp)), ("B", ctypes.c_int), ("est", ctypes.c_int)]
+
+
+_LIB = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libmine_b200.so; raises if it is absent (never falls back)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is missing: build it with __graft_entry__.build() "
+                           "(the engine has no CPU fallback)")
+    L = ctypes.CDLL(path)
+    vp = ctypes.c_void_p
+    L.mine_b200_last_error.restype = ctypes.c_char_p
+    L.mine_b200_create.restype = vp
+    L.mine_b200_create.argtypes = [ctypes.c_int]
+    L.mine_b200_destroy.argtypes = [vp]
+    L.mine_b200_destroy.restype = None
+    L.mine_b200_grid_bound.argtypes = [ctypes.c_longlong, ctypes.c_double]
+    L.mine_b200_cell_count.argtypes = [ctypes.c_int]
+    L.mine_b200_last_launches.argtypes = [vp]
+    L.mine_b200_last_launches.restype = ctypes.c_longlong
+    P = ctypes.POINTER
+    L.mine_b200_pairwise.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, P(MineParameter),
+                                     P(MineOpts), P(MineStatsOut)]
+    L.mine_b200_cross.argtypes = [vp, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int,
+                                  P(MineParameter), P(MineOpts), P(MineStatsOut)]
+    L.mine_b200_pairs.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_longlong,
+                                  P(MineParameter), P(MineOpts), P(MineStatsOut)]
+    L.mine_b200_debug_subproblem.argtypes = [vp, ctypes.c_int, _dp, _dp, ctypes.c_int, ctypes.c_int,
+                                             ctypes.c_int, _ip, _ip, _ip, _ip, _ip, _dp, _dp]
+    L.mine_check_parameter.argtypes = [P(MineParameter)]
+    L.mine_check_parameter.restype = ctypes.c_char_p
+    L.mine_compute_score.argtypes = [P(MineProblem), P(MineParameter)]
+    L.mine_compute_score.restype = P(MineScore)
+    L.mine_free_score.argtypes = [P(P(MineScore))]
+    L.mine_free_score.restype = None
+    for f in ("mine_mic", "mine_mas", "mine_mev", "mine_mcn_general", "mine_mic_e"):
+        getattr(L, f).argtypes = [P(MineScore)]
+        getattr(L, f).restype = ctypes.c_double
+    L.mine_mcn.argtypes = [P(MineScore), ctypes.c_double]
+    L.mine_mcn.restype = ctypes.c_double
+    L.mine_tic.argtypes = [P(MineScore), ctypes.c_int]
+    L.mine_tic.restype = ctypes.c_double
+    _LIB = L
+    return L
+
+
+def exported_symbols() -> list[str]:
+    """Entry points declared in include/mine_b200.h (checked by the CPU tests)."""
+    hdr = os.path.join(os.path.dirname(_PKG), "include", "mine_b200.h")
+    import re
+    names = []
+    for m in re.finditer(r"^[A-Za-z_][\w\s\*]*?\b(mine_\w+)\s*\(", open(hdr).read(), re.M):
+        names.append(m.group(1))
+    return sorted(set(names))
+
+
+# ---------------------------------------------------------------------------
+@dataclass
+class Parameters:
+    """mine::Parameters (char_matrix.hpp:11-14) plus the est extension."""
+    alpha: float = 0.6
+    c: float = 15.0
+    est: int = MIC_APPROX
+
+    def _c(self) -> MineParameter:
+        return MineParameter(float(self.alpha), float(self.c), int(self.est))
+
+
+def validate_parameters(params: Parameters) -> None:
+    """char_matrix.cpp:11-15 -- raises MineError."""
+    if not (params.alpha > 0.0) or params.alpha > 1.0:
+        raise MineError("parameters: alpha must be in (0, 1]")
+    if not (params.c > 0.0):
+        raise MineError("parameters: c must be > 0")
+    if params.est not in (MIC_APPROX, MIC_E):
+        raise MineError("parameters: est must be MIC_APPROX or MIC_E")
+
+
+def grid_bound(n: int, alpha: float) -> int:
+    """char_matrix.cpp:17-20 (pure arithmetic, host side)."""
+    return max(int(math.floor(math.pow(float(n), alpha))), 4)
+
+
+def cell_shapes(bound: int) -> list[tuple[int, int]]:
+    """(x, y) in for_each order, char_matrix.hpp:43-47."""
+    return [(x, y) for y in range(2, bound // 2 + 1) for x in range(2, bound // y + 1)]
+
+
+class CharacteristicMatrix:
+    """mine::CharacteristicMatrix (char_matrix.hpp:25-49), built from the GPU's
+    per-orientation cells.  entry(x, y) = max of the two orientations
+    (update_max, char_matrix.cpp:28-35)."""
+
+    def __init__(self, bound: int, o1: np.ndarray, o2: np.ndarray):
+        self._bound = bound
+        self.shapes = cell_shapes(bound)
+        self.o1 = np.asarray(o1, dtype=np.float64)
+        self.o2 = np.asarray(o2, dtype=np.float64)
+        self.cells = np.where(self.o2 > self.o1, self.o2, self.o1)
+        self._index = {s: i for i, s in enumerate(self.shapes)}
+
+    def bound(self) -> int:
+        return self._bound
+
+    def max_row_target(self) -> int:
+        return self._bound // 2
+
+    def max_col_target(self, y: int) -> int:
+        return self._bound // y
+
+    def contains(self, x: int, y: int) -> bool:
+        return x >= 2 and y >= 2 and x * y <= self._bound
+
+    def entry(self, x: int, y: int) -> float:
+        return float(self.cells[self._index[(x, y)]])
+
+    def for_each(self):
+        for (x, y), v in zip(self.shapes, self.cells):
+            yield x, y, float(v)
+
+    def equicharacteristic(self) -> np.ndarray:
+        """Extension: E(x,y) = O1 if x<y, O2 if x>y, max if x==y."""
+        return np.array([a if x < y else (b if x > y else m) for (x, y), a, b, m in
+                         zip(self.shapes, self.o1, self.o2, self.cells)])
+
+
+# ---------------------------------------------------------------------------
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+class Engine:
+    """One engine context (device buffers, cached tables, streams) on one GPU."""
+
+    def __init__(self, device: int = 0):
+        self.L = load_library()
+        self.ctx = self.L.mine_b200_create(device)
+        if not self.ctx:
+            raise RuntimeError("mine_b200_create failed: " + self.L.mine_b200_last_error().decode())
+        self.device = device
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.L.mine_b200_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int):
+        if rc != 0:
+            raise MineError(self.L.mine_b200_last_error().decode())
+
+    @property
+    def last_launches(self) -> int:
+        return int(self.L.mine_b200_last_launches(self.ctx))
+
+    # -- output plumbing ----------------------------------------------------
+    @staticmethod
+    def _outputs(count: int, stats, cells: bool, bound: int | None):
+        res = {k: np.empty(count) for k in stats}
+        so = MineStatsOut()
+        for k in STATS:
+            setattr(so, k, res[k].ctypes.data_as(_dp) if k in res else None)
+        if cells:
+            nc = len(cell_shapes(bound))
+            res["cells"] = np.empty((count, 2, nc))
+            so.cells = res["cells"].ctypes.data_as(_dp)
+        return res, so
+
+    @staticmethod
+    def _opts(first=0, count=0, tier=0) -> MineOpts:
+        o = MineOpts()
+        o.first, o.count, o.tier = int(first), int(count), int(tier)
+        return o
+
+    # -- batch calls ----------------------------------------------------------
+    def pairwise(self, vars_, params: Parameters = Parameters(), first: int = 0, count: int | None = None,
+                 stats=STATS, cells: bool = False, tier: int = 0):
+        """All pairs i<j in PairSequence order (analysis.cpp:66-81)."""
+        v = _f64(vars_)
+        p, n = v.shape
+        total = p * (p - 1) // 2
+        count = total - first if count is None else count
+        res, so = self._outputs(count, stats, cells, grid_bound(n, params.alpha))
+        self._check(self.L.mine_b200_pairwise(self.ctx, _ptr(v), p, n, ctypes.byref(params._c()),
+                                              ctypes.byref(self._opts(first, count, tier)),
+                                              ctypes.byref(so)))
+        return res
+
+    def cross(self, X, Y, params: Parameters = Parameters(), stats=STATS, cells: bool = False,
+              tier: int = 0, first: int = 0, count: int | None = None):
+        X, Y = _f64(X), _f64(Y)
+        if X.shape[1] != Y.shape[1]:
+            raise MineError("compute_score: input lengths differ")
+        total = X.shape[0] * Y.shape[0]
+        count = total - first if count is None else count
+        res, so = self._outputs(count, stats, cells, grid_bound(X.shape[1], params.alpha))
+        self._check(self.L.mine_b200_cross(self.ctx, _ptr(X), X.shape[0], _ptr(Y), Y.shape[0],
+                                           X.shape[1], ctypes.byref(params._c()),
+                                           ctypes.byref(self._opts(first, count, tier)),
+                                           ctypes.byref(so)))
+        return res
+
+    def pairs(self, vars_, xi, yi, params: Parameters = Parameters(), stats=STATS,
+              cells: bool = False, tier: int = 0):
+        v = _f64(vars_)
+        xi = np.ascontiguousarray(xi, dtype=np.int32)
+        yi = np.ascontiguousarray(yi, dtype=np.int32)
+        res, so = self._outputs(xi.size, stats, cells, grid_bound(v.shape[1], params.alpha))
+        self._check(self.L.mine_b200_pairs(self.ctx, _ptr(v), v.shape[0], v.shape[1], _ptr(xi),
+                                           _ptr(yi), xi.size, ctypes.byref(params._c()),
+                                           ctypes.byref(self._opts(0, xi.size, tier)),
+                                           ctypes.byref(so)))
+        return res
+
+    def pairwise_device(self, vars_ptr: int, p: int, n: int, params: Parameters, out_ptrs: dict,
+                        stream: int = 0, first: int = 0, count: int = 0, tier: int = 0,
+                        async_: bool = True):
+        """Device-resident variant (torch tensors' data_ptr()s): inputs and
+        outputs in HBM, enqueued on `stream`."""
+        so = MineStatsOut()
+        for k in STATS:
+            setattr(so, k, ctypes.cast(ctypes.c_void_p(out_ptrs[k]), _dp) if out_ptrs.get(k) else None)
+        o = self._opts(first, count, tier)
+        o.device_io, o.async_, o.stream = 1, int(async_), ctypes.c_void_p(stream)
+        self._check(self.L.mine_b200_pairwise(self.ctx, ctypes.c_void_p(vars_ptr), p, n,
+                                              ctypes.byref(params._c()), ctypes.byref(o),
+                                              ctypes.byref(so)))
+
+    def debug_subproblem(self, col_var, row_var, y_target: int, x_max: int, k_hat: int):
+        """GPU general-tier partition + DP of one (orientation, y) subproblem
+        (the stage sequence of score_orientation, char_matrix.cpp:44-56)."""
+        col_var, row_var = _f64(col_var), _f64(row_var)
+        n = col_var.size
+        rc, raw, k = (np.zeros(1, np.int32) for _ in range(3))
+        qx = np.zeros(n, np.int32)
+        bounds = np.zeros(n + 1, np.int32)
+        hq = np.zeros(1)
+        vals = np.zeros(max(x_max - 1, 1))
+        self._check(self.L.mine_b200_debug_subproblem(
+            self.ctx, n, col_var.ctypes.data_as(_dp), row_var.ctypes.data_as(_dp), y_target, x_max,
+            k_hat, rc.ctypes.data_as(_ip), qx.ctypes.data_as(_ip), raw.ctypes.data_as(_ip),
+            k.ctypes.data_as(_ip), bounds.ctypes.data_as(_ip), hq.ctypes.data_as(_dp),
+            vals.ctypes.data_as(_dp)))
+        return dict(row_count=int(rc[0]), q_x=qx, clump_count=int(raw[0]), k=int(k[0]),
+                    bounds=bounds[: int(k[0]) + 1].copy(), h_q=float(hq[0]), values=vals[: x_max - 1])
+
+    # -- single pair, the reference's signatures -----------------------------
+    def compute_score(self, xs, ys, params: Parameters = Parameters(), tier: int = 0) -> CharacteristicMatrix:
+        """mine::compute_score (char_matrix.cpp:70-81)."""
+        xs, ys = _f64(xs), _f64(ys)
+        if xs.shape != ys.shape:
+            raise MineError("compute_score: input lengths differ")
+        validate_parameters(params)
+        if xs.size < 2:
+            raise MineError("compute_score: need at least 2 samples")
+        b = grid_bound(xs.size, params.alpha)
+        res = self.pairs(np.stack([xs, ys]), [0], [1], params, stats=("mic",), cells=True, tier=tier)
+        return CharacteristicMatrix(b, res["cells"][0, 0], res["cells"][0, 1])
+
+    def compute_statistics(self, xs, ys, params: Parameters = Parameters(), tier: int = 0) -> dict:
+        """mine::compute_statistics (statistics.cpp:53-63) minus Pearson, plus
+        MIC_e and TIC."""
+        xs, ys = _f64(xs), _f64(ys)
+        if xs.shape != ys.shape:
+            raise MineError("compute_score: input lengths differ")
+        res = self.pairs(np.stack([xs, ys]), [0], [1], params, tier=tier)
+        return {k: float(v[0]) for k, v in res.items()}
+
+
+_DEFAULT: Engine | None = None
+
+
+def default_engine() -> Engine:
+    global _DEFAULT
+    if _DEFAULT is None:
+        _DEFAULT = Engine(int(os.environ.get("MINE_B200_DEVICE", "0")))
+    return _DEFAULT
+
+
+def compute_score(xs, ys, params: Parameters = Parameters()) -> CharacteristicMatrix:
+    return default_engine().compute_score(xs, ys, params)
+
+
+def compute_statistics(xs, ys, params: Parameters = Parameters()) -> dict:
+    return default_engine().compute_statistics(xs, ys, params)
