@@ -103,10 +103,21 @@ typedef struct mine_b200_opts {
   int device_io;     /* 1: inputs and outputs are device pointers (HBM-resident) */
   int async;         /* 1 (with device_io): enqueue on `stream` and return */
   void* stream;      /* cudaStream_t or NULL for the context's stream */
-  int tier;          /* 0 auto, 1 force tiny (n<=32, B<=7), 2 force general */
+  int tier;          /* 0 auto, 1 tiny (n<=32, B<=7), 2 general, 3 memo (n<=25, B<=7) */
   long long first;   /* first work item (pairwise/cross/list index) */
   long long count;   /* items to score; <= 0 means all from `first` */
+  /* Measurement hooks (bench / profiling), all optional:
+   *   counters: host array of MINE_B200_NCOUNTERS realised-work totals
+   *             (the reference arithmetic's FP64 ops and p*log(p) lookups, DP
+   *             candidates, span entries, subproblems; then the table gathers
+   *             the executing tier needs), accumulated by the kernels;
+   *   ev_begin / ev_end: cudaEvent_t recorded on the stream around the
+   *             pair-scoring kernels (the dominant kernels of a call). */
+  unsigned long long* counters;
+  void* ev_begin;
+  void* ev_end;
 } mine_b200_opts;
+#define MINE_B200_NCOUNTERS 6
 
 /* ---- engine API ---------------------------------------------------------- */
 const char* mine_b200_last_error(void);

@@ -18,6 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libmine_b200.so")
+PROBES = os.path.join(PKG, "libmine_b200_probes.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CUDA_INC = "/usr/local/cuda/include"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -61,6 +62,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(o)
     if force or not _newer(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lpthread"])
+    probe_src = os.path.join(CSRC, "probes.cu")
+    if force or not _newer(PROBES, [probe_src]):
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+              "-cudart", "static", "-o", PROBES, probe_src])
     return LIB
 
 

@@ -177,7 +177,8 @@ struct mine_b200_ctx {
   std::mutex mu;
   TableSet tables;
   DevBuf vals, perm, runid, runstart, nruns, q, yhat, hq, lw, rsmask;
-  DevBuf ocells, fscratch, stats, flag, idx;
+  DevBuf ocells, fscratch, stats, flag, idx, counters, memo, rec;
+  int memo_n = -1;
   std::vector<cudaEvent_t> events;
   long long launches = 0;
 };
@@ -236,12 +237,23 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   const bool dio = opts.device_io != 0;
   const int B = grid_bound(n, par->alpha);
   const int ny = B / 2 - 1;
+  // Tier: 0 auto (memo > tiny > general), 1 tiny, 2 general, 3 memo.
   const bool tiny_ok = n <= 32 && B <= 7;
-  bool tiny = tiny_ok && opts.tier != 2;
+  const bool memo_ok = memo_fits(n, B);
   if (opts.tier == 1 && !tiny_ok) throw Failure("mine_b200: tiny tier needs n <= 32 and B <= 7");
+  if (opts.tier == 3 && !memo_ok) throw Failure("mine_b200: memo tier needs n <= 25 and B <= 7");
+  const bool memo = memo_ok && (opts.tier == 0 || opts.tier == 3);
+  const bool tiny = tiny_ok && (opts.tier == 1 || (opts.tier == 0 && !memo));
 
   ctx->tables.build(n, B, s);
   const Tables tb = ctx->tables.view();
+  if (memo && ctx->memo_n != n) {
+    ctx->memo_n = -1;
+    double* mt = static_cast<double*>(ctx->memo.ensure(sizeof(double) * memo_doubles(n)));
+    launch_build_memo(tb, mt, n, s);
+    CK(cudaGetLastError());
+    ctx->memo_n = n;
+  }
   const int ncell = tb.ncell;
 
   // ---- variables -> device
@@ -279,7 +291,11 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   launch_sort_vars(vs, s);
   launch_equipartition(vs, tb, s);
   ctx->launches += 2;
-  if (tiny) {
+  if (memo) {
+    vs.rec = static_cast<uint4*>(ctx->rec.ensure(sizeof(uint4) * 6 * (size_t)V));
+    launch_pack_memo(vs, s);
+    ++ctx->launches;
+  } else if (tiny) {
     vs.lw = static_cast<uint8_t*>(ctx->lw.ensure((size_t)V * n));
     vs.rsmask = static_cast<uint32_t*>(ctx->rsmask.ensure(sizeof(uint32_t) * V));
     launch_pack_tiny(vs, s);
@@ -311,7 +327,8 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   // ---- outputs: device-resident, or a device staging area drained by the
   // copy stream chunk by chunk while the next chunk computes.
   double* const user_stat[6] = {out->mic, out->mas, out->mev, out->mcn, out->mic_e, out->tic};
-  const long long chunk = tiny ? std::min<long long>(count, 1LL << 20)
+  const bool small = tiny || memo;  // one thread per pair, stats written directly
+  const long long chunk = small ? (dio ? count : std::min<long long>(count, 1LL << 20))
                                : std::max<long long>(1, std::min<long long>(
                                      count, (256LL << 20) / (16LL * ncell)));
   const long long nchunks = (count + chunk - 1) / chunk;
@@ -321,7 +338,7 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   const size_t stage_cells = out->cells ? 2 * (size_t)ncell * chunk : 0;
   if (!dio) stage = static_cast<double*>(ctx->stats.ensure(sizeof(double) * nslots * (stage_stats + stage_cells)));
   double* ocells = nullptr;
-  if (!tiny) ocells = static_cast<double*>(ctx->ocells.ensure(sizeof(double) * 2 * (size_t)ncell * chunk));
+  if (!small) ocells = static_cast<double*>(ctx->ocells.ensure(sizeof(double) * 2 * (size_t)ncell * chunk));
 
   std::vector<YParams> yps;
   for (int y = 2; y <= B / 2; ++y) {
@@ -332,12 +349,19 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
     yp.k_hat = std::max(1, static_cast<int>(std::floor(par->c * static_cast<double>(yp.x_max))));
     yps.push_back(yp);
   }
-  if (!tiny) {
+  if (!small) {
     for (const auto& yp : yps)
       if (general_smem_bytes(n, yp, false) > 227 * 1024)
         throw Failure("mine_b200: general tier shared-memory plan exceeds 227 KB for n=" +
                       std::to_string(n) + " y=" + std::to_string(yp.y));
   }
+
+  unsigned long long* dcnt = nullptr;
+  if (opts.counters) {
+    dcnt = static_cast<unsigned long long*>(ctx->counters.ensure(sizeof(unsigned long long) * kNumCounters));
+    CK(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long) * kNumCounters, s));
+  }
+  if (opts.ev_begin) CK(cudaEventRecord(static_cast<cudaEvent_t>(opts.ev_begin), s));
 
   for (long long ci = 0; ci < nchunks; ++ci) {
     const long long c0 = ci * chunk;
@@ -363,13 +387,16 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
     PairSpace pc = ps;
     pc.first = first + c0;
     pc.count = cn;
-    if (tiny) {
-      launch_tiny_pairs(vs, tb, pc, par->c, par->est, so, cells_dst, s);
+    if (memo) {
+      launch_memo_pairs(vs, tb, ctx->memo.as<double>(), pc, par->c, par->est, so, cells_dst, dcnt, s);
+      ++ctx->launches;
+    } else if (tiny) {
+      launch_tiny_pairs(vs, tb, pc, par->c, par->est, so, cells_dst, dcnt, s);
       ++ctx->launches;
     } else {
       for (const auto& yp : yps) {
         if (general_f_fits(n, yp)) {
-          launch_general(vs, tb, pc, 0, cn, yp, ocells, nullptr, nullptr, -1, s);
+          launch_general(vs, tb, pc, 0, cn, yp, ocells, nullptr, nullptr, -1, dcnt, s);
           ++ctx->launches;
         } else {
           // F table in global scratch: bound the CTAs per launch.
@@ -378,7 +405,7 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
           const long long step = std::max<long long>(1, max_ctas / 2);
           double* fs = static_cast<double*>(ctx->fscratch.ensure(per_cta * 2 * step));
           for (long long b0 = 0; b0 < cn; b0 += step) {
-            launch_general(vs, tb, pc, b0, std::min(step, cn - b0), yp, ocells + 0, fs, nullptr, -1, s);
+            launch_general(vs, tb, pc, b0, std::min(step, cn - b0), yp, ocells, fs, nullptr, -1, dcnt, s);
             ++ctx->launches;
           }
         }
@@ -404,9 +431,12 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
       CK(cudaEventRecord(ctx_event(ctx, 2 * slot + 1), ctx->copy));
     }
   }
-  if (dio && opts.async) return;
+  if (opts.ev_end) CK(cudaEventRecord(static_cast<cudaEvent_t>(opts.ev_end), s));
+  if (dio && opts.async && !opts.counters) return;
   if (!dio) CK(cudaStreamSynchronize(ctx->copy));
   CK(cudaStreamSynchronize(s));
+  if (opts.counters)
+    CK(cudaMemcpy(opts.counters, dcnt, sizeof(unsigned long long) * kNumCounters, cudaMemcpyDeviceToHost));
   int h_flag = 0;
   CK(cudaMemcpy(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost));
   if (h_flag) throw Failure("compute_score: inputs must be finite");
@@ -572,7 +602,7 @@ int mine_b200_debug_subproblem(mine_b200_ctx* ctx, int n, const double* col_var,
     double* fs = nullptr;
     if (!general_f_fits(n, yp))
       fs = static_cast<double*>(ctx->fscratch.ensure(sizeof(double) * (size_t)(std::min(n, k_hat) + 1) * (x_max - 1)));
-    launch_general(vs, tb, ps, 0, 1, yp, oc, fs, &dbg, 0, s);
+    launch_general(vs, tb, ps, 0, 1, yp, oc, fs, &dbg, 0, nullptr, s);
     CK(cudaGetLastError());
     std::vector<char> h(bytes);
     CK(cudaMemcpyAsync(h.data(), dd, bytes, cudaMemcpyDeviceToHost, s));

@@ -14,8 +14,10 @@
 //                               clumps/superclumps/cell counts (partition.cpp:108-165,
 //                               mutual_info.cpp:9-24) + t-outer exact DP (mutual_info.cpp:26-72)
 //              k_reduce       per pair: max-merge + MIC/MAS/MEV/MCN/MIC_e/TIC (statistics.cpp:10-37)
+#include <algorithm>
 #include <cfloat>
 #include <cstdint>
+#include <cstring>
 
 #include "mine_kernels.h"
 
@@ -103,6 +105,40 @@ __device__ __forceinline__ void pair_vars(const PairSpace& ps, long long w, int&
     vx = ps.xi[w];
     vy = ps.yi[w];
   }
+}
+
+// Realised algorithmic work of one exact subproblem (rows R, k clumps): the
+// FP64 operations the reference arithmetic itself requires (mutual_info.cpp:
+// 47-66 with every 0.0 + x start elided), its p*log(p) lookups, DP candidates
+// and span entries.  Used only when counters are requested.
+__device__ void subproblem_work(int R, int k, int x_max, unsigned long long* w,
+                                bool gathers_as_reference = true) {
+  if (k < 2) return;
+  const long long l_max = min(x_max, k), K = k;
+  const long long f2 = l_max >= 3 ? K * (K - 1) / 2 : K - 1;  // F(t,2) candidates
+  long long spans = 0, cand = 0;
+  if (l_max >= 3) {
+    spans = K - 2;                                             // t = k
+    if (l_max >= 4) spans += (K - 3) * (K - 2) / 2;            // t = 3 .. k-1
+    for (long long l = 3; l <= l_max; ++l) {
+      cand += K - l + 1;                                       // t = k
+      if (l <= l_max - 1) cand += (K - l) * (K - l + 1) / 2;   // t = l .. k-1
+    }
+  }
+  w[kCntFp64] += f2 * (2 * R + 2) + spans * (R + 2) + cand * 3;
+  w[kCntLookups] += f2 * (2 * R + 2) + spans * R;
+  if (gathers_as_reference) w[kCntGathers] += f2 * (2 * R + 2) + spans * R;
+  w[kCntCand] += cand;
+  w[kCntSpans] += spans;
+  w[kCntSub] += 1;
+}
+
+// Instrumented runs only (untimed): plain per-thread atomics, safe from any
+// divergent call site.
+__device__ void flush_work(const unsigned long long* w, unsigned long long* counters) {
+#pragma unroll
+  for (int i = 0; i < kNumCounters; ++i)
+    if (w[i]) atomicAdd(counters + i, w[i]);
 }
 
 // ---------------------------------------------------------------------------
@@ -240,15 +276,12 @@ __device__ __forceinline__ double tiny_cand2(const TinyCtx& c, const uint32_t* m
   return __dsub_rn(-acc2, -accj);
 }
 
-// One (orientation, y) subproblem; returns I_2 and I_3 (I_3 = I_2 if x_max=2).
-__device__ void tiny_subproblem(const TinyCtx& c, const uint32_t* m, int rows, uint32_t rsm,
-                                int x_max, int k_hat, double hq, double& i2, double& i3) {
-  const int n = c.n;
-  uint32_t d = 0;
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-    if (r < rows) d |= m[r] ^ (m[r] << 1);
-  d &= c.valid & ~1u;
+// Clump ends over x-sorted positions packed in one word (n <= 32).  d: label
+// changes (bit t: lab[t] != lab[t-1]), rsm: x tie-run starts.  Returns the
+// boundary mask (bit t: a clump starts at t >= 1) and k; applies Alg. 2 when
+// k > k_hat.
+__device__ uint32_t bits_partition(uint32_t d, uint32_t rsm, uint32_t valid, int n, int k_hat,
+                                   int& k_out) {
   // Alg. 1 sentinel fusing (partition.cpp:116-133): an x-tie run whose labels
   // change inside it is fused; fused runs never merge with neighbours.
   uint32_t fp = d & ~rsm, fm = 0;
@@ -256,13 +289,13 @@ __device__ void tiny_subproblem(const TinyCtx& c, const uint32_t* m, int rows, u
     const int t = __ffs(fp) - 1;
     const uint32_t upto = (t >= 31) ? 0xffffffffu : ((2u << t) - 1u);
     const int start = 31 - __clz(rsm & upto);
-    const uint32_t after = rsm & ~upto & c.valid;
+    const uint32_t after = rsm & ~upto & valid;
     const int end = after ? __ffs(after) - 1 : n;
     const uint32_t run = prefix(end) & ~prefix(start);
     fm |= run;
     fp &= ~run;
   }
-  uint32_t bnd = rsm & c.valid & ~1u & (d | fm | (fm << 1));
+  uint32_t bnd = rsm & valid & ~1u & (d | fm | (fm << 1));
   int k = __popc(bnd) + 1;
   if (k > k_hat) {  // Alg. 2 (partition.cpp:148-165): equipartition clump ordinals
     double desired = (double)n / (double)k_hat;
@@ -285,6 +318,23 @@ __device__ void tiny_subproblem(const TinyCtx& c, const uint32_t* m, int rows, u
     bnd = nb;
     k = curr;
   }
+  k_out = k;
+  return bnd;
+}
+
+// One (orientation, y) subproblem; returns I_2 and I_3 (I_3 = I_2 if x_max=2).
+__device__ void tiny_subproblem(const TinyCtx& c, const uint32_t* m, int rows, uint32_t rsm,
+                                int x_max, int k_hat, double hq, double& i2, double& i3,
+                                unsigned long long* work) {
+  const int n = c.n;
+  uint32_t d = 0;
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    if (r < rows) d |= m[r] ^ (m[r] << 1);
+  d &= c.valid & ~1u;
+  int k;
+  const uint32_t bnd = bits_partition(d, rsm, c.valid, n, k_hat, k);
+  if (work) subproblem_work(rows, k, x_max, work);
   if (k < 2) {
     i2 = 0.0;
     i3 = 0.0;
@@ -337,9 +387,52 @@ __device__ __forceinline__ double norm_cell(double I, double logl, double logy) 
   return 0.0 < v ? v : 0.0;
 }
 
+// Statistics of a B <= 7 matrix (cells 0:(2,2) 1:(3,2) 2:(2,3)) from the two
+// orientations' cells -- update_max merge (char_matrix.cpp:28-35), then
+// statistics.cpp:10-37 and the MIC_e / TIC extensions.
+__device__ __forceinline__ void small_stats(const double (&o)[2][3], int ncell, int est,
+                                            const double* lg2, const StatsOut& out,
+                                            long long oi, double* ocells) {
+  const int cxy[3] = {4, 6, 6};
+  double M[3], E[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    M[i] = o[1][i] > o[0][i] ? o[1][i] : o[0][i];
+    E[i] = i == 0 ? M[i] : (i == 1 ? o[1][i] : o[0][i]);  // (3,2): x>y -> O2; (2,3): x<y -> O1
+  }
+  double mic = 0.0, mev = 0.0, mice = 0.0, mas = 0.0, tic = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    if (i < ncell) {
+      mic = dmax(mic, M[i]);
+      mev = dmax(mev, M[i]);  // every stored shape has x == 2 or y == 2 when B <= 7
+      mice = dmax(mice, E[i]);
+      const double tr = i == 0 ? M[0] : M[3 - i];
+      mas = dmax(mas, fabs(M[i] - tr));
+      tic = __dadd_rn(tic, est ? E[i] : M[i]);
+    }
+  }
+  int best = 1 << 30;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    if (i < ncell && M[i] == mic) best = min(best, cxy[i]);
+  if (out.mic) out.mic[oi] = mic;
+  if (out.mas) out.mas[oi] = mas;
+  if (out.mev) out.mev[oi] = mev;
+  if (out.mcn) out.mcn[oi] = lg2[best > 7 ? 0 : best];
+  if (out.mic_e) out.mic_e[oi] = mice;
+  if (out.tic) out.tic[oi] = tic;
+  if (ocells) {
+    for (int i = 0; i < ncell; ++i) {
+      ocells[(size_t)oi * 2 * ncell + i] = o[0][i];
+      ocells[(size_t)oi * 2 * ncell + ncell + i] = o[1][i];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(128) k_tiny_pairs(VarSet vs, Tables tb, PairSpace ps,
                                                     double cpar, int est, StatsOut out,
-                                                    double* ocells) {
+                                                    double* ocells, unsigned long long* counters) {
   __shared__ double pl_s[561];  // tri(33): rows m <= 32
   __shared__ double lg[8], lg2[8];
   const int n = vs.n, B = tb.B;
@@ -350,7 +443,12 @@ __global__ void __launch_bounds__(128) k_tiny_pairs(VarSet vs, Tables tb, PairSp
   }
   __syncthreads();
   const long long wl = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (wl >= ps.count) return;
+  unsigned long long work[kNumCounters] = {0, 0, 0, 0, 0, 0};
+  unsigned long long* wk = counters ? work : nullptr;
+  if (wl >= ps.count) {
+    if (counters) flush_work(work, counters);
+    return;
+  }
   int va, vb;
   pair_vars(ps, ps.first + wl, va, vb);
 
@@ -382,7 +480,7 @@ __global__ void __launch_bounds__(128) k_tiny_pairs(VarSet vs, Tables tb, PairSp
       const int x_max = B / 2;
       const int k_hat = max(1, (int)floor(cpar * (double)x_max));
       double i2, i3;
-      tiny_subproblem(c, m2, rows, rsm, x_max, k_hat, vs.hq[(size_t)Y * ny], i2, i3);
+      tiny_subproblem(c, m2, rows, rsm, x_max, k_hat, vs.hq[(size_t)Y * ny], i2, i3, wk);
       o[orient][0] = norm_cell(i2, lg[2], lg[rows]);
       if (x_max >= 3) o[orient][orient ? 2 : 1] = norm_cell(i3, lg[3], lg[rows]);
     }
@@ -391,43 +489,360 @@ __global__ void __launch_bounds__(128) k_tiny_pairs(VarSet vs, Tables tb, PairSp
       const int x_max = B / 3;
       const int k_hat = max(1, (int)floor(cpar * (double)x_max));
       double i2, i3;
-      tiny_subproblem(c, m3, rows, rsm, x_max, k_hat, vs.hq[(size_t)Y * ny + 1], i2, i3);
+      tiny_subproblem(c, m3, rows, rsm, x_max, k_hat, vs.hq[(size_t)Y * ny + 1], i2, i3, wk);
       o[orient][orient ? 1 : 2] = norm_cell(i2, lg[2], lg[rows]);
     }
   }
-  const int ncell = ny > 1 ? 3 : 1;
-  const int cxy[3] = {4, 6, 6};
-  double M[3], E[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    M[i] = o[1][i] > o[0][i] ? o[1][i] : o[0][i];
-    E[i] = i == 0 ? M[i] : (i == 1 ? o[1][i] : o[0][i]);  // (3,2): x>y -> O2; (2,3): x<y -> O1
-  }
-  double mic = 0.0, mev = 0.0, mice = 0.0, mas = 0.0, tic = 0.0;
-  for (int i = 0; i < ncell; ++i) {
-    mic = dmax(mic, M[i]);
-    mev = dmax(mev, M[i]);  // every stored shape has x == 2 or y == 2 when B <= 7
-    mice = dmax(mice, E[i]);
-    const double tr = i == 0 ? M[0] : M[3 - i];
-    mas = dmax(mas, fabs(M[i] - tr));
-    tic = __dadd_rn(tic, est ? E[i] : M[i]);
-  }
-  int best = 1 << 30;
-  for (int i = 0; i < ncell; ++i)
-    if (M[i] == mic) best = min(best, cxy[i]);
-  const long long oi = wl;
-  if (out.mic) out.mic[oi] = mic;
-  if (out.mas) out.mas[oi] = mas;
-  if (out.mev) out.mev[oi] = mev;
-  if (out.mcn) out.mcn[oi] = lg2[best > 7 ? 0 : best];
-  if (out.mic_e) out.mic_e[oi] = mice;
-  if (out.tic) out.tic[oi] = tic;
-  if (ocells) {
-    for (int i = 0; i < ncell; ++i) {
-      ocells[(size_t)oi * 2 * ncell + i] = o[0][i];
-      ocells[(size_t)oi * 2 * ncell + ncell + i] = o[1][i];
+  small_stats(o, ny > 1 ? 3 : 1, est, lg2, out, wl, ocells);
+  if (counters) flush_work(work, counters);
+}
+
+// ---------------------------------------------------------------------------
+// Memo tier (n <= 25, B <= 7; the c1 shape).  With two rows every F(t,2)
+// candidate H(P) - H(P,Q) (mutual_info.cpp:51-52) is a function of (c_t, c_s,
+// a0, b0) only (a1 = c_s - a0, b1 = c_t - c_s - b0), and there are only
+// C(n+4,4)-ish such tuples.  k_build_memo evaluates every candidate ONCE with
+// the reference's exact operation sequence (sequential p*log(p) sums, then
+// (-acc2) - (-accj)), so a candidate becomes one shared-memory gather instead
+// of six, bit-identically.  Likewise the level-3 span term at t = k, and the
+// first three joint-entropy terms of the three-row case.
+__host__ __device__ __forceinline__ int memo_G(int ct, int cs) {
+  // entries of K2 before c_s within block c_t: sum_{u=2}^{cs} u (ct + 2 - u)
+  return (ct + 2) * (cs * (cs + 1) / 2 - 1) - (cs * (cs + 1) * (2 * cs + 1) / 6 - 1);
+}
+
+__host__ __device__ inline MemoLayout memo_layout(int n) {
+  MemoLayout L;
+  int k2 = 0;
+  for (int ct = 2; ct <= n; ++ct) k2 += memo_G(ct, ct);
+  L.n = n;
+  L.k2 = 0;
+  L.t3 = k2;
+  L.w2 = L.t3 + n * (n + 1) * (n + 2) / 6;
+  L.e2 = L.w2 + n * (n + 1) - n * (n - 1) / 2;
+  L.r1 = L.e2 + n + 1;
+  L.pln = L.r1 + n + 1;
+  L.offk = L.pln + n + 1;                     // (n + 2) ints
+  L.gq = L.offk + (n + 3) / 2;                // (n + 1) ints: packed (g1, 2 g1 - g2) per c_s
+  L.t3o = L.gq + (n + 2) / 2;                 // (n + 1)^2 ints: t3_index(c_s, a0, 0)
+  L.total = L.t3o + ((n + 1) * (n + 1) + 1) / 2;
+  return L;
+}
+
+struct MemoCtx {
+  const double* tab;
+  const int* offk;
+  const int* gq;
+  const int* t3o;
+  MemoLayout L;
+  int n;
+  uint32_t valid;
+};
+
+__device__ __forceinline__ int t3_index(int cs, int a0, int a1) {
+  return cs * (cs + 1) * (cs + 2) / 6 + a0 * (cs + 1) - a0 * (a0 - 1) / 2 + a1;
+}
+__device__ __forceinline__ int w2_index(int n, int cs, int u0) {
+  return cs * (n + 1) - cs * (cs - 1) / 2 + u0;
+}
+
+// Table builder: one block, the same FP64 op sequence as tiny_cand2 / the
+// general tier (both bit-exact against the reference).
+__global__ void k_build_memo(Tables tb, double* memo, int n) {
+  const MemoLayout L = memo_layout(n);
+  int* offk = reinterpret_cast<int*>(memo + L.offk);
+  const double* pl = tb.pl;
+  auto PL = [&](int m, int w) { return pl[tri(m) + w]; };
+  if (threadIdx.x == 0) {
+    int off = 0;
+    for (int ct = 0; ct <= n + 1; ++ct) {
+      offk[ct] = off;
+      if (ct >= 2 && ct <= n) off += memo_G(ct, ct);
     }
   }
+  int* gq = reinterpret_cast<int*>(memo + L.gq);
+  int* t3o = reinterpret_cast<int*>(memo + L.t3o);
+  for (int cs = threadIdx.x; cs <= n; cs += blockDim.x) {
+    const int g1 = cs * (cs + 1) / 2 - 1;
+    const int g2 = cs * (cs + 1) * (2 * cs + 1) / 6 - 1;
+    gq[cs] = (g1 << 16) + (2 * g1 - g2 + 8192);
+    for (int a0 = 0; a0 <= n; ++a0) t3o[cs * (n + 1) + a0] = a0 <= cs ? t3_index(cs, a0, 0) : 0;
+  }
+  // K2[ct][cs][a0][b0]
+  for (int idx = threadIdx.x; idx < (n + 1) * (n + 1); idx += blockDim.x) {
+    const int ct = idx / (n + 1), cs = idx % (n + 1);
+    if (ct < 2 || cs < 1 || cs >= ct) continue;
+    int base = memo_G(ct, cs);
+    for (int c = 2; c < ct; ++c) base += memo_G(c, c);
+    double acc2 = PL(ct, cs);
+    acc2 = __dadd_rn(acc2, PL(ct, ct - cs));
+    for (int a0 = 0; a0 <= cs; ++a0)
+      for (int b0 = 0; b0 <= ct - cs; ++b0) {
+        double accj = PL(ct, a0);
+        accj = __dadd_rn(accj, PL(ct, cs - a0));
+        accj = __dadd_rn(accj, PL(ct, b0));
+        accj = __dadd_rn(accj, PL(ct, ct - cs - b0));
+        memo[L.k2 + base + a0 * (ct - cs + 1) + b0] = __dsub_rn(-acc2, -accj);
+      }
+  }
+  // T3[cs][a0][a1] (c_t = n), W2[cs][u0] (c_t = n), E2, R1, PLn
+  for (int cs = threadIdx.x; cs < n; cs += blockDim.x) {
+    for (int a0 = 0; a0 <= cs; ++a0)
+      for (int a1 = 0; a0 + a1 <= cs; ++a1) {
+        double acc = PL(n, a0);
+        acc = __dadd_rn(acc, PL(n, a1));
+        acc = __dadd_rn(acc, PL(n, cs - a0 - a1));
+        memo[L.t3 + t3_index(cs, a0, a1)] = acc;
+      }
+    const int m = n - cs;
+    for (int u0 = 0; u0 <= m; ++u0) {
+      double acch = PL(m, u0);
+      acch = __dadd_rn(acch, PL(m, m - u0));
+      memo[L.w2 + w2_index(n, cs, u0)] =
+          __dmul_rn(__ddiv_rn(__dsub_rn((double)n, (double)cs), (double)n), -acch);
+    }
+  }
+  for (int i = threadIdx.x; i <= n; i += blockDim.x) {
+    double acc2 = PL(n, i);
+    acc2 = __dadd_rn(acc2, PL(n, n - i));
+    memo[L.e2 + i] = -acc2;
+    memo[L.r1 + i] = __ddiv_rn((double)i, (double)n);
+    memo[L.pln + i] = PL(n, i);
+  }
+}
+
+// Per-variable 96-byte record: rank byte of each sample (x-sorted position),
+// label flags (bit0: y=2 row 1, bit1: y=3 row 1, bit2: y=3 row 2), H(Q) for
+// y = 2, 3, the run-start mask and yhat for y = 2, 3.
+__global__ void k_pack_memo(VarSet vs) {
+  const int var = blockIdx.x * blockDim.x + threadIdx.x;
+  if (var >= vs.V) return;
+  const int n = vs.n;
+  uint8_t rec[96];
+#pragma unroll
+  for (int i = 0; i < 96; ++i) rec[i] = 0;
+  const int* perm = vs.perm + (size_t)var * n;
+  const int* rid = vs.runid + (size_t)var * n;
+  const uint16_t* q2 = vs.q + (size_t)var * vs.ny * n;
+  const uint16_t* q3 = q2 + n;
+  uint32_t rsm = 0;
+  for (int t = 0; t < n; ++t) {
+    rec[perm[t]] = (uint8_t)t;
+    if (t == 0 || rid[t] != rid[t - 1]) rsm |= 1u << t;
+  }
+  for (int s = 0; s < n; ++s) {
+    uint8_t f = q2[s] == 1 ? 1 : 0;
+    if (vs.ny > 1) f |= (q3[s] == 1 ? 2 : 0) | (q3[s] == 2 ? 4 : 0);
+    rec[32 + s] = f;
+  }
+  const double h2 = vs.hq[(size_t)var * vs.ny];
+  const double h3 = vs.ny > 1 ? vs.hq[(size_t)var * vs.ny + 1] : 0.0;
+  memcpy(rec + 64, &h2, 8);
+  memcpy(rec + 72, &h3, 8);
+  memcpy(rec + 80, &rsm, 4);
+  rec[84] = (uint8_t)vs.yhat[(size_t)var * vs.ny];
+  rec[85] = vs.ny > 1 ? (uint8_t)vs.yhat[(size_t)var * vs.ny + 1] : 0;
+  uint4* dst = vs.rec + (size_t)var * 6;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    uint4 v;
+    memcpy(&v, rec + 16 * i, 16);
+    dst[i] = v;
+  }
+}
+
+__device__ __forceinline__ uint32_t byte_of(const uint32_t* w, int s) {
+  return (w[s >> 2] >> ((s & 3) * 8)) & 0xffu;
+}
+
+// y = 2 (two rows; row-1 positions m0): I_2 and, if x_max == 3, I_3.
+// The K2 index of candidate (s, t) factors as
+//   OFFK(c_t) + G(c_t, c_s) + a0 (c_t - c_s + 1) + b0
+//     = [OFFK(c_t) + B0(t)] + c_t * P_s + Q_s,
+//   P_s = g1(c_s) + a0(s),  Q_s = 2 g1(c_s) - g2(c_s) - a0(s) c_s,
+// so P_s / Q_s are computed once per boundary into this thread's column of
+// shared scratch (bank = lane: conflict-free) and the inner loop is one
+// scratch read, one IMAD and one table gather per candidate.
+__device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, int k_hat,
+                        double hq, double& i2, double& i3, unsigned long long* work,
+                        int* scr, int sstride) {
+  const int n = c.n;
+  const uint32_t d = (m0 ^ (m0 << 1)) & c.valid & ~1u;
+  int k;
+  const uint32_t bnd = bits_partition(d, rsm, c.valid, n, k_hat, k);
+  if (work) {
+    subproblem_work(2, k, x_max, work, false);
+    if (k >= 2) work[kCntGathers] += x_max <= 2 ? k - 1 : k * (k - 1) / 2 + 2 * (k - 2);
+  }
+  if (k < 2) {
+    i2 = i3 = 0.0;
+    return;
+  }
+  const int c0 = __popc(m0);
+  const double* K2 = c.tab + c.L.k2;
+  double f2k = kLowest, best3 = kLowest;
+  if (x_max <= 2) {
+    const double* kb = K2 + c.offk[n];
+    for (uint32_t s = bnd; s; s &= s - 1) {
+      const int cs = __ffs(s) - 1;
+      const int a0 = __popc(m0 & prefix(cs));
+      f2k = dmax(f2k, kb[memo_G(n, cs) + a0 * (n - cs + 1) + (c0 - a0)]);
+    }
+  } else {
+    int cnt = 0;
+    for (uint32_t s = bnd; s; s &= s - 1, ++cnt) {
+      const int cs = __ffs(s) - 1;
+      const int a0 = __popc(m0 & ((1u << cs) - 1u));  // c_s < n <= 31
+      scr[cnt * sstride] = c.gq[cs] + (a0 << 16) - a0 * cs;
+    }
+    const double* W2 = c.tab + c.L.w2;
+    const double* R1 = c.tab + c.L.r1;
+    int j = 0;
+    for (uint32_t ts = bnd;; ts &= ts - 1) {
+      const int t = ts ? __ffs(ts) - 1 : n;
+      ++j;
+      if (j >= 2) {
+        const int b0t = __popc(m0 & prefix(t));
+        const double* kb = K2 + (c.offk[t] + b0t - 8192);
+        double f2 = kLowest;
+        for (int i = 0; i < j - 1; ++i) {
+          const int v = scr[i * sstride];
+          f2 = dmax(f2, kb[t * (v >> 16) + (v & 0xffff)]);
+        }
+        if (t < n)
+          best3 = dmax(best3, __dsub_rn(__dmul_rn(R1[t], f2), W2[w2_index(n, t, c0 - b0t)]));
+        else
+          f2k = f2;
+      }
+      if (!ts) break;
+    }
+  }
+  i2 = dmax(0.0, __dadd_rn(hq, f2k));
+  i3 = min(x_max, k) >= 3 ? dmax(0.0, __dadd_rn(hq, best3)) : i2;
+}
+
+// y = 3 with three rows (x_max = 2: F(k,2) only, c_t = n).
+__device__ double memo_y3_rows3(const MemoCtx& c, uint32_t m0, uint32_t m1, uint32_t rsm,
+                                int k_hat, double hq, unsigned long long* work) {
+  const int n = c.n;
+  const uint32_t d = ((m0 ^ (m0 << 1)) | (m1 ^ (m1 << 1))) & c.valid & ~1u;
+  int k;
+  const uint32_t bnd = bits_partition(d, rsm, c.valid, n, k_hat, k);
+  if (work) {
+    subproblem_work(3, k, 2, work, false);
+    if (k >= 2) work[kCntGathers] += 5 * (k - 1);
+  }
+  if (k < 2) return 0.0;
+  const int c0 = __popc(m0), c1 = __popc(m1);
+  const double* T3 = c.tab + c.L.t3;
+  const double* E2 = c.tab + c.L.e2;
+  const double* P = c.tab + c.L.pln;
+  double best = kLowest;
+  const int* t3o = c.t3o;
+  for (uint32_t s = bnd; s; s &= s - 1) {
+    const int cs = __ffs(s) - 1;
+    const uint32_t pre = (1u << cs) - 1u;  // c_s < n <= 31
+    const int a0 = __popc(m0 & pre), a1 = __popc(m1 & pre);
+    const int b0 = c0 - a0, b1 = c1 - a1, b2 = (n - cs) - b0 - b1;
+    double acc = T3[t3o[cs * (n + 1) + a0] + a1];
+    acc = __dadd_rn(acc, P[b0]);
+    acc = __dadd_rn(acc, P[b1]);
+    acc = __dadd_rn(acc, P[b2]);
+    best = dmax(best, __dsub_rn(E2[cs], -acc));
+  }
+  return dmax(0.0, __dadd_rn(hq, best));
+}
+
+constexpr int kMemoMaxThreads = 768;
+
+__global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Tables tb,
+                                                               const double* __restrict__ memo,
+                                                               PairSpace ps, double cpar, int est,
+                                                               StatsOut out, double* ocells,
+                                                               unsigned long long* counters) {
+  extern __shared__ __align__(16) double msm[];
+  const int n = vs.n, B = tb.B;
+  const MemoLayout L = memo_layout(n);
+  {
+    const double2* src = reinterpret_cast<const double2*>(memo);
+    double2* dst = reinterpret_cast<double2*>(msm);
+    for (int i = threadIdx.x; i < (L.total + 1) / 2; i += blockDim.x) dst[i] = src[i];
+  }
+  __shared__ double lg[8], lg2[8];
+  if (threadIdx.x < 8) {
+    lg[threadIdx.x] = threadIdx.x <= B ? tb.logi[threadIdx.x] : 0.0;
+    lg2[threadIdx.x] = threadIdx.x <= B ? tb.log2i[threadIdx.x] : 0.0;
+  }
+  __syncthreads();
+  // per-thread scratch column after the tables: n ints, stride blockDim.x
+  int* scr = reinterpret_cast<int*>(msm + ((L.total + 1) & ~1)) + threadIdx.x;
+  const int sstride = blockDim.x;
+  MemoCtx c;
+  c.tab = msm;
+  c.offk = reinterpret_cast<const int*>(msm + L.offk);
+  c.gq = reinterpret_cast<const int*>(msm + L.gq);
+  c.t3o = reinterpret_cast<const int*>(msm + L.t3o);
+  c.L = L;
+  c.n = n;
+  c.valid = prefix(n);
+  const int x2 = B / 2;  // 2 or 3
+  const bool has_y3 = B >= 6;
+  const int kh2 = max(1, (int)floor(cpar * (double)x2));
+  const int kh3 = max(1, (int)floor(cpar * 2.0));
+  unsigned long long work[kNumCounters] = {0, 0, 0, 0, 0, 0};
+  unsigned long long* wk = counters ? work : nullptr;
+
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long wl = blockIdx.x * (long long)blockDim.x + threadIdx.x; wl < ps.count; wl += stride) {
+    int va, vb;
+    pair_vars(ps, ps.first + wl, va, vb);
+    double o[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+#pragma unroll
+    for (int orient = 0; orient < 2; ++orient) {
+      // column variable X: rank bytes + run starts; row variable Y: label
+      // flags, H(Q), yhat.  Loaded per orientation to keep registers low.
+      const uint4* px = vs.rec + (size_t)(orient ? vb : va) * 6;
+      const uint4* py = vs.rec + (size_t)(orient ? va : vb) * 6;
+      uint32_t rx[8], fy[8];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const uint4 u = __ldg(px + i), v = __ldg(py + 2 + i);
+        rx[4 * i] = u.x, rx[4 * i + 1] = u.y, rx[4 * i + 2] = u.z, rx[4 * i + 3] = u.w;
+        fy[4 * i] = v.x, fy[4 * i + 1] = v.y, fy[4 * i + 2] = v.z, fy[4 * i + 3] = v.w;
+      }
+      uint32_t m2 = 0, m3a = 0, m3b = 0;
+#pragma unroll
+      for (int sidx = 0; sidx < 32; ++sidx) {
+        if (sidx < n) {
+          const uint32_t pos = byte_of(rx, sidx), f = byte_of(fy, sidx);
+          m2 |= (f & 1u) << pos;
+          m3a |= ((f >> 1) & 1u) << pos;
+          m3b |= ((f >> 2) & 1u) << pos;
+        }
+      }
+      const uint4 sx = __ldg(px + 5), hy = __ldg(py + 4), sy = __ldg(py + 5);
+      const uint32_t rsm = sx.x;
+      const int yh2 = sy.y & 0xff, yh3 = (sy.y >> 8) & 0xff;
+      const double hq2 = __hiloint2double(hy.y, hy.x);
+      const double hq3 = __hiloint2double(hy.w, hy.z);
+      if (yh2 >= 2) {
+        double i2, i3;
+        memo_y2(c, m2, rsm, x2, kh2, hq2, i2, i3, wk, scr, sstride);
+        o[orient][0] = norm_cell(i2, lg[2], lg[yh2]);
+        if (x2 >= 3) o[orient][orient ? 2 : 1] = norm_cell(i3, lg[3], lg[yh2]);
+      }
+      if (has_y3 && yh3 >= 2) {
+        double i2, dummy;
+        if (yh3 == 3)
+          i2 = memo_y3_rows3(c, m3a, m3b, rsm, kh3, hq3, wk);
+        else
+          memo_y2(c, m3a, rsm, 2, kh3, hq3, i2, dummy, wk, scr, sstride);
+        o[orient][orient ? 1 : 2] = norm_cell(i2, lg[2], lg[yh3]);
+      }
+    }
+    small_stats(o, has_y3 ? 3 : 1, est, lg2, out, wl, ocells);
+  }
+  if (counters) flush_work(work, counters);
 }
 
 // ---------------------------------------------------------------------------
@@ -479,7 +894,8 @@ __global__ void __launch_bounds__(kGenThreads) k_general(VarSet vs, Tables tb, P
                                                          double* __restrict__ ocells,
                                                          double* __restrict__ fscratch,
                                                          SubDebug dbg, int has_dbg,
-                                                         int orient_only, int f_smem) {
+                                                         int orient_only, int f_smem,
+                                                         unsigned long long* counters) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = vs.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int norient = orient_only >= 0 ? 1 : 2;
@@ -584,6 +1000,12 @@ __global__ void __launch_bounds__(kGenThreads) k_general(VarSet vs, Tables tb, P
   }
   __syncthreads();
 
+  if (counters && tid == 0) {
+    unsigned long long w[kNumCounters] = {0, 0, 0, 0, 0, 0};
+    subproblem_work(rows, k, x_max, w);
+    for (int i = 0; i < kNumCounters; ++i)
+      if (w[i]) atomicAdd(counters + i, w[i]);
+  }
   if (has_dbg && tid == 0) {
     *dbg.row_count = rows;
     *dbg.raw_k = kraw;
@@ -764,10 +1186,45 @@ void launch_pack_tiny(const VarSet& vs, cudaStream_t s) {
 }
 
 void launch_tiny_pairs(const VarSet& vs, const Tables& tb, const PairSpace& ps, double c, int est,
-                       StatsOut out, double* o_cells, cudaStream_t s) {
+                       StatsOut out, double* o_cells, unsigned long long* counters,
+                       cudaStream_t s) {
   if (ps.count <= 0) return;
   const unsigned blocks = (unsigned)((ps.count + 127) / 128);
-  k_tiny_pairs<<<blocks, 128, 0, s>>>(vs, tb, ps, c, est, out, o_cells);
+  k_tiny_pairs<<<blocks, 128, 0, s>>>(vs, tb, ps, c, est, out, o_cells, counters);
+}
+
+size_t memo_doubles(int n) { return (size_t)memo_layout(n).total; }
+
+bool memo_fits(int n, int B) {
+  // tables + at least 8 warps of n-int scratch columns in 226 KB
+  return n >= 2 && n <= 32 && B <= 7 &&
+         (memo_doubles(n) + 1) * sizeof(double) + sizeof(int) * (size_t)n * 256 <= 226 * 1024;
+}
+
+void launch_build_memo(const Tables& tb, double* memo, int n, cudaStream_t s) {
+  k_build_memo<<<1, 256, 0, s>>>(tb, memo, n);
+}
+
+void launch_pack_memo(const VarSet& vs, cudaStream_t s) {
+  k_pack_memo<<<(vs.V + 127) / 128, 128, 0, s>>>(vs);
+}
+
+void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo, const PairSpace& ps,
+                       double c, int est, StatsOut out, double* o_cells,
+                       unsigned long long* counters, cudaStream_t s) {
+  if (ps.count <= 0) return;
+  const size_t tab = ((memo_doubles(vs.n) + 1) & ~size_t(1)) * sizeof(double);
+  const size_t budget = 226 * 1024 - tab;
+  int threads = (int)std::min<size_t>(kMemoMaxThreads, budget / (sizeof(int) * vs.n)) / 32 * 32;
+  threads = std::max(threads, 32);
+  const size_t sm = tab + sizeof(int) * (size_t)vs.n * threads;
+  cudaFuncSetAttribute(k_memo_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long need = (ps.count + threads - 1) / threads;
+  const unsigned blocks = (unsigned)std::min<long long>(sms, need);
+  k_memo_pairs<<<blocks, threads, sm, s>>>(vs, tb, memo, ps, c, est, out, o_cells, counters);
 }
 
 size_t general_smem_bytes(int n, const YParams& yp, bool f_in_smem) {
@@ -780,7 +1237,8 @@ bool general_f_fits(int n, const YParams& yp) {
 
 void launch_general(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
                     long long npairs, const YParams& yp, double* ocells, double* fscratch,
-                    const SubDebug* dbg, int orient_only, cudaStream_t s) {
+                    const SubDebug* dbg, int orient_only, unsigned long long* counters,
+                    cudaStream_t s) {
   if (npairs <= 0) return;
   const bool fs = fscratch == nullptr;
   const size_t sm = general_smem_bytes(vs.n, yp, fs);
@@ -789,7 +1247,7 @@ void launch_general(const VarSet& vs, const Tables& tb, const PairSpace& ps, lon
   SubDebug d{};
   if (dbg) d = *dbg;
   k_general<<<blocks, kGenThreads, sm, s>>>(vs, tb, ps, base, yp, ocells, fscratch, d,
-                                            dbg ? 1 : 0, orient_only, fs ? 1 : 0);
+                                            dbg ? 1 : 0, orient_only, fs ? 1 : 0, counters);
 }
 
 void launch_reduce(const Tables& tb, long long npairs, const double* ocells, int est, StatsOut out,

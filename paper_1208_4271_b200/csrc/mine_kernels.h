@@ -26,6 +26,12 @@ struct VarSet {
   double* hq = nullptr;          // V x ny     H(Q), reference-exact (mutual_info.cpp:33)
   uint8_t* lw = nullptr;         // V x n      tiny tier: packed labels (y=2: bits 0-1, y=3: 2-3)
   uint32_t* rsmask = nullptr;    // V          tiny tier: run-start bitmask over sorted positions
+  uint4* rec = nullptr;          // V x 6      memo tier: 96-byte per-variable record
+};
+
+// Memo-tier table layout (offsets in doubles), see mine_kernels.cu.
+struct MemoLayout {
+  int n, k2, t3, w2, e2, r1, pln, offk, gq, t3o, total;
 };
 
 // Host-built constant tables (glibc libm, the reference's own arithmetic).
@@ -65,6 +71,14 @@ struct StatsOut {
   double* tic = nullptr;
 };
 
+// Realised-work counters: algorithmic FP64 ops of the
+// reference arithmetic, p*log(p) lookups, DP candidates, span entries,
+// subproblems.
+enum { kCntFp64 = 0, kCntLookups, kCntCand, kCntSpans, kCntSub, kCntGathers, kNumCounters };
+// kCntGathers: shared-memory table gathers the executing tier actually needs
+// (memo tier: one per F(t,2) candidate, ...); the other counters describe the
+// reference's own arithmetic, independent of the tier.
+
 // Parameters of one row target for the general tier.
 struct YParams {
   int y, yi, x_max, k_hat;
@@ -90,7 +104,17 @@ void launch_pack_tiny(const VarSet& vs, cudaStream_t s);
 // Tiny tier (n <= 32, B <= 7): one thread per pair, stats (and optionally the
 // per-orientation cells o1/o2, ncell each per pair) written directly.
 void launch_tiny_pairs(const VarSet& vs, const Tables& tb, const PairSpace& ps, double c,
-                       int est, StatsOut out, double* o_cells, cudaStream_t s);
+                       int est, StatsOut out, double* o_cells, unsigned long long* counters,
+                       cudaStream_t s);
+
+// Memo tier (n <= 25, B <= 7): every F(t,2) candidate precomputed per n.
+size_t memo_doubles(int n);
+bool memo_fits(int n, int B);
+void launch_build_memo(const Tables& tb, double* memo, int n, cudaStream_t s);
+void launch_pack_memo(const VarSet& vs, cudaStream_t s);
+void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo, const PairSpace& ps,
+                       double c, int est, StatsOut out, double* o_cells,
+                       unsigned long long* counters, cudaStream_t s);
 
 // General tier: one CTA per (pair, orientation) for one row target; writes the
 // normalised per-orientation cells into ocells[(pair - base) * 2 * ncell ...].
@@ -100,7 +124,8 @@ size_t general_smem_bytes(int n, const YParams& yp, bool f_in_smem);
 bool general_f_fits(int n, const YParams& yp);
 void launch_general(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
                     long long npairs, const YParams& yp, double* ocells, double* fscratch,
-                    const SubDebug* dbg, int orient_only, cudaStream_t s);
+                    const SubDebug* dbg, int orient_only, unsigned long long* counters,
+                    cudaStream_t s);
 void launch_reduce(const Tables& tb, long long npairs, const double* ocells, int est,
                    StatsOut out, long long out_offset, cudaStream_t s);
 

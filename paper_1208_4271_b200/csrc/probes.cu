@@ -1,0 +1,78 @@
+// Measurement probes (bench.py only, not part of the engine ABI): the
+// sustained FP64 add rate and the shared-memory 8-byte gather rate of this
+// B200, the denominators of the roofline for the exact MINE DP, which is
+// neither HBM- nor tensor-core-bound.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace {
+
+constexpr int kChains = 8;
+
+__global__ void k_dadd(double* out, int iters, double inc) {
+  double a[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) a[c] = threadIdx.x * 1e-3 + c;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(a[c]) : "d"(inc));
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) s += a[c];
+  if (s == 12345.678) out[0] = s;
+}
+
+// Random 8-byte gathers from a 561-entry shared table (the tiny tier's
+// p*log(p) table size), 8 independent streams per thread.
+__global__ void k_lds(double* out, int iters) {
+  __shared__ double tab[561];
+  for (int i = threadIdx.x; i < 561; i += blockDim.x) tab[i] = i * 0.5;
+  __syncthreads();
+  uint32_t st = 2654435761u * (threadIdx.x + 1) + blockIdx.x;
+  double acc = 0;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+      st = st * 1664525u + 1013904223u;
+      acc += tab[(st >> 8) % 561u];
+    }
+  }
+  if (acc == 12345.678) out[0] = acc;
+}
+
+template <typename F>
+float time_ms(F&& launch) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  launch();  // warm-up
+  cudaEventRecord(a);
+  launch();
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return ms;
+}
+
+}  // namespace
+
+extern "C" int mine_b200_probe(int device, double* dadd_per_s, double* lds_per_s) {
+  if (cudaSetDevice(device) != cudaSuccess) return -1;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  double* out = nullptr;
+  if (cudaMalloc(&out, sizeof(double)) != cudaSuccess) return -1;
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  float ms = time_ms([&] { k_dadd<<<blocks, threads>>>(out, iters, 1e-9); });
+  *dadd_per_s = (double)blocks * threads * iters * kChains / (ms * 1e-3);
+  const int liters = 2048;
+  ms = time_ms([&] { k_lds<<<blocks, threads>>>(out, liters); });
+  *lds_per_s = (double)blocks * threads * liters * kChains / (ms * 1e-3);
+  cudaFree(out);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}

@@ -39,9 +39,15 @@ class MineStatsOut(ctypes.Structure):
     _fields_ = [(k, _dp) for k in STATS] + [("cells", _dp)]
 
 
+NCOUNTERS = 6
+COUNTERS = ("fp64_ops", "lookups", "dp_candidates", "span_entries", "subproblems", "gathers")
+
+
 class MineOpts(ctypes.Structure):
     _fields_ = [("device_io", ctypes.c_int), ("async_", ctypes.c_int), ("stream", ctypes.c_void_p),
-                ("tier", ctypes.c_int), ("first", ctypes.c_longlong), ("count", ctypes.c_longlong)]
+                ("tier", ctypes.c_int), ("first", ctypes.c_longlong), ("count", ctypes.c_longlong),
+                ("counters", ctypes.POINTER(ctypes.c_ulonglong)), ("ev_begin", ctypes.c_void_p),
+                ("ev_end", ctypes.c_void_p)]
 
 
 class MineProblem(ctypes.Structure):
@@ -280,17 +286,36 @@ class Engine:
 
     def pairwise_device(self, vars_ptr: int, p: int, n: int, params: Parameters, out_ptrs: dict,
                         stream: int = 0, first: int = 0, count: int = 0, tier: int = 0,
-                        async_: bool = True):
+                        async_: bool = True, counters: bool = False, ev_begin: int = 0,
+                        ev_end: int = 0):
         """Device-resident variant (torch tensors' data_ptr()s): inputs and
-        outputs in HBM, enqueued on `stream`."""
+        outputs in HBM, enqueued on `stream`.  counters=True returns the
+        realised-work totals (synchronises)."""
         so = MineStatsOut()
         for k in STATS:
             setattr(so, k, ctypes.cast(ctypes.c_void_p(out_ptrs[k]), _dp) if out_ptrs.get(k) else None)
         o = self._opts(first, count, tier)
         o.device_io, o.async_, o.stream = 1, int(async_), ctypes.c_void_p(stream)
+        cnt = (ctypes.c_ulonglong * NCOUNTERS)()
+        if counters:
+            o.counters = cnt
+        o.ev_begin, o.ev_end = ctypes.c_void_p(ev_begin or None), ctypes.c_void_p(ev_end or None)
         self._check(self.L.mine_b200_pairwise(self.ctx, ctypes.c_void_p(vars_ptr), p, n,
                                               ctypes.byref(params._c()), ctypes.byref(o),
                                               ctypes.byref(so)))
+        return dict(zip(COUNTERS, list(cnt))) if counters else None
+
+    def pairwise_host(self, vars_np: np.ndarray, params: Parameters, outs: dict, first: int = 0,
+                      count: int = 0):
+        """The reference-facing call with HOST buffers (e2e leg): H2D of the
+        variables, scoring, D2H of the requested statistics into `outs`
+        (preallocated, ideally pinned, numpy arrays)."""
+        so = MineStatsOut()
+        for k in STATS:
+            setattr(so, k, outs[k].ctypes.data_as(_dp) if k in outs else None)
+        p, n = vars_np.shape
+        self._check(self.L.mine_b200_pairwise(self.ctx, _ptr(vars_np), p, n, ctypes.byref(params._c()),
+                                              ctypes.byref(self._opts(first, count)), ctypes.byref(so)))
 
     def debug_subproblem(self, col_var, row_var, y_target: int, x_max: int, k_hat: int):
         """GPU general-tier partition + DP of one (orientation, y) subproblem

@@ -63,15 +63,18 @@ def test_debug_subproblem_bit_exact(engine, oracle, seed):
         assert_bit_equal(g["values"], o["values"], ctx)
 
 
-@pytest.mark.parametrize("tier", [0, 2])
-def test_tiny_shapes_bit_exact(engine, oracle, tier):
-    """n <= 32, B <= 7: the tiny tier (tier 0 -> auto) and the general tier
-    must both match the oracle bit for bit."""
+@pytest.mark.parametrize("tier", [0, 1, 2, 3])
+def test_small_shapes_bit_exact(engine, oracle, tier):
+    """n <= 32, B <= 7: the memo tier (auto / 3, n <= 24), the tiny tier (1)
+    and the general tier (2) must all match the oracle bit for bit, including
+    ties, monotone and constant variables and superclumping (small c)."""
     rng = np.random.default_rng(7 + tier)
-    for it in range(60):
-        n = int(rng.integers(2, 26))
-        alpha = [0.6, 0.5, 0.55][it % 3]
-        c = [15.0, 1.0, 2.0][it % 3]
+    for it in range(80):
+        n = int(rng.integers(2, 25 if tier == 3 else 33))
+        alpha = [0.6, 0.5, 0.55, 0.45][it % 4]
+        if grid_bound(n, alpha) > 7:
+            alpha = 0.5 if grid_bound(n, 0.5) <= 7 else 0.4
+        c = [15.0, 1.0, 2.0, 0.7][it % 4]
         x, y = random_pair(rng, n, it % 4)
         res = engine.pairs(np.stack([x, y]), [0], [1], Parameters(alpha, c), cells=True, tier=tier)
         b, o1, o2, m = oracle.score(x, y, alpha, c)
@@ -122,14 +125,15 @@ def test_identity_and_constant(engine):
     assert c["mic"] == 0.0 and c["mcn"] == 2.0
 
 
-def test_c1_pairwise_bit_exact(engine, oracle):
-    """Config c1's shape (n=23, B=6, tiny tier): a 300-variable slice, all
-    pairs, against the oracle."""
+@pytest.mark.parametrize("tier", [0, 1, 2])
+def test_c1_pairwise_bit_exact(engine, oracle, tier):
+    """Config c1's shape (n=23, B=6): a 300-variable slice, all pairs, against
+    the oracle, through every tier that admits it."""
     w = datagen.make(1)
     V = w.X[:300]
-    res = engine.pairwise(V)
+    res = engine.pairwise(V, tier=tier)
     want = oracle.pairwise(V)
-    assert_bit_equal(stats_matrix(res), want, "c1 slice")
+    assert_bit_equal(stats_matrix(res), want, f"c1 slice tier={tier}")
 
 
 def test_c0_pairs_bit_exact(engine, oracle):
