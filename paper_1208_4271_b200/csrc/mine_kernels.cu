@@ -162,7 +162,13 @@ __global__ void k_sort_vars(VarSet vs) {
   int* tmp = rs + n;
   const int var = blockIdx.x;
   const double* src = vs.vals + (size_t)var * n;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) v[i] = src[i];
+  // NaN would break the total order and leave holes in perm; such inputs are
+  // rejected after the call (k_check_finite), but the pipeline must stay
+  // memory-safe until then, so NaN sorts as +inf here.
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double x = src[i];
+    v[i] = isnan(x) ? HUGE_VAL : x;
+  }
   __syncthreads();
   int* perm = vs.perm + (size_t)var * n;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {

@@ -141,3 +141,150 @@ def test_c0_pairs_bit_exact(engine, oracle):
     res = engine.pairs(w.X, w.xi, w.yi, Parameters(w.alpha, w.c, w.est))
     want = oracle.pairs(w.X, w.xi, w.yi, w.alpha, w.c, w.est)
     assert_bit_equal(stats_matrix(res), want, "c0")
+
+
+# --- against the committed golden fixtures (the reference's own outputs) ----
+GOLDEN = __import__("os").path.join(__import__("os").path.dirname(__file__), "golden")
+
+
+def _golden(name):
+    return np.load(__import__("os").path.join(GOLDEN, name))
+
+
+@pytest.mark.parametrize("tier", [0, 2])
+def test_golden_pairs_gpu(engine, tier):
+    g = _golden("ref_pairs.npz")
+    for i in range(len(g["n"])):
+        x = g["x"][g["off"][i]:g["off"][i + 1]]
+        y = g["y"][g["off"][i]:g["off"][i + 1]]
+        alpha, c = float(g["alpha"][i]), float(g["c"][i])
+        if tier == 2 and len(x) <= 3:
+            continue
+        res = engine.pairs(np.stack([x, y]), [0], [1], Parameters(alpha, c), cells=True, tier=tier)
+        cells = res["cells"][0]
+        m = np.where(cells[1] > cells[0], cells[1], cells[0])
+        assert_bit_equal(m, g["cells"][g["coff"][i]:g["coff"][i + 1]], f"case {i}")
+        assert_bit_equal(stats_matrix(res)[0, :4], g["stats"][i], f"case {i}")
+
+
+def test_golden_subproblems_gpu(engine):
+    g = _golden("ref_subproblems.npz")
+    for i, (n, yt, xm, kh, rc, raw, k) in enumerate(g["meta"]):
+        x = g["x"][g["off"][i]:g["off"][i + 1]]
+        y = g["y"][g["off"][i]:g["off"][i + 1]]
+        d = engine.debug_subproblem(x, y, int(yt), int(xm), int(kh))
+        assert (d["row_count"], d["clump_count"], d["k"]) == (rc, raw, k), i
+        assert d["h_q"] == g["h_q"][i]
+        assert (d["bounds"] == g["bounds"][g["boff"][i]:g["boff"][i + 1]]).all()
+        assert_bit_equal(d["values"], g["values"][g["voff"][i]:g["voff"][i + 1]], f"sub {i}")
+
+
+def test_golden_configs_gpu(engine):
+    g = _golden("ref_configs.npz")
+    assert_bit_equal(stats_matrix(engine.pairwise(g["c1_vars"]))[:, :4], g["c1_stats"], "c1")
+    V = g["c0_vars"]
+    r = engine.pairs(V, np.arange(0, len(V), 2), np.arange(1, len(V), 2))
+    assert_bit_equal(stats_matrix(r)[:, :4], g["c0_stats"], "c0")
+    r = engine.pairwise(g["c2_vars"], Parameters(0.6, 15.0, MIC_E))
+    assert_bit_equal(stats_matrix(r)[:, :4], g["c2_stats"], "c2")
+    assert_bit_equal(stats_matrix(engine.pairwise(g["c3_vars"]))[:, :4], g["c3_stats"], "c3")
+    r = engine.cross(g["c4r_X"], g["c4r_Y"], Parameters(0.75, 15.0, MIC_E))
+    assert_bit_equal(stats_matrix(r)[:, :4], g["c4r_stats"], "c4 (n=1500)")
+
+
+# --- config-scale parity and size-independent properties ---------------------
+def test_c2_poisson_ties_slice(engine, oracle):
+    """c2 (heavy ties / zeros): 12 variables -> 66 pairs, est = MIC_e."""
+    w = datagen.make(2)
+    V = w.X[[0, 1, 2, 3, 10, 11, 500, 501, 1000, 1001, 1998, 1999]]
+    res = engine.pairwise(V, Parameters(w.alpha, w.c, w.est))
+    want = oracle.pairwise(V, w.alpha, w.c, w.est)
+    assert_bit_equal(stats_matrix(res), want, "c2 slice")
+
+
+def test_c3_slice_and_monotone_invariance(engine, oracle):
+    """c3 at full n=1340: 6 variables vs the oracle, and M is rank-invariant
+    (SURVEY A3): a strictly monotone transform changes nothing."""
+    w = datagen.make(3)
+    V = w.X[:6]
+    res = engine.pairwise(V)
+    assert_bit_equal(stats_matrix(res), oracle.pairwise(V), "c3 slice")
+    T = np.stack([np.exp(V[0] / 4), V[1] ** 3, np.tanh(V[2] / 4), V[3], 3 * V[4] + 1, V[5]])
+    assert_bit_equal(stats_matrix(engine.pairwise(T)), stats_matrix(res), "monotone")
+
+
+def test_full_size_properties_c0(engine):
+    """All 256 c0 pairs at full size: swap invariance (test_statistics.cpp:
+    114-132), MAS/MEV <= MIC, MCN range, and c-saturation
+    (test_char_matrix.cpp:111-121)."""
+    w = datagen.make(0)
+    p = Parameters(w.alpha, w.c, w.est)
+    a = engine.pairs(w.X, w.xi, w.yi, p)
+    b = engine.pairs(w.X, w.yi, w.xi, p)
+    for k in ("mic", "mas", "mev", "mcn", "mic_e"):
+        assert_bit_equal(a[k], b[k], f"swap {k}")
+    assert np.all(a["mas"] <= a["mic"]) and np.all(a["mev"] <= a["mic"])
+    assert np.all(a["mcn"] >= 2.0) and np.all(a["mcn"] <= np.log2(grid_bound(1000, 0.6)))
+    assert np.all((a["mic"] >= 0) & (a["mic"] <= 1)) and np.all(a["mic_e"] <= 1)
+    # functional noiseless pairs (sigma = 0: pairs i with i % 4 == 0, f not indep.)
+    noiseless = [i for i in range(256) if i % 4 == 0 and i % 5 != 4]
+    assert np.all(a["mic"][noiseless] > 0.9)
+    sub = list(range(0, 256, 17))
+    s1 = engine.pairs(w.X, w.xi[sub], w.yi[sub], Parameters(0.6, 1000.0))
+    s2 = engine.pairs(w.X, w.xi[sub], w.yi[sub], Parameters(0.6, 3000.0))
+    for k in STAT_COLS:
+        assert_bit_equal(s1[k], s2[k], f"c-saturation {k}")
+
+
+def test_batch_slicing_is_bitwise_stable(engine):
+    """Any (first, count) window of the pair space gives the same bits as the
+    full batch (the multi-GPU sharding contract)."""
+    w = datagen.make(1)
+    V = w.X[:200]
+    full = engine.pairwise(V)
+    total = 200 * 199 // 2
+    for first, count in ((0, 1), (5, 1000), (7000, total - 7000), (total - 3, 3)):
+        part = engine.pairwise(V, first=first, count=count)
+        for k in STAT_COLS:
+            assert_bit_equal(part[k], full[k][first:first + count], f"{k} window {first}")
+
+
+def test_minepy_c_api(engine, oracle):
+    """mine_compute_score / mine_mic ... and mine_compute_pstats through the
+    C ABI (the minepy-style drop-in names)."""
+    import ctypes
+    from paper_1208_4271_b200 import engine as E
+    L = E.load_library()
+    rng = np.random.default_rng(3)
+    x = rng.uniform(0, 1, 300)
+    y = np.sin(6 * x) + rng.normal(0, 0.2, 300)
+    prob = E.MineProblem(300, x.ctypes.data_as(E._dp), y.ctypes.data_as(E._dp))
+    par = E.MineParameter(0.6, 15.0, 0)
+    sc = L.mine_compute_score(ctypes.byref(prob), ctypes.byref(par))
+    assert sc, L.mine_b200_last_error()
+    want = oracle.statistics(x, y)
+    got = [L.mine_mic(sc), L.mine_mas(sc), L.mine_mev(sc), L.mine_mcn(sc, 0.0), L.mine_mic_e(sc)]
+    assert_bit_equal(np.array(got), want[:5], "mine_* accessors")
+    b, o1, o2, m = oracle.score(x, y)
+    assert abs(L.mine_tic(sc, 0) - m.sum()) < 1e-9
+    L.mine_free_score(ctypes.byref(sc))
+    # invalid input -> NULL + message
+    bad = np.array([1.0, np.nan, 2.0])
+    prob = E.MineProblem(3, bad.ctypes.data_as(E._dp), bad.ctypes.data_as(E._dp))
+    assert not L.mine_compute_score(ctypes.byref(prob), ctypes.byref(par))
+    assert b"finite" in L.mine_b200_last_error()
+
+
+def test_errors_like_the_reference(engine):
+    """char_matrix.cpp:11-15,71-75: validation failures raise."""
+    from paper_1208_4271_b200 import MineError
+    with pytest.raises(MineError):
+        engine.compute_statistics([1, 2, 3], [1, 2])
+    with pytest.raises(MineError):
+        engine.compute_statistics([1.0], [2.0])
+    with pytest.raises(MineError):
+        engine.compute_statistics([1, 2, np.inf, 4], [1, 2, 3, 4])
+    with pytest.raises(MineError):
+        engine.compute_statistics([1, 2, 3, 4], [1, 2, 3, 4], Parameters(0.6, -1.0))
+    with pytest.raises(MineError):
+        engine.pairwise(np.zeros((3, 5)), first=2, count=5)
