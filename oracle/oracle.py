@@ -29,11 +29,15 @@ _dp = ctypes.POINTER(ctypes.c_double)
 _ip = ctypes.POINTER(ctypes.c_int)
 
 
-def build(reference: bool = True) -> None:
-    """Build the C restatement, and the reference .so when its sources exist."""
+def build(reference: bool = True, reference_tests: bool = False) -> None:
+    """Build the C restatement, and the reference .so (plus, on request, the
+    reference's own test binaries against the GPU adapter) when its sources
+    exist."""
     subprocess.run(["make", "-s", "-C", HERE, os.path.join("_ref", "libmine_oracle.so")], check=True)
     if reference and os.path.isdir(REFERENCE_SRC):
         subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+        if reference_tests:
+            subprocess.run(["make", "-s", "-C", HERE, "ref-tests"], check=True)
 
 
 def _d(a: np.ndarray):

@@ -485,6 +485,15 @@ mine_b200_ctx* mine_b200_create(int device) {
     CK(cudaGetDeviceProperties(&prop, device));
     if (prop.major < 10) throw Failure("mine_b200: needs an sm_100 (Blackwell) GPU");
     CK(cudaSetDevice(device));
+    {
+      static std::mutex init_mu;
+      static std::vector<int> inited;
+      std::lock_guard<std::mutex> lk(init_mu);
+      if (std::find(inited.begin(), inited.end(), device) == inited.end()) {
+        CK(init_kernel_attributes(device));
+        inited.push_back(device);
+      }
+    }
     std::unique_ptr<mine_b200_ctx> c(new mine_b200_ctx());
     c->device = device;
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));

@@ -1169,6 +1169,28 @@ __global__ void k_reduce(Tables tb, long long npairs, const double* __restrict__
 
 // ---------------------------------------------------------------------------
 // Launchers.
+
+// Opt every dynamic-shared-memory kernel into the device maximum once per
+// device.  Setting it per launch would race between host threads that use
+// different sizes (a smaller value set by one thread fails another's launch).
+cudaError_t init_kernel_attributes(int device) {
+  int optin = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (e != cudaSuccess) return e;
+  const void* fns[] = {reinterpret_cast<const void*>(k_sort_vars),
+                       reinterpret_cast<const void*>(k_memo_pairs),
+                       reinterpret_cast<const void*>(k_general)};
+  for (const void* f : fns) {
+    cudaFuncAttributes fa{};
+    e = cudaFuncGetAttributes(&fa, f);
+    if (e != cudaSuccess) return e;
+    // static + dynamic shared memory must fit the opt-in limit
+    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin - (int)fa.sharedSizeBytes);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
 void launch_check_finite(const double* v, long long count, int* flag, cudaStream_t s) {
   const int blocks = (int)std::min<long long>(4 * 148, (count + 255) / 256 + 1);
   k_check_finite<<<blocks, 256, 0, s>>>(v, count, flag);
@@ -1177,7 +1199,6 @@ void launch_check_finite(const double* v, long long count, int* flag, cudaStream
 void launch_sort_vars(const VarSet& vs, cudaStream_t s) {
   const int threads = vs.n <= 256 ? 128 : (vs.n <= 2048 ? 256 : 1024);
   const size_t sm = sizeof(double) * vs.n + sizeof(int) * (vs.n + 64);
-  if (sm > 48 * 1024) cudaFuncSetAttribute(k_sort_vars, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_sort_vars<<<vs.V, threads, sm, s>>>(vs);
 }
 
@@ -1224,7 +1245,6 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo, c
   int threads = (int)std::min<size_t>(kMemoMaxThreads, budget / (sizeof(int) * vs.n)) / 32 * 32;
   threads = std::max(threads, 32);
   const size_t sm = tab + sizeof(int) * (size_t)vs.n * threads;
-  cudaFuncSetAttribute(k_memo_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1248,7 +1268,6 @@ void launch_general(const VarSet& vs, const Tables& tb, const PairSpace& ps, lon
   if (npairs <= 0) return;
   const bool fs = fscratch == nullptr;
   const size_t sm = general_smem_bytes(vs.n, yp, fs);
-  cudaFuncSetAttribute(k_general, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const unsigned blocks = (unsigned)(npairs * (orient_only >= 0 ? 1 : 2));
   SubDebug d{};
   if (dbg) d = *dbg;

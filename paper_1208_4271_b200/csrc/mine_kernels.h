@@ -96,6 +96,8 @@ struct SubDebug {
 };
 
 // ---- launchers ------------------------------------------------------------
+// Must run once per device (under a lock) before any launch.
+cudaError_t init_kernel_attributes(int device);
 void launch_check_finite(const double* v, long long count, int* flag, cudaStream_t s);
 void launch_sort_vars(const VarSet& vs, cudaStream_t s);
 void launch_equipartition(const VarSet& vs, const Tables& tb, cudaStream_t s);
