@@ -271,9 +271,16 @@ def run_ours(args, world, rank, local):
         kern_s = statistics.mean(kern_ms) / 1e3
         gathers = work["gathers"]
         achieved = gathers / kern_s / 1e9
+        traffic = None
+        try:
+            t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))["k_memo_pairs"]
+            traffic = int(t["dram_bytes_read"] + t["dram_bytes_write"])
+        except Exception:
+            pass
         roof = {"bound": "lsu", "achieved": achieved, "peak": lds / 1e9 if lds else None,
                 "unit": "Ggather/s", "frac": achieved / (lds / 1e9) if lds else None,
-                "traffic": None,
+                "traffic": traffic,
+                "traffic_source": "profiles/ncu_traffic.json (dram read+write bytes per launch, ncu)",
                 "kernel": "k_memo_pairs (the pair-scoring launch of a step)",
                 "per_launch_work": {k: int(v) * world for k, v in work.items()},
                 "work_unit": "8-byte shared-memory table gathers the memo-tier algorithm needs "
