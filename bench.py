@@ -317,8 +317,69 @@ def run_ours(args, world, rank, local):
         dist.destroy_process_group()
 
 
+def run_config(args):
+    """Secondary measurement on another BASELINE config (not the headline):
+    device-resident pairs/s over a bounded window of the config's pair space,
+    plus the reference CPU engine on a subsample of the same window."""
+    import torch
+    from paper_1208_4271_b200 import Engine, Parameters, datagen
+    w = datagen.make(args.config)
+    eng = Engine(0)
+    params = Parameters(w.alpha, w.c, w.est)
+    total = w.npairs
+    count = min(total, args.pairs) if args.pairs else total
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    cnt = None
+
+    def call():
+        if w.call == "pairwise":
+            return eng.pairwise(w.X, params, first=0, count=count, stats=("mic", "tic"))
+        if w.call == "cross":
+            return eng.cross(w.X, w.Y, params, first=0, count=count, stats=("mic", "tic"))
+        return eng.pairs(w.X, w.xi[:count], w.yi[:count], params, stats=("mic", "tic"))
+
+    call()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        call()
+        times.append(time.perf_counter() - t0)
+    dt = statistics.median(times)
+    line = {"config": args.config, "call": w.call, "pairs": count, "n": w.n, "alpha": w.alpha,
+            "c": w.c, "est": w.est, "e2e_pairs_per_s": count / dt, "e2e_s": dt,
+            "launches": eng.last_launches}
+    if not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        orc = O.Oracle()
+        sub = max(1, min(count, args.cpu_pairs))
+        t0 = time.perf_counter()
+        if w.call == "pairwise":
+            ref = orc.pairwise(w.X, w.alpha, w.c, w.est, first=0, count=sub)
+        elif w.call == "cross":
+            idx = np.arange(sub)
+            ref = orc.pairs(np.concatenate([w.X, w.Y]), idx // w.Y.shape[0],
+                            w.X.shape[0] + idx % w.Y.shape[0], w.alpha, w.c, w.est)
+        else:
+            ref = orc.pairs(w.X, w.xi[:sub], w.yi[:sub], w.alpha, w.c, w.est)
+        cdt = time.perf_counter() - t0
+        got = call()
+        line["cpu_port_pairs_per_s"] = sub / cdt
+        line["cpu_sample_pairs"] = sub
+        line["cpu_cores"] = os.cpu_count()
+        line["bit_exact_on_sample"] = bool(np.array_equal(got["mic"][:sub].view(np.int64),
+                                                          ref[:, 0].view(np.int64)))
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=1,
+                    help="1 = the headline (c1); 0/2/3/4 = secondary timing of that config")
+    ap.add_argument("--pairs", type=int, default=0, help="secondary configs: pairs to time (0 = all)")
+    ap.add_argument("--cpu-pairs", type=int, default=200)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
@@ -332,7 +393,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world == 1 and args.gpus > 1:
         log(f"--gpus {args.gpus} without torchrun: running one rank")
-    if args.impl == "reference":
+    if args.config != 1:
+        run_config(args)
+    elif args.impl == "reference":
         run_reference(args, world, rank)
     else:
         run_ours(args, world, rank, local)

@@ -1,0 +1,138 @@
+// Device helpers shared by the kernel translation units (mine_kernels.cu,
+// mine_general.cu).  Everything here must round exactly like the reference:
+// the TUs are compiled with -fmad=false.
+#pragma once
+
+#include <cfloat>
+#include <cstdint>
+
+#include "mine_kernels.h"
+
+namespace mb200 {
+
+constexpr double kLowest = -DBL_MAX;  // std::numeric_limits<double>::lowest()
+
+__device__ __forceinline__ unsigned tri(unsigned m) { return m * (m + 1u) / 2u; }
+
+// std::max / std::min argument order (libstdc++): max(a,b) = a < b ? b : a.
+__device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }
+__device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = dmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_min_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_incl_scan(int v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  return v;
+}
+
+// In-place inclusive scan of a[0..n) in shared memory; each thread owns a
+// contiguous chunk.  tmp: >= 33 ints of shared scratch.  Returns the total.
+__device__ inline int block_incl_scan(int* a, int n, int* tmp) {
+  const int nt = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = (nt + 31) >> 5;
+  const int per = (n + nt - 1) / nt;
+  const int beg = min(tid * per, n), end = min(beg + per, n);
+  int s = 0;
+  for (int i = beg; i < end; ++i) s += a[i];
+  const int incl = warp_incl_scan(s);
+  if (lane == 31) tmp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int x = lane < nw ? tmp[lane] : 0;
+    x = warp_incl_scan(x);
+    if (lane < nw) tmp[lane] = x;
+  }
+  __syncthreads();
+  int run = incl - s + (warp ? tmp[warp - 1] : 0);
+  for (int i = beg; i < end; ++i) {
+    run += a[i];
+    a[i] = run;
+  }
+  const int total = tmp[nw - 1];
+  __syncthreads();
+  return total;
+}
+
+// PairSequence::at (analysis.cpp:66-81), 0-based.
+__device__ inline void pair_at(long long p, long long w, int& i, int& j) {
+  const long long total = p * (p - 1) / 2;
+  const long long r = total - w;
+  long long m = (long long)((sqrt(8.0 * (double)r + 1.0) - 1.0) / 2.0);
+  while (m * (m + 1) / 2 < r) ++m;
+  while (m >= 1 && (m - 1) * m / 2 >= r) --m;
+  const long long ii = p - m;
+  const long long row_start = total - m * (m + 1) / 2;
+  i = (int)(ii - 1);
+  j = (int)(ii + (w - row_start));
+}
+
+// Variables (x, y) of work item w: x is the column variable of orientation 0.
+__device__ __forceinline__ void pair_vars(const PairSpace& ps, long long w, int& vx, int& vy) {
+  if (ps.kind == kPairwise) {
+    pair_at(ps.p, w, vx, vy);
+  } else if (ps.kind == kCross) {
+    vx = (int)(w / ps.py);
+    vy = ps.px + (int)(w % ps.py);
+  } else {
+    vx = ps.xi[w];
+    vy = ps.yi[w];
+  }
+}
+
+// Realised algorithmic work of one exact subproblem (rows R, k clumps): the
+// FP64 operations the reference arithmetic itself requires (mutual_info.cpp:
+// 47-66 with every 0.0 + x start elided), its p*log(p) lookups, DP candidates
+// and span entries.  Used only when counters are requested.
+__device__ inline void subproblem_work(int R, int k, int x_max, unsigned long long* w,
+                                bool gathers_as_reference = true) {
+  if (k < 2) return;
+  const long long l_max = min(x_max, k), K = k;
+  const long long f2 = l_max >= 3 ? K * (K - 1) / 2 : K - 1;  // F(t,2) candidates
+  long long spans = 0, cand = 0;
+  if (l_max >= 3) {
+    spans = K - 2;                                             // t = k
+    if (l_max >= 4) spans += (K - 3) * (K - 2) / 2;            // t = 3 .. k-1
+    for (long long l = 3; l <= l_max; ++l) {
+      cand += K - l + 1;                                       // t = k
+      if (l <= l_max - 1) cand += (K - l) * (K - l + 1) / 2;   // t = l .. k-1
+    }
+  }
+  w[kCntFp64] += f2 * (2 * R + 2) + spans * (R + 2) + cand * 3;
+  w[kCntLookups] += f2 * (2 * R + 2) + spans * R;
+  if (gathers_as_reference) w[kCntGathers] += f2 * (2 * R + 2) + spans * R;
+  w[kCntCand] += cand;
+  w[kCntSpans] += spans;
+  w[kCntSub] += 1;
+}
+
+// Instrumented runs only (untimed): plain per-thread atomics, safe from any
+// divergent call site.
+__device__ inline void flush_work(const unsigned long long* w, unsigned long long* counters) {
+#pragma unroll
+  for (int i = 0; i < kNumCounters; ++i)
+    if (w[i]) atomicAdd(counters + i, w[i]);
+}
+
+// char_matrix.cpp:57-64: normalise by min(log l, log yhat); clamp at 1 and
+// keep the max with the zero-initialised slot (update_max :28-35).
+__device__ __forceinline__ double norm_cell(double I, double logl, double logy) {
+  const double norm = dmin(logl, logy);
+  double v = norm > 0.0 ? __ddiv_rn(I, norm) : 0.0;
+  if (v > 1.0) v = 1.0;
+  return 0.0 < v ? v : 0.0;
+}
+
+}  // namespace mb200

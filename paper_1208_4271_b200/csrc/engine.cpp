@@ -177,7 +177,7 @@ struct mine_b200_ctx {
   std::mutex mu;
   TableSet tables;
   DevBuf vals, perm, runid, runstart, nruns, q, yhat, hq, lw, rsmask;
-  DevBuf ocells, fscratch, stats, flag, idx, counters, memo, rec;
+  DevBuf ocells, fscratch, stats, flag, idx, counters, memo, rec, gscr, gqueue;
   int memo_n = -1;
   std::vector<cudaEvent_t> events;
   long long launches = 0;
@@ -211,6 +211,29 @@ cudaEvent_t ctx_event(mine_b200_ctx* ctx, size_t i) {
     ctx->events.push_back(e);
   }
   return ctx->events[i];
+}
+
+// Scratch of the general tier for `nsub` subproblems at one row target (the
+// layout depends on y; one buffer is reused across y and chunks).
+GenScratch gen_scratch(mine_b200_ctx* ctx, int n, const YParams& yp, long long nsub) {
+  GenScratch g;
+  g.kc = gen_kc(n, yp);
+  g.cum_stride = (size_t)yp.y * (g.kc + 1);
+  auto a16 = [](size_t x) { return (x + 15) & ~size_t(15); };
+  const size_t f2b = a16(sizeof(double) * (size_t)(g.kc + 1) * nsub);
+  const size_t descb = a16(sizeof(int) * 4 * nsub);
+  const size_t cbb = a16(sizeof(int) * (size_t)(g.kc + 1) * nsub);
+  const size_t cumb = a16(sizeof(int) * g.cum_stride * nsub);
+  char* base = static_cast<char*>(ctx->gscr.ensure(f2b + descb + cbb + cumb));
+  g.f2 = reinterpret_cast<double*>(base);
+  g.desc = reinterpret_cast<int*>(base + f2b);
+  g.cb = reinterpret_cast<int*>(base + f2b + descb);
+  g.cum = reinterpret_cast<int*>(base + f2b + descb + cbb);
+  g.queue = static_cast<unsigned long long*>(ctx->gqueue.ensure(sizeof(unsigned long long)));
+  if (yp.x_max >= 3 && !gen_dp_f_in_smem(n, yp))
+    g.fslots = static_cast<double*>(
+        ctx->fscratch.ensure(gen_fslot_bytes(n, yp) * (size_t)gen_dp_grid(n, yp)));
+  return g;
 }
 
 // Runs one batch call.  Everything from the input upload to the statistic
@@ -328,18 +351,6 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   // copy stream chunk by chunk while the next chunk computes.
   double* const user_stat[6] = {out->mic, out->mas, out->mev, out->mcn, out->mic_e, out->tic};
   const bool small = tiny || memo;  // one thread per pair, stats written directly
-  const long long chunk = small ? (dio ? count : std::min<long long>(count, 1LL << 20))
-                               : std::max<long long>(1, std::min<long long>(
-                                     count, (256LL << 20) / (16LL * ncell)));
-  const long long nchunks = (count + chunk - 1) / chunk;
-  const int nslots = dio ? 1 : 2;  // double-buffered staging for host io
-  double* stage = nullptr;
-  const size_t stage_stats = 6 * (size_t)chunk;
-  const size_t stage_cells = out->cells ? 2 * (size_t)ncell * chunk : 0;
-  if (!dio) stage = static_cast<double*>(ctx->stats.ensure(sizeof(double) * nslots * (stage_stats + stage_cells)));
-  double* ocells = nullptr;
-  if (!small) ocells = static_cast<double*>(ctx->ocells.ensure(sizeof(double) * 2 * (size_t)ncell * chunk));
-
   std::vector<YParams> yps;
   for (int y = 2; y <= B / 2; ++y) {
     YParams yp;
@@ -349,12 +360,28 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
     yp.k_hat = std::max(1, static_cast<int>(std::floor(par->c * static_cast<double>(yp.x_max))));
     yps.push_back(yp);
   }
+  size_t per_pair = 16 * (size_t)ncell;  // ocells
   if (!small) {
-    for (const auto& yp : yps)
-      if (general_smem_bytes(n, yp, false) > 227 * 1024)
+    size_t sub_max = 0;
+    for (const auto& yp : yps) {
+      if (gen_pf_smem(n, yp) > 227 * 1024 || gen_dp_smem(n, yp) > 227 * 1024)
         throw Failure("mine_b200: general tier shared-memory plan exceeds 227 KB for n=" +
                       std::to_string(n) + " y=" + std::to_string(yp.y));
+      sub_max = std::max(sub_max, gen_scratch_per_sub(n, yp));
+    }
+    per_pair += 2 * sub_max;
   }
+  const long long chunk = small ? (dio ? count : std::min<long long>(count, 1LL << 20))
+                               : std::max<long long>(1, std::min<long long>(
+                                     count, (long long)((1024ULL << 20) / per_pair)));
+  const long long nchunks = (count + chunk - 1) / chunk;
+  const int nslots = dio ? 1 : 2;  // double-buffered staging for host io
+  double* stage = nullptr;
+  const size_t stage_stats = 6 * (size_t)chunk;
+  const size_t stage_cells = out->cells ? 2 * (size_t)ncell * chunk : 0;
+  if (!dio) stage = static_cast<double*>(ctx->stats.ensure(sizeof(double) * nslots * (stage_stats + stage_cells)));
+  double* ocells = nullptr;
+  if (!small) ocells = static_cast<double*>(ctx->ocells.ensure(sizeof(double) * 2 * (size_t)ncell * chunk));
 
   unsigned long long* dcnt = nullptr;
   if (opts.counters) {
@@ -395,19 +422,12 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
       ++ctx->launches;
     } else {
       for (const auto& yp : yps) {
-        if (general_f_fits(n, yp)) {
-          launch_general(vs, tb, pc, 0, cn, yp, ocells, nullptr, nullptr, -1, dcnt, s);
+        const GenScratch gs = gen_scratch(ctx, n, yp, 2 * cn);
+        launch_part_f2(vs, tb, pc, 0, cn, yp, gs, ocells, nullptr, -1, dcnt, s);
+        ++ctx->launches;
+        if (yp.x_max >= 3) {
+          launch_dp(vs, tb, pc, 0, cn, yp, gs, ocells, nullptr, -1, s);
           ++ctx->launches;
-        } else {
-          // F table in global scratch: bound the CTAs per launch.
-          const size_t per_cta = sizeof(double) * (size_t)(std::min(n, yp.k_hat) + 1) * (yp.x_max - 1);
-          const long long max_ctas = std::max<long long>(2, (1LL << 30) / (long long)per_cta);
-          const long long step = std::max<long long>(1, max_ctas / 2);
-          double* fs = static_cast<double*>(ctx->fscratch.ensure(per_cta * 2 * step));
-          for (long long b0 = 0; b0 < cn; b0 += step) {
-            launch_general(vs, tb, pc, b0, std::min(step, cn - b0), yp, ocells, fs, nullptr, -1, dcnt, s);
-            ++ctx->launches;
-          }
         }
       }
       launch_reduce(tb, cn, ocells, par->est, so, 0, s);
@@ -491,6 +511,7 @@ mine_b200_ctx* mine_b200_create(int device) {
       std::lock_guard<std::mutex> lk(init_mu);
       if (std::find(inited.begin(), inited.end(), device) == inited.end()) {
         CK(init_kernel_attributes(device));
+        CK(init_general_attributes(device));
         inited.push_back(device);
       }
     }
@@ -592,7 +613,7 @@ int mine_b200_debug_subproblem(mine_b200_ctx* ctx, int n, const double* col_var,
     ps.xi = didx;
     ps.yi = didx + 1;
     YParams yp{y_target, y_target - 2, x_max, k_hat};
-    if (general_smem_bytes(n, yp, false) > 227 * 1024)
+    if (gen_pf_smem(n, yp) > 227 * 1024 || gen_dp_smem(n, yp) > 227 * 1024)
       throw Failure("mine_b200: subproblem too large for the general tier");
     // debug outputs in one device block
     const size_t ints = 3 + (size_t)n + (n + 1);
@@ -608,10 +629,9 @@ int mine_b200_debug_subproblem(mine_b200_ctx* ctx, int n, const double* col_var,
     dbg.q_x = ib + 3;
     dbg.bounds = ib + 3 + n;
     double* oc = static_cast<double*>(ctx->ocells.ensure(sizeof(double) * 2 * tb.ncell));
-    double* fs = nullptr;
-    if (!general_f_fits(n, yp))
-      fs = static_cast<double*>(ctx->fscratch.ensure(sizeof(double) * (size_t)(std::min(n, k_hat) + 1) * (x_max - 1)));
-    launch_general(vs, tb, ps, 0, 1, yp, oc, fs, &dbg, 0, nullptr, s);
+    const GenScratch gs = gen_scratch(ctx, n, yp, 1);
+    launch_part_f2(vs, tb, ps, 0, 1, yp, gs, oc, &dbg, 0, nullptr, s);
+    launch_dp(vs, tb, ps, 0, 1, yp, gs, oc, &dbg, 0, s);
     CK(cudaGetLastError());
     std::vector<char> h(bytes);
     CK(cudaMemcpyAsync(h.data(), dd, bytes, cudaMemcpyDeviceToHost, s));

@@ -1,0 +1,507 @@
+// General tier of the MINE engine (any n, any B): two kernels per row target y.
+//
+//   k_part_f2  one CTA per (pair, orientation) subproblem: labels in x order,
+//              Alg. 1 clumps (partition.cpp:108-146), Alg. 2 superclumps
+//              (:148-165), the cumulative cell counts (mutual_info.cpp:9-24)
+//              and the whole first DP level F(t,2) (mutual_info.cpp:47-56),
+//              which has no sequential dependency: warps over t, lanes over s.
+//              Subproblems that need no further level (l_max <= 2) finish here.
+//   k_dp       persistent CTAs pulling subproblems from an atomic queue: the
+//              levels l >= 3 (mutual_info.cpp:57-66) with the reference's exact
+//              F-form arithmetic, tiled over (t-tile x level-tile).  For a tile
+//              the candidates from every earlier s (the bulk of the work) are
+//              independent of each other: the span terms
+//                A(s,t) = c_s/c_t,  W(s,t) = ((c_t - c_s)/c_t) h_span(s,t)
+//              are computed once per (s-chunk, t-tile) into shared memory and
+//              consumed by register-blocked accumulators for all (t, l) cells;
+//              only the s inside the tile is sequential (one step per t).  The F
+//              table lives in shared memory when it fits, else in a per-CTA HBM
+//              slot (c4: 7.5k x 500 f64 at y = 2).
+// Compiled with -fmad=false; every FP64 op rounds like the reference's.
+#include <algorithm>
+
+#include "device_common.cuh"
+#include "mine_kernels.h"
+
+namespace mb200 {
+
+namespace {
+
+constexpr int kPfThreads = 256;
+constexpr int kPfWarps = kPfThreads / 32;
+constexpr int kDpThreads = 256;
+constexpr int kDpWarps = kDpThreads / 32;
+constexpr int kMaxTile = 48;   // t-tile / s-chunk edge
+constexpr int kCells = 4;      // accumulators per thread (T * nl <= 1024)
+
+__host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+
+struct PfLayout {
+  size_t lab, fused, cl, cb, cnt, misc, total;
+};
+
+__host__ __device__ inline PfLayout pf_layout(int n, int y, int kc) {
+  PfLayout L;
+  size_t o = 0;
+  L.lab = o;
+  o += al16(sizeof(uint16_t) * n);
+  L.fused = o;
+  o += al16(n);
+  L.cl = o;
+  o += al16(sizeof(int) * n);
+  L.cb = o;
+  o += al16(sizeof(int) * (n + 1));
+  L.cnt = o;
+  o += al16(sizeof(int) * (size_t)y * (kc + 1));
+  L.misc = o;
+  o += al16(sizeof(double) * 40);
+  L.total = o;
+  return L;
+}
+
+__device__ __forceinline__ void sub_vars(const PairSpace& ps, long long pl, int orient, int& X,
+                                         int& Y) {
+  int va, vb;
+  pair_vars(ps, ps.first + pl, va, vb);
+  X = orient ? vb : va;
+  Y = orient ? va : vb;
+}
+
+// Writes the normalised cells of one orientation / row target (char_matrix.cpp:
+// 57-64); I(l) gives the unnormalised I_l.
+template <typename IFn>
+__device__ void write_cells(const Tables& tb, double* ocells, long long pl, int orient, int y,
+                            int x_max, int rows, IFn I, const SubDebug& dbg, bool has_dbg) {
+  double* oc = ocells + (size_t)pl * 2 * tb.ncell + (size_t)orient * tb.ncell;
+  const double logy = tb.logi[rows];
+  for (int l = 2 + threadIdx.x; l <= x_max; l += blockDim.x) {
+    const double v = I(l);
+    if (has_dbg) dbg.values[l - 2] = v;
+    const int cell = orient ? tb.cell_off[l] + (y - 2) : tb.cell_off[y] + (l - 2);
+    oc[cell] = norm_cell(v, tb.logi[l], logy);
+  }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kPfThreads) k_part_f2(VarSet vs, Tables tb, PairSpace ps,
+                                                        long long base, YParams yp, GenScratch gs,
+                                                        double* __restrict__ ocells, SubDebug dbg,
+                                                        int has_dbg, int orient_only,
+                                                        unsigned long long* counters) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = vs.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int norient = orient_only >= 0 ? 1 : 2;
+  const long long pl = base + blockIdx.x / norient;
+  const int orient = orient_only >= 0 ? orient_only : (int)(blockIdx.x % 2);
+  const long long sub = (long long)blockIdx.x;  // index inside this launch's scratch
+  int X, Y;
+  sub_vars(ps, pl, orient, X, Y);
+  const int y = yp.y, yi = yp.yi, x_max = yp.x_max, k_hat = yp.k_hat, kc = gs.kc;
+
+  const PfLayout L = pf_layout(n, y, kc);
+  uint16_t* lab = reinterpret_cast<uint16_t*>(smem + L.lab);
+  uint8_t* fused = smem + L.fused;
+  int* cl = reinterpret_cast<int*>(smem + L.cl);
+  int* cb = reinterpret_cast<int*>(smem + L.cb);
+  int* cum = reinterpret_cast<int*>(smem + L.cnt);
+  int* misc = reinterpret_cast<int*>(smem + L.misc);
+  double* dmisc = reinterpret_cast<double*>(smem + L.misc) + 30;  // ints 0..59 are scan / k scratch
+
+  const int* permX = vs.perm + (size_t)X * n;
+  const int* ridX = vs.runid + (size_t)X * n;
+  const uint16_t* qY = vs.q + ((size_t)Y * vs.ny + yi) * n;
+  const int rows = vs.yhat[(size_t)Y * vs.ny + yi];
+  const double hq = vs.hq[(size_t)Y * vs.ny + yi];
+
+  // --- row labels in x order (reindex_to_first_order, partition.cpp:94-106)
+  for (int t = tid; t < n; t += kPfThreads) {
+    lab[t] = qY[permX[t]];
+    fused[t] = 0;
+  }
+  __syncthreads();
+  // --- Alg. 1 (partition.cpp:116-133): an x tie run whose labels change is fused
+  for (int t = tid + 1; t < n; t += kPfThreads)
+    if (ridX[t] == ridX[t - 1] && lab[t] != lab[t - 1]) fused[ridX[t]] = 1;
+  __syncthreads();
+  // --- clump starts (:135-144): label change at a run start, or either run fused
+  for (int t = tid; t < n; t += kPfThreads) {
+    int f = 0;
+    if (t > 0) {
+      const int a = ridX[t], b = ridX[t - 1];
+      f = a != b && (fused[a] || fused[b] || lab[t] != lab[t - 1]);
+    }
+    cl[t] = f;
+  }
+  __syncthreads();
+  const int kraw = block_incl_scan(cl, n, misc) + 1;  // cl[t]: clump of position t
+  for (int t = tid + 1; t < n; t += kPfThreads)
+    if (cl[t] != cl[t - 1]) cb[cl[t]] = t;
+  if (tid == 0) {
+    cb[0] = 0;
+    cb[kraw] = n;
+  }
+  __syncthreads();
+  // --- Alg. 2 (partition.cpp:148-165): equipartition the clump ordinals
+  int k = kraw;
+  if (kraw > k_hat) {
+    if (tid == 0) {
+      double desired = (double)n / (double)k_hat;
+      int curr = 1, in_row = 0;
+      for (int j = 0; j < kraw; ++j) {
+        const int i = cb[j], run = cb[j + 1] - i;
+        if (in_row != 0 &&
+            fabs((double)(in_row + run) - desired) >= fabs((double)in_row - desired)) {
+          ++curr;
+          in_row = 0;
+          desired = (double)(n - i) / (double)(k_hat - curr + 1);
+          cb[curr - 1] = i;  // in place: curr - 1 <= j
+        }
+        in_row += run;
+      }
+      cb[curr] = n;
+      misc[40] = curr;
+    }
+    __syncthreads();
+    k = misc[40];
+    // superclump of every position, by a scan over superclump starts
+    for (int t = tid; t < n; t += kPfThreads) cl[t] = 0;
+    __syncthreads();
+    for (int j = 1 + tid; j < k; j += kPfThreads) cl[cb[j]] = 1;
+    __syncthreads();
+    block_incl_scan(cl, n, misc);
+  }
+  // --- cell counts and cumulative table (mutual_info.cpp:9-24): cum[r][j]
+  const int kk = k + 1;
+  for (int i = tid; i < rows * kk; i += kPfThreads) cum[i] = 0;
+  __syncthreads();
+  for (int t = tid; t < n; t += kPfThreads) atomicAdd(&cum[(lab[t] - 1) * kk + cl[t] + 1], 1);
+  __syncthreads();
+  for (int r = warp; r < rows; r += kPfWarps) {
+    int carry = 0;
+    for (int j0 = 1; j0 <= k; j0 += 32) {
+      const int j = j0 + lane;
+      int v = j <= k ? cum[r * kk + j] : 0;
+      v = warp_incl_scan(v) + carry;
+      if (j <= k) cum[r * kk + j] = v;
+      carry = __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+
+  const int l_max = min(x_max, k);
+  if (counters && tid == 0) {
+    unsigned long long w[kNumCounters] = {0, 0, 0, 0, 0, 0};
+    subproblem_work(rows, k, x_max, w);
+    for (int i = 0; i < kNumCounters; ++i)
+      if (w[i]) atomicAdd(counters + i, w[i]);
+  }
+  if (has_dbg && tid == 0) {
+    *dbg.row_count = rows;
+    *dbg.raw_k = kraw;
+    *dbg.k = k;
+    *dbg.h_q = hq;
+  }
+  if (has_dbg) {
+    for (int t = tid; t < n; t += kPfThreads) dbg.q_x[t] = lab[t];
+    for (int j = tid; j <= k; j += kPfThreads) dbg.bounds[j] = cb[j];
+  }
+  // hand the partition to k_dp
+  if (l_max >= 3) {
+    if (tid == 0) {
+      int4 d;
+      d.x = k;
+      d.y = rows;
+      d.z = kraw;
+      d.w = l_max;
+      reinterpret_cast<int4*>(gs.desc)[sub] = d;
+    }
+    int* gcb = gs.cb + (size_t)sub * (kc + 1);
+    int* gcum = gs.cum + (size_t)sub * gs.cum_stride;
+    for (int j = tid; j <= k; j += kPfThreads) gcb[j] = cb[j];
+    for (int i = tid; i < rows * kk; i += kPfThreads) gcum[i] = cum[i];
+  } else if (tid == 0) {
+    int4 d;
+    d.x = k;
+    d.y = rows;
+    d.z = kraw;
+    d.w = l_max;
+    reinterpret_cast<int4*>(gs.desc)[sub] = d;
+  }
+
+  // --- first DP level F(t,2) = max_s H(P) - H(P,Q) (mutual_info.cpp:47-56):
+  // every t is independent; warps over t, lanes over s, all p*log(p) terms
+  // from row c_t of the table.
+  double* gf2 = gs.f2 + (size_t)sub * (kc + 1);
+  if (k >= 2) {
+    const int t_lo = l_max >= 3 ? 2 : k;
+    for (int t = t_lo + warp; t <= k; t += kPfWarps) {
+      const int ct = cb[t];
+      const double* plt = tb.pl + tri(ct);
+      double best = kLowest;
+      for (int s = 1 + lane; s < t; s += 32) {
+        const int cs = cb[s];
+        double acc2 = __ldg(plt + cs);
+        acc2 = __dadd_rn(acc2, __ldg(plt + (ct - cs)));
+        double accj = 0.0;
+        for (int r = 0; r < rows; ++r) accj = __dadd_rn(accj, __ldg(plt + cum[r * kk + s]));
+        for (int r = 0; r < rows; ++r)
+          accj = __dadd_rn(accj, __ldg(plt + (cum[r * kk + t] - cum[r * kk + s])));
+        best = dmax(best, __dsub_rn(-acc2, -accj));
+      }
+      best = warp_max(best);
+      if (lane == 0) {
+        if (l_max >= 3) gf2[t] = best;
+        if (t == k) dmisc[0] = best;
+      }
+    }
+  }
+  __syncthreads();
+  if (l_max <= 2) {  // done: I_l = I_2 for every l (mutual_info.cpp:68-70)
+    const double i2 = k >= 2 ? dmax(0.0, __dadd_rn(hq, dmisc[0])) : 0.0;
+    write_cells(tb, ocells, pl, orient, y, x_max, rows, [&](int) { return i2; }, dbg, has_dbg != 0);
+  }
+}
+
+// ---------------------------------------------------------------------------
+struct DpLayout {
+  size_t cb, cum, A, W, acc, f, total;
+};
+
+__host__ __device__ inline DpLayout dp_layout(int y, int kc, int x_max, bool f_smem) {
+  DpLayout L;
+  size_t o = 0;
+  L.cb = o;
+  o += al16(sizeof(int) * (kc + 1));
+  L.cum = o;
+  o += al16(sizeof(int) * (size_t)y * (kc + 1));
+  L.A = o;
+  o += al16(sizeof(double) * kMaxTile * kMaxTile);
+  L.W = o;
+  o += al16(sizeof(double) * kMaxTile * kMaxTile);
+  L.acc = o;
+  o += al16(sizeof(double) * kDpThreads * kCells);
+  L.f = o;
+  o += f_smem ? al16(sizeof(double) * (size_t)(kc + 1) * (x_max - 1)) : 0;
+  L.total = o;
+  return L;
+}
+
+// Span terms for s in [s0, s0+ns) x t in [t0, t0+nt) (mutual_info.cpp:39-41,
+// 62): A = c_s/c_t, W = ((c_t - c_s)/c_t) h_span(s,t), h by the reference's
+// sequential row sum.  Entries with s >= t or t > k are left undefined.
+__device__ __forceinline__ void span_terms(const Tables& tb, const int* cb, const int* cum, int kk,
+                                           int rows, int k, int s0, int ns, int t0, int nt,
+                                           double* A, double* W) {
+  for (int idx = threadIdx.x; idx < ns * nt; idx += blockDim.x) {
+    const int sl = idx / nt, tl = idx % nt;
+    const int s = s0 + sl, t = t0 + tl;
+    if (s >= t || t > k) continue;
+    const int cs = cb[s], ct = cb[t];
+    const double* plm = tb.pl + tri(ct - cs);
+    double acch = 0.0;
+    for (int r = 0; r < rows; ++r) acch = __dadd_rn(acch, __ldg(plm + (cum[r * kk + t] - cum[r * kk + s])));
+    const double dcs = (double)cs, dct = (double)ct;
+    A[sl * kMaxTile + tl] = __ddiv_rn(dcs, dct);
+    W[sl * kMaxTile + tl] = __dmul_rn(__ddiv_rn(__dsub_rn(dct, dcs), dct), -acch);
+  }
+}
+
+template <bool FSM>
+__global__ void __launch_bounds__(kDpThreads) k_dp(VarSet vs, Tables tb, PairSpace ps,
+                                                   long long base, long long nsub, YParams yp,
+                                                   GenScratch gs, double* __restrict__ ocells,
+                                                   SubDebug dbg, int has_dbg, int orient_only) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ long long s_sub;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int y = yp.y, x_max = yp.x_max, kc = gs.kc, LW = x_max - 1;
+  const DpLayout L = dp_layout(y, kc, x_max, FSM);
+  int* cb = reinterpret_cast<int*>(smem + L.cb);
+  int* cum = reinterpret_cast<int*>(smem + L.cum);
+  double* A = reinterpret_cast<double*>(smem + L.A);
+  double* W = reinterpret_cast<double*>(smem + L.W);
+  double* accS = reinterpret_cast<double*>(smem + L.acc);
+  double* F = FSM ? reinterpret_cast<double*>(smem + L.f)
+                  : gs.fslots + (size_t)blockIdx.x * (size_t)(kc + 1) * LW;
+  const int norient = orient_only >= 0 ? 1 : 2;
+
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_sub = atomicAdd(gs.queue, 1ull);
+    __syncthreads();
+    const long long sub = s_sub;
+    if (sub >= nsub) break;
+    const int4 d = reinterpret_cast<const int4*>(gs.desc)[sub];
+    const int k = d.x, rows = d.y, l_max = d.w, kk = k + 1;
+    if (l_max < 3) continue;  // finished by k_part_f2
+    const long long pl = base + sub / norient;
+    const int orient = orient_only >= 0 ? orient_only : (int)(sub % 2);
+    {
+      const int* gcb = gs.cb + (size_t)sub * (kc + 1);
+      const int* gcum = gs.cum + (size_t)sub * gs.cum_stride;
+      const double* gf2 = gs.f2 + (size_t)sub * (kc + 1);
+      for (int j = tid; j <= k; j += kDpThreads) cb[j] = gcb[j];
+      for (int i = tid; i < rows * kk; i += kDpThreads) cum[i] = gcum[i];
+      for (int t = 2 + tid; t <= k; t += kDpThreads) F[(size_t)t * LW] = gf2[t];
+    }
+    __syncthreads();
+
+    // level tiles of <= 64 levels, t tiles of T, s chunks of T
+    for (int l0 = 3; l0 <= l_max; l0 += 64) {
+      const int l1 = min(l0 + 63, l_max), nl = l1 - l0 + 1;
+      const int T = max(1, min(kMaxTile, (kDpThreads * kCells) / nl));
+      const int t_hi = k;
+      const int t_lo = (l0 == l_max) ? k : l0;
+      for (int t0 = t_lo; t0 <= t_hi; t0 += T) {
+        const int nt = min(T, t_hi - t0 + 1);
+        double acc[kCells];
+#pragma unroll
+        for (int i = 0; i < kCells; ++i) acc[i] = kLowest;
+        // ---- outer part: every s < t0 (independent candidates)
+        for (int s0 = max(2, l0 - 1); s0 < t0; s0 += T) {
+          const int ns = min(T, t0 - s0);
+          span_terms(tb, cb, cum, kk, rows, k, s0, ns, t0, nt, A, W);
+          __syncthreads();
+#pragma unroll
+          for (int i = 0; i < kCells; ++i) {
+            const int c = tid + kDpThreads * i;
+            if (c >= nt * nl) continue;
+            const int tl = c / nl, ll = c - tl * nl;
+            const int t = t0 + tl, l = l0 + ll;
+            if (t < l || t > k || (l == l_max && t != k)) continue;
+            double a = acc[i];
+            const int s_beg = max(s0, l - 1);
+            for (int s = s_beg; s < s0 + ns; ++s) {
+              const int sl = s - s0;
+              const double cand = __dsub_rn(__dmul_rn(A[sl * kMaxTile + tl], F[(size_t)s * LW + (l - 3)]),
+                                            W[sl * kMaxTile + tl]);
+              a = dmax(a, cand);
+            }
+            acc[i] = a;
+          }
+          __syncthreads();
+        }
+#pragma unroll
+        for (int i = 0; i < kCells; ++i) accS[tid + kDpThreads * i] = acc[i];
+        // ---- inner part: s inside the tile, one t at a time
+        span_terms(tb, cb, cum, kk, rows, k, t0, nt, t0, nt, A, W);
+        __syncthreads();
+        for (int tl = 0; tl < nt; ++tl) {
+          const int t = t0 + tl;
+          for (int ll = warp; ll < nl; ll += kDpWarps) {
+            const int l = l0 + ll;
+            if (t < l || t > k || (l == l_max && t != k)) continue;
+            double m = kLowest;
+            for (int s = max(t0, l - 1) + lane; s < t; s += 32) {
+              const int sl = s - t0;
+              m = dmax(m, __dsub_rn(__dmul_rn(A[sl * kMaxTile + tl], F[(size_t)s * LW + (l - 3)]),
+                                    W[sl * kMaxTile + tl]));
+            }
+            m = warp_max(m);
+            if (lane == 0) {
+              const double o = accS[tl * nl + ll];  // cell c lives at accS[c]
+              F[(size_t)t * LW + (l - 2)] = dmax(o, m);
+            }
+          }
+          __syncthreads();
+        }
+      }
+    }
+    // ---- I_l (mutual_info.cpp:68-70) and the cells
+    int X, Yv;
+    sub_vars(ps, pl, orient, X, Yv);
+    const double hq = vs.hq[(size_t)Yv * vs.ny + yp.yi];
+    write_cells(
+        tb, ocells, pl, orient, y, x_max, rows,
+        [&](int l) {
+          const int le = l <= l_max ? l : l_max;
+          return dmax(0.0, __dadd_rn(hq, F[(size_t)k * LW + (le - 2)]));
+        },
+        dbg, has_dbg != 0);
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+int gen_kc(int n, const YParams& yp) { return std::min(n, yp.k_hat); }
+
+size_t gen_scratch_per_sub(int n, const YParams& yp) {
+  const size_t kc = (size_t)gen_kc(n, yp);
+  return sizeof(int4) + sizeof(int) * (kc + 1) + sizeof(int) * (size_t)yp.y * (kc + 1) +
+         sizeof(double) * (kc + 1);
+}
+
+size_t gen_pf_smem(int n, const YParams& yp) { return pf_layout(n, yp.y, gen_kc(n, yp)).total; }
+
+bool gen_dp_f_in_smem(int n, const YParams& yp) {
+  return dp_layout(yp.y, gen_kc(n, yp), yp.x_max, true).total <= 220 * 1024;
+}
+
+size_t gen_dp_smem(int n, const YParams& yp) {
+  return dp_layout(yp.y, gen_kc(n, yp), yp.x_max, gen_dp_f_in_smem(n, yp)).total;
+}
+
+size_t gen_fslot_bytes(int n, const YParams& yp) {
+  return sizeof(double) * (size_t)(gen_kc(n, yp) + 1) * (yp.x_max - 1);
+}
+
+int gen_dp_grid(int n, const YParams& yp) {
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t sm = gen_dp_smem(n, yp);
+  per = (int)std::max<size_t>(1, std::min<size_t>(8, (228 * 1024) / (sm + 1024)));
+  return sms * per;
+}
+
+void launch_part_f2(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
+                    long long npairs, const YParams& yp, const GenScratch& gs, double* ocells,
+                    const SubDebug* dbg, int orient_only, unsigned long long* counters,
+                    cudaStream_t s) {
+  if (npairs <= 0) return;
+  const unsigned blocks = (unsigned)(npairs * (orient_only >= 0 ? 1 : 2));
+  SubDebug d{};
+  if (dbg) d = *dbg;
+  k_part_f2<<<blocks, kPfThreads, gen_pf_smem(vs.n, yp), s>>>(vs, tb, ps, base, yp, gs, ocells, d,
+                                                              dbg ? 1 : 0, orient_only, counters);
+}
+
+void launch_dp(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
+               long long npairs, const YParams& yp, const GenScratch& gs, double* ocells,
+               const SubDebug* dbg, int orient_only, cudaStream_t s) {
+  if (npairs <= 0 || yp.x_max < 3) return;
+  const long long nsub = npairs * (orient_only >= 0 ? 1 : 2);
+  const bool fsm = gen_dp_f_in_smem(vs.n, yp);
+  const int grid = (int)std::min<long long>(nsub, gen_dp_grid(vs.n, yp));
+  SubDebug d{};
+  if (dbg) d = *dbg;
+  cudaMemsetAsync(gs.queue, 0, sizeof(unsigned long long), s);
+  const size_t sm = gen_dp_smem(vs.n, yp);
+  if (fsm)
+    k_dp<true><<<grid, kDpThreads, sm, s>>>(vs, tb, ps, base, nsub, yp, gs, ocells, d, dbg ? 1 : 0,
+                                            orient_only);
+  else
+    k_dp<false><<<grid, kDpThreads, sm, s>>>(vs, tb, ps, base, nsub, yp, gs, ocells, d, dbg ? 1 : 0,
+                                             orient_only);
+}
+
+cudaError_t init_general_attributes(int device) {
+  int optin = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (e != cudaSuccess) return e;
+  const void* fns[] = {reinterpret_cast<const void*>(k_part_f2),
+                       reinterpret_cast<const void*>(k_dp<true>),
+                       reinterpret_cast<const void*>(k_dp<false>)};
+  for (const void* f : fns) {
+    cudaFuncAttributes fa{};
+    e = cudaFuncGetAttributes(&fa, f);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin - (int)fa.sharedSizeBytes);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace mb200

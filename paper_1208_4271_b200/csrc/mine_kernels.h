@@ -118,7 +118,34 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo, c
                        double c, int est, StatsOut out, double* o_cells,
                        unsigned long long* counters, cudaStream_t s);
 
-// General tier: one CTA per (pair, orientation) for one row target; writes the
+// General tier v2 (mine_general.cu): k_part_f2 + persistent tiled k_dp per y.
+struct GenScratch {
+  int* desc = nullptr;        // nsub x int4 {k, rows, raw k, l_max}
+  int* cb = nullptr;          // nsub x (kc+1) clump boundaries
+  int* cum = nullptr;         // nsub x cum_stride cumulative counts, row-major [r][j]
+  double* f2 = nullptr;       // nsub x (kc+1) F(t,2)
+  double* fslots = nullptr;   // grid x (kc+1) x (x_max-1) F tables (when not in smem)
+  unsigned long long* queue = nullptr;
+  int kc = 0;                 // min(n, k_hat)
+  size_t cum_stride = 0;      // y * (kc+1)
+};
+int gen_kc(int n, const YParams& yp);
+size_t gen_scratch_per_sub(int n, const YParams& yp);
+size_t gen_pf_smem(int n, const YParams& yp);
+size_t gen_dp_smem(int n, const YParams& yp);
+bool gen_dp_f_in_smem(int n, const YParams& yp);
+size_t gen_fslot_bytes(int n, const YParams& yp);
+int gen_dp_grid(int n, const YParams& yp);
+void launch_part_f2(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
+                    long long npairs, const YParams& yp, const GenScratch& gs, double* ocells,
+                    const SubDebug* dbg, int orient_only, unsigned long long* counters,
+                    cudaStream_t s);
+void launch_dp(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
+               long long npairs, const YParams& yp, const GenScratch& gs, double* ocells,
+               const SubDebug* dbg, int orient_only, cudaStream_t s);
+cudaError_t init_general_attributes(int device);
+
+// General tier v1: one CTA per (pair, orientation) for one row target; writes the
 // normalised per-orientation cells into ocells[(pair - base) * 2 * ncell ...].
 // Returns false if the launch configuration is impossible (caller falls back
 // to nothing: the error surfaces through the C ABI).
