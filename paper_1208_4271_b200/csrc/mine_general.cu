@@ -32,7 +32,7 @@ constexpr int kPfWarps = kPfThreads / 32;
 constexpr int kDpThreads = 256;
 constexpr int kDpWarps = kDpThreads / 32;
 constexpr int kMaxTile = 48;   // t-tile / s-chunk edge
-constexpr int kCells = 4;      // accumulators per thread (T * nl <= 1024)
+constexpr int kCells = 8;      // accumulators per thread
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -292,22 +292,27 @@ __host__ __device__ inline DpLayout dp_layout(int y, int kc, int x_max, bool f_s
 __device__ __forceinline__ void span_terms(const Tables& tb, const int* cb, const int* cum, int kk,
                                            int rows, int k, int s0, int ns, int t0, int nt,
                                            double* A, double* W) {
-  for (int idx = threadIdx.x; idx < ns * nt; idx += blockDim.x) {
-    const int sl = idx / nt, tl = idx % nt;
-    const int s = s0 + sl, t = t0 + tl;
-    if (s >= t || t > k) continue;
-    const int cs = cb[s], ct = cb[t];
-    const double* plm = tb.pl + tri(ct - cs);
-    double acch = 0.0;
-    for (int r = 0; r < rows; ++r) acch = __dadd_rn(acch, __ldg(plm + (cum[r * kk + t] - cum[r * kk + s])));
-    const double dcs = (double)cs, dct = (double)ct;
-    A[sl * kMaxTile + tl] = __ddiv_rn(dcs, dct);
-    W[sl * kMaxTile + tl] = __dmul_rn(__ddiv_rn(__dsub_rn(dct, dcs), dct), -acch);
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int sl = threadIdx.x >> 5; sl < ns; sl += nw) {
+    const int s = s0 + sl, cs = cb[s];
+    const double dcs = (double)cs;
+    for (int tl = lane; tl < nt; tl += 32) {
+      const int t = t0 + tl;
+      if (s >= t || t > k) continue;
+      const int ct = cb[t];
+      const double* plm = tb.pl + tri(ct - cs);
+      double acch = 0.0;
+      for (int r = 0; r < rows; ++r)
+        acch = __dadd_rn(acch, __ldg(plm + (cum[r * kk + t] - cum[r * kk + s])));
+      const double dct = (double)ct;
+      A[sl * kMaxTile + tl] = __ddiv_rn(dcs, dct);
+      W[sl * kMaxTile + tl] = __dmul_rn(__ddiv_rn(__dsub_rn(dct, dcs), dct), -acch);
+    }
   }
 }
 
 template <bool FSM>
-__global__ void __launch_bounds__(kDpThreads) k_dp(VarSet vs, Tables tb, PairSpace ps,
+__global__ void __launch_bounds__(kDpThreads, 1) k_dp(VarSet vs, Tables tb, PairSpace ps,
                                                    long long base, long long nsub, YParams yp,
                                                    GenScratch gs, double* __restrict__ ocells,
                                                    SubDebug dbg, int has_dbg, int orient_only) {
@@ -346,61 +351,88 @@ __global__ void __launch_bounds__(kDpThreads) k_dp(VarSet vs, Tables tb, PairSpa
     }
     __syncthreads();
 
-    // level tiles of <= 64 levels, t tiles of T, s chunks of T
+    // Level tiles of <= 64 levels.  A thread owns 8 cells: two adjacent t
+    // (t0 + 2p, t0 + 2p + 1) x a group of 4 consecutive levels, so each s
+    // costs one 16-byte load for both A, one for both W and four F loads for
+    // 8 independent max chains.  T t's per tile with (T/2) * groups <= 256.
     for (int l0 = 3; l0 <= l_max; l0 += 64) {
       const int l1 = min(l0 + 63, l_max), nl = l1 - l0 + 1;
-      const int T = max(1, min(kMaxTile, (kDpThreads * kCells) / nl));
-      const int t_hi = k;
-      const int t_lo = (l0 == l_max) ? k : l0;
-      for (int t0 = t_lo; t0 <= t_hi; t0 += T) {
-        const int nt = min(T, t_hi - t0 + 1);
-        double acc[kCells];
+      const int ng = (nl + 3) >> 2;
+      const int T = max(2, min(kMaxTile, 2 * (kDpThreads / ng)));
+      const int t_lo = (l0 == l_max) ? k : l0;  // level l_max is needed at t = k only
+      const int my_tp = tid / ng, my_g = tid - my_tp * ng;
+      const int my_l = l0 + 4 * my_g;           // first of my 4 levels
+      const int my_tl = 2 * my_tp;              // first of my 2 t's (tile-local)
+      for (int t0 = t_lo; t0 <= k; t0 += T) {
+        const int nt = min(T, k - t0 + 1);
+        const bool owner = my_tl < nt;
+        double acc[8];
 #pragma unroll
-        for (int i = 0; i < kCells; ++i) acc[i] = kLowest;
+        for (int i = 0; i < 8; ++i) acc[i] = kLowest;
         // ---- outer part: every s < t0 (independent candidates)
         for (int s0 = max(2, l0 - 1); s0 < t0; s0 += T) {
           const int ns = min(T, t0 - s0);
           span_terms(tb, cb, cum, kk, rows, k, s0, ns, t0, nt, A, W);
           __syncthreads();
+          if (owner) {
+            // s >= l - 1 holds for all 4 levels once s >= my_l + 2; only the
+            // first chunk(s) near the diagonal need the per-level test.
+            // Cells that are not valid accumulate garbage that is never read.
+            int sl = 0;
+            for (; sl < ns && s0 + sl < my_l + 2; ++sl) {
+              const int s = s0 + sl;
+              const double2 a = *reinterpret_cast<const double2*>(A + sl * kMaxTile + my_tl);
+              const double2 w = *reinterpret_cast<const double2*>(W + sl * kMaxTile + my_tl);
+              const double* fr = F + (size_t)s * LW + (my_l - 3);
 #pragma unroll
-          for (int i = 0; i < kCells; ++i) {
-            const int c = tid + kDpThreads * i;
-            if (c >= nt * nl) continue;
-            const int tl = c / nl, ll = c - tl * nl;
-            const int t = t0 + tl, l = l0 + ll;
-            if (t < l || t > k || (l == l_max && t != k)) continue;
-            double a = acc[i];
-            const int s_beg = max(s0, l - 1);
-            for (int s = s_beg; s < s0 + ns; ++s) {
-              const int sl = s - s0;
-              const double cand = __dsub_rn(__dmul_rn(A[sl * kMaxTile + tl], F[(size_t)s * LW + (l - 3)]),
-                                            W[sl * kMaxTile + tl]);
-              a = dmax(a, cand);
+              for (int i = 0; i < 4; ++i)
+                if (s >= my_l + i - 1) {
+                  const double f = fr[i];
+                  acc[i] = dmax(acc[i], __dsub_rn(__dmul_rn(a.x, f), w.x));
+                  acc[4 + i] = dmax(acc[4 + i], __dsub_rn(__dmul_rn(a.y, f), w.y));
+                }
             }
-            acc[i] = a;
+            const double* Ap = A + my_tl;
+            const double* Wp = W + my_tl;
+            const double* fr = F + (size_t)(s0 + sl) * LW + (my_l - 3);
+#pragma unroll 2
+            for (; sl < ns; ++sl, fr += LW) {
+              const double2 a = *reinterpret_cast<const double2*>(Ap + sl * kMaxTile);
+              const double2 w = *reinterpret_cast<const double2*>(Wp + sl * kMaxTile);
+              const double f0 = fr[0], f1 = fr[1], f2 = fr[2], f3 = fr[3];
+              acc[0] = dmax(acc[0], __dsub_rn(__dmul_rn(a.x, f0), w.x));
+              acc[1] = dmax(acc[1], __dsub_rn(__dmul_rn(a.x, f1), w.x));
+              acc[2] = dmax(acc[2], __dsub_rn(__dmul_rn(a.x, f2), w.x));
+              acc[3] = dmax(acc[3], __dsub_rn(__dmul_rn(a.x, f3), w.x));
+              acc[4] = dmax(acc[4], __dsub_rn(__dmul_rn(a.y, f0), w.y));
+              acc[5] = dmax(acc[5], __dsub_rn(__dmul_rn(a.y, f1), w.y));
+              acc[6] = dmax(acc[6], __dsub_rn(__dmul_rn(a.y, f2), w.y));
+              acc[7] = dmax(acc[7], __dsub_rn(__dmul_rn(a.y, f3), w.y));
+            }
           }
           __syncthreads();
         }
 #pragma unroll
-        for (int i = 0; i < kCells; ++i) accS[tid + kDpThreads * i] = acc[i];
-        // ---- inner part: s inside the tile, one t at a time
+        for (int i = 0; i < 8; ++i) accS[tid * 8 + i] = acc[i];
+        // ---- inner part: s inside the tile, one t at a time, a level per thread
         span_terms(tb, cb, cum, kk, rows, k, t0, nt, t0, nt, A, W);
         __syncthreads();
         for (int tl = 0; tl < nt; ++tl) {
-          const int t = t0 + tl;
-          for (int ll = warp; ll < nl; ll += kDpWarps) {
+          const int tt = t0 + tl;
+          const int ll = tid;  // nl <= 64
+          if (ll < nl) {
             const int l = l0 + ll;
-            if (t < l || t > k || (l == l_max && t != k)) continue;
-            double m = kLowest;
-            for (int s = max(t0, l - 1) + lane; s < t; s += 32) {
-              const int sl = s - t0;
-              m = dmax(m, __dsub_rn(__dmul_rn(A[sl * kMaxTile + tl], F[(size_t)s * LW + (l - 3)]),
-                                    W[sl * kMaxTile + tl]));
-            }
-            m = warp_max(m);
-            if (lane == 0) {
-              const double o = accS[tl * nl + ll];  // cell c lives at accS[c]
-              F[(size_t)t * LW + (l - 2)] = dmax(o, m);
+            if (tt >= l && !(l == l_max && tt != k)) {
+              // owner of cell (tl, ll): thread (tl/2)*ng + ll/4, slot (tl&1)*4 + (ll&3)
+              double m = accS[((tl >> 1) * ng + (ll >> 2)) * 8 + (tl & 1) * 4 + (ll & 3)];
+              const double* Ap = A + tl;
+              const double* Wp = W + tl;
+              for (int s = max(t0, l - 1); s < tt; ++s) {
+                const int sl = s - t0;
+                m = dmax(m, __dsub_rn(__dmul_rn(Ap[sl * kMaxTile], F[(size_t)s * LW + (l - 3)]),
+                                      Wp[sl * kMaxTile]));
+              }
+              F[(size_t)tt * LW + (l - 2)] = m;
             }
           }
           __syncthreads();
