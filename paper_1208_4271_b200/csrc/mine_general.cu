@@ -19,6 +19,7 @@
 //              slot (c4: 7.5k x 500 f64 at y = 2).
 // Compiled with -fmad=false; every FP64 op rounds like the reference's.
 #include <algorithm>
+#include <cstdlib>
 
 #include "device_common.cuh"
 #include "mine_kernels.h"
@@ -466,8 +467,13 @@ size_t gen_scratch_per_sub(int n, const YParams& yp) {
 
 size_t gen_pf_smem(int n, const YParams& yp) { return pf_layout(n, yp.y, gen_kc(n, yp)).total; }
 
+// F in shared memory only when a CTA then still leaves room for a second one
+// per SM; a bigger F goes to a per-CTA HBM slot (L1/L2-cached), which keeps
+// 2-3 CTAs per SM resident -- measured faster on c3 than 1 CTA with smem F.
 bool gen_dp_f_in_smem(int n, const YParams& yp) {
-  return dp_layout(yp.y, gen_kc(n, yp), yp.x_max, true).total <= 220 * 1024;
+  const char* env = getenv("MINE_B200_DP_FSMEM_KB");
+  const size_t limit = (env ? (size_t)atoi(env) : 110) * 1024;
+  return dp_layout(yp.y, gen_kc(n, yp), yp.x_max, true).total <= limit;
 }
 
 size_t gen_dp_smem(int n, const YParams& yp) {
