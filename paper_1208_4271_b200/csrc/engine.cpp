@@ -81,7 +81,8 @@ int cell_count(int B) {
 // Host-built constant tables, cached per (n, B) on a context.
 struct TableSet {
   int n = -1, B = -1, ncell = 0;
-  DevBuf pl, logi, log2i, cell_off, cell_tr, cell_xy, cell_edge, cell_cmp;
+  DevBuf pl, logi, log2i, cell_off, cell_tr, cell_xy, cell_edge, cell_cmp, div;
+  bool has_div = false;
   std::vector<int> h_off;
 
   void build(int n_, int B_, cudaStream_t s) {
@@ -146,6 +147,12 @@ struct TableSet {
     CK(cudaMemcpyAsync(cell_xy.ensure(std::max(c, 1) * 4), xy.data(), c * 4, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(cell_edge.ensure(std::max(c, 1)), edge.data(), c, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(cell_cmp.ensure(std::max(c, 1)), cmp.data(), c, cudaMemcpyHostToDevice, s));
+    // exact c_s / c_t quotients for the general tier's span terms (device-built)
+    has_div = n_ <= 4096;
+    if (has_div) {
+      launch_build_div(static_cast<double*>(div.ensure(sizeof(double) * div_table_doubles(n_))), n_, s);
+      CK(cudaGetLastError());
+    }
     CK(cudaStreamSynchronize(s));  // host vectors go out of scope
     n = n_;
     B = B_;
@@ -161,6 +168,7 @@ struct TableSet {
     t.cell_xy = cell_xy.as<int>();
     t.cell_edge = cell_edge.as<uint8_t>();
     t.cell_cmp = cell_cmp.as<int8_t>();
+    t.div = has_div ? div.as<double>() : nullptr;
     t.n = n;
     t.B = B;
     t.ncell = ncell;
@@ -230,7 +238,7 @@ GenScratch gen_scratch(mine_b200_ctx* ctx, int n, const YParams& yp, long long n
   g.cb = reinterpret_cast<int*>(base + f2b + descb);
   g.cum = reinterpret_cast<int*>(base + f2b + descb + cbb);
   g.queue = static_cast<unsigned long long*>(ctx->gqueue.ensure(sizeof(unsigned long long)));
-  if (yp.x_max >= 3 && !gen_dp_f_in_smem(n, yp))
+  if (yp.x_max >= 3)
     g.fslots = static_cast<double*>(
         ctx->fscratch.ensure(gen_fslot_bytes(n, yp) * (size_t)gen_dp_grid(n, yp)));
   return g;

@@ -31,7 +31,6 @@ namespace {
 constexpr int kPfThreads = 256;
 constexpr int kPfWarps = kPfThreads / 32;
 constexpr int kDpThreads = 256;
-constexpr int kDpWarps = kDpThreads / 32;
 constexpr int kMaxTile = 48;   // t-tile / s-chunk edge
 constexpr int kCells = 8;      // accumulators per thread
 
@@ -265,10 +264,13 @@ __global__ void __launch_bounds__(kPfThreads) k_part_f2(VarSet vs, Tables tb, Pa
 
 // ---------------------------------------------------------------------------
 struct DpLayout {
-  size_t cb, cum, A, W, acc, f, total;
+  size_t cb, cum, A, W, acc, fs, ft, total;
 };
 
-__host__ __device__ inline DpLayout dp_layout(int y, int kc, int x_max, bool f_smem) {
+constexpr int kFsW = 64;       // staged F row width (levels l0-1 .. l1-1)
+constexpr int kFtW = 65;       // tile F row width (levels l0-1 .. l1)
+
+__host__ __device__ inline DpLayout dp_layout(int y, int kc) {
   DpLayout L;
   size_t o = 0;
   L.cb = o;
@@ -281,22 +283,25 @@ __host__ __device__ inline DpLayout dp_layout(int y, int kc, int x_max, bool f_s
   o += al16(sizeof(double) * kMaxTile * kMaxTile);
   L.acc = o;
   o += al16(sizeof(double) * kDpThreads * kCells);
-  L.f = o;
-  o += f_smem ? al16(sizeof(double) * (size_t)(kc + 1) * (x_max - 1)) : 0;
+  L.fs = o;
+  o += al16(sizeof(double) * kMaxTile * kFsW);
+  L.ft = o;
+  o += al16(sizeof(double) * kMaxTile * kFtW);
   L.total = o;
   return L;
 }
 
 // Span terms for s in [s0, s0+ns) x t in [t0, t0+nt) (mutual_info.cpp:39-41,
 // 62): A = c_s/c_t, W = ((c_t - c_s)/c_t) h_span(s,t), h by the reference's
-// sequential row sum.  Entries with s >= t or t > k are left undefined.
+// sequential row sum.  The two quotients come from the exact c_s/c_t table
+// when it exists (same IEEE quotient, no DDIV).  Entries with s >= t or t > k
+// are left undefined.
 __device__ __forceinline__ void span_terms(const Tables& tb, const int* cb, const int* cum, int kk,
                                            int rows, int k, int s0, int ns, int t0, int nt,
                                            double* A, double* W) {
   const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int sl = threadIdx.x >> 5; sl < ns; sl += nw) {
     const int s = s0 + sl, cs = cb[s];
-    const double dcs = (double)cs;
     for (int tl = lane; tl < nt; tl += 32) {
       const int t = t0 + tl;
       if (s >= t || t > k) continue;
@@ -305,30 +310,46 @@ __device__ __forceinline__ void span_terms(const Tables& tb, const int* cb, cons
       double acch = 0.0;
       for (int r = 0; r < rows; ++r)
         acch = __dadd_rn(acch, __ldg(plm + (cum[r * kk + t] - cum[r * kk + s])));
-      const double dct = (double)ct;
-      A[sl * kMaxTile + tl] = __ddiv_rn(dcs, dct);
-      W[sl * kMaxTile + tl] = __dmul_rn(__ddiv_rn(__dsub_rn(dct, dcs), dct), -acch);
+      double a, q;
+      if (tb.div) {
+        const double* dr = tb.div + tri(ct);
+        a = __ldg(dr + cs);
+        q = __ldg(dr + (ct - cs));
+      } else {
+        const double dcs = (double)cs, dct = (double)ct;
+        a = __ddiv_rn(dcs, dct);
+        q = __ddiv_rn(__dsub_rn(dct, dcs), dct);
+      }
+      A[sl * kMaxTile + tl] = a;
+      W[sl * kMaxTile + tl] = __dmul_rn(q, -acch);
     }
   }
 }
 
-template <bool FSM>
-__global__ void __launch_bounds__(kDpThreads, 1) k_dp(VarSet vs, Tables tb, PairSpace ps,
-                                                   long long base, long long nsub, YParams yp,
-                                                   GenScratch gs, double* __restrict__ ocells,
-                                                   SubDebug dbg, int has_dbg, int orient_only) {
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// F lives in a per-CTA HBM slot (L2-resident for typical sizes); each outer
+// s-chunk's rows are staged into shared memory with coalesced loads, and the
+// current t-tile's rows are kept in shared memory while its inner part runs.
+__global__ void __launch_bounds__(kDpThreads, 2) k_dp(VarSet vs, Tables tb, PairSpace ps,
+                                                      long long base, long long nsub, YParams yp,
+                                                      GenScratch gs, double* __restrict__ ocells,
+                                                      SubDebug dbg, int has_dbg, int orient_only) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ long long s_sub;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int y = yp.y, x_max = yp.x_max, kc = gs.kc, LW = x_max - 1;
-  const DpLayout L = dp_layout(y, kc, x_max, FSM);
+  const DpLayout L = dp_layout(y, kc);
   int* cb = reinterpret_cast<int*>(smem + L.cb);
   int* cum = reinterpret_cast<int*>(smem + L.cum);
   double* A = reinterpret_cast<double*>(smem + L.A);
   double* W = reinterpret_cast<double*>(smem + L.W);
   double* accS = reinterpret_cast<double*>(smem + L.acc);
-  double* F = FSM ? reinterpret_cast<double*>(smem + L.f)
-                  : gs.fslots + (size_t)blockIdx.x * (size_t)(kc + 1) * LW;
+  double* fs = reinterpret_cast<double*>(smem + L.fs);
+  double* ft = reinterpret_cast<double*>(smem + L.ft);
+  double* F = gs.fslots + (size_t)blockIdx.x * (size_t)(kc + 1) * LW;
   const int norient = orient_only >= 0 ? 1 : 2;
 
   for (;;) {
@@ -354,16 +375,17 @@ __global__ void __launch_bounds__(kDpThreads, 1) k_dp(VarSet vs, Tables tb, Pair
 
     // Level tiles of <= 64 levels.  A thread owns 8 cells: two adjacent t
     // (t0 + 2p, t0 + 2p + 1) x a group of 4 consecutive levels, so each s
-    // costs one 16-byte load for both A, one for both W and four F loads for
-    // 8 independent max chains.  T t's per tile with (T/2) * groups <= 256.
+    // costs one 16-byte load for both A, one for both W and two for four F
+    // values, feeding 8 independent max chains.  (T/2) * groups <= 256.
     for (int l0 = 3; l0 <= l_max; l0 += 64) {
       const int l1 = min(l0 + 63, l_max), nl = l1 - l0 + 1;
       const int ng = (nl + 3) >> 2;
       const int T = max(2, min(kMaxTile, 2 * (kDpThreads / ng)));
       const int t_lo = (l0 == l_max) ? k : l0;  // level l_max is needed at t = k only
       const int my_tp = tid / ng, my_g = tid - my_tp * ng;
-      const int my_l = l0 + 4 * my_g;           // first of my 4 levels
-      const int my_tl = 2 * my_tp;              // first of my 2 t's (tile-local)
+      const int my_l = l0 + 4 * my_g;  // first of my 4 levels
+      const int my_tl = 2 * my_tp;     // first of my 2 t's (tile-local)
+      const int inner_threads = ((nl + 31) >> 5) << 5;
       for (int t0 = t_lo; t0 <= k; t0 += T) {
         const int nt = min(T, k - t0 + 1);
         const bool owner = my_tl < nt;
@@ -374,70 +396,76 @@ __global__ void __launch_bounds__(kDpThreads, 1) k_dp(VarSet vs, Tables tb, Pair
         for (int s0 = max(2, l0 - 1); s0 < t0; s0 += T) {
           const int ns = min(T, t0 - s0);
           span_terms(tb, cb, cum, kk, rows, k, s0, ns, t0, nt, A, W);
+          for (int i = tid; i < ns * nl; i += kDpThreads) {  // stage F(s, l0-1 .. l1-1)
+            const int sl = i / nl, j = i - sl * nl;
+            fs[sl * kFsW + j] = F[(size_t)(s0 + sl) * LW + (l0 - 3) + j];
+          }
           __syncthreads();
           if (owner) {
             // s >= l - 1 holds for all 4 levels once s >= my_l + 2; only the
-            // first chunk(s) near the diagonal need the per-level test.
-            // Cells that are not valid accumulate garbage that is never read.
+            // chunk(s) near the diagonal need the per-level test.  Cells that
+            // are not valid accumulate garbage that is never read.
+            const double* fr = fs + 4 * my_g;
             int sl = 0;
             for (; sl < ns && s0 + sl < my_l + 2; ++sl) {
               const int s = s0 + sl;
               const double2 a = *reinterpret_cast<const double2*>(A + sl * kMaxTile + my_tl);
               const double2 w = *reinterpret_cast<const double2*>(W + sl * kMaxTile + my_tl);
-              const double* fr = F + (size_t)s * LW + (my_l - 3);
 #pragma unroll
               for (int i = 0; i < 4; ++i)
                 if (s >= my_l + i - 1) {
-                  const double f = fr[i];
+                  const double f = fr[sl * kFsW + i];
                   acc[i] = dmax(acc[i], __dsub_rn(__dmul_rn(a.x, f), w.x));
                   acc[4 + i] = dmax(acc[4 + i], __dsub_rn(__dmul_rn(a.y, f), w.y));
                 }
             }
-            const double* Ap = A + my_tl;
-            const double* Wp = W + my_tl;
-            const double* fr = F + (size_t)(s0 + sl) * LW + (my_l - 3);
 #pragma unroll 2
-            for (; sl < ns; ++sl, fr += LW) {
-              const double2 a = *reinterpret_cast<const double2*>(Ap + sl * kMaxTile);
-              const double2 w = *reinterpret_cast<const double2*>(Wp + sl * kMaxTile);
-              const double f0 = fr[0], f1 = fr[1], f2 = fr[2], f3 = fr[3];
-              acc[0] = dmax(acc[0], __dsub_rn(__dmul_rn(a.x, f0), w.x));
-              acc[1] = dmax(acc[1], __dsub_rn(__dmul_rn(a.x, f1), w.x));
-              acc[2] = dmax(acc[2], __dsub_rn(__dmul_rn(a.x, f2), w.x));
-              acc[3] = dmax(acc[3], __dsub_rn(__dmul_rn(a.x, f3), w.x));
-              acc[4] = dmax(acc[4], __dsub_rn(__dmul_rn(a.y, f0), w.y));
-              acc[5] = dmax(acc[5], __dsub_rn(__dmul_rn(a.y, f1), w.y));
-              acc[6] = dmax(acc[6], __dsub_rn(__dmul_rn(a.y, f2), w.y));
-              acc[7] = dmax(acc[7], __dsub_rn(__dmul_rn(a.y, f3), w.y));
+            for (; sl < ns; ++sl) {
+              const double2 a = *reinterpret_cast<const double2*>(A + sl * kMaxTile + my_tl);
+              const double2 w = *reinterpret_cast<const double2*>(W + sl * kMaxTile + my_tl);
+              const double2 f01 = *reinterpret_cast<const double2*>(fr + sl * kFsW);
+              const double2 f23 = *reinterpret_cast<const double2*>(fr + sl * kFsW + 2);
+              acc[0] = dmax(acc[0], __dsub_rn(__dmul_rn(a.x, f01.x), w.x));
+              acc[1] = dmax(acc[1], __dsub_rn(__dmul_rn(a.x, f01.y), w.x));
+              acc[2] = dmax(acc[2], __dsub_rn(__dmul_rn(a.x, f23.x), w.x));
+              acc[3] = dmax(acc[3], __dsub_rn(__dmul_rn(a.x, f23.y), w.x));
+              acc[4] = dmax(acc[4], __dsub_rn(__dmul_rn(a.y, f01.x), w.y));
+              acc[5] = dmax(acc[5], __dsub_rn(__dmul_rn(a.y, f01.y), w.y));
+              acc[6] = dmax(acc[6], __dsub_rn(__dmul_rn(a.y, f23.x), w.y));
+              acc[7] = dmax(acc[7], __dsub_rn(__dmul_rn(a.y, f23.y), w.y));
             }
           }
           __syncthreads();
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) accS[tid * 8 + i] = acc[i];
-        // ---- inner part: s inside the tile, one t at a time, a level per thread
+        // ---- inner part: s inside the tile, one t at a time, a level per
+        // thread; only the warps holding levels take part (named barrier).
         span_terms(tb, cb, cum, kk, rows, k, t0, nt, t0, nt, A, W);
+        for (int tl = tid; tl < nt; tl += kDpThreads)  // column 0: level l0 - 1
+          ft[tl * kFtW] = F[(size_t)(t0 + tl) * LW + (l0 - 3)];
         __syncthreads();
-        for (int tl = 0; tl < nt; ++tl) {
-          const int tt = t0 + tl;
-          const int ll = tid;  // nl <= 64
-          if (ll < nl) {
-            const int l = l0 + ll;
-            if (tt >= l && !(l == l_max && tt != k)) {
+        if (tid < inner_threads) {
+          const int ll = tid, l = l0 + ll;
+          for (int tl = 0; tl < nt; ++tl) {
+            const int tt = t0 + tl;
+            if (ll < nl && tt >= l && !(l == l_max && tt != k)) {
               // owner of cell (tl, ll): thread (tl/2)*ng + ll/4, slot (tl&1)*4 + (ll&3)
               double m = accS[((tl >> 1) * ng + (ll >> 2)) * 8 + (tl & 1) * 4 + (ll & 3)];
               const double* Ap = A + tl;
               const double* Wp = W + tl;
               for (int s = max(t0, l - 1); s < tt; ++s) {
                 const int sl = s - t0;
-                m = dmax(m, __dsub_rn(__dmul_rn(Ap[sl * kMaxTile], F[(size_t)s * LW + (l - 3)]),
+                m = dmax(m, __dsub_rn(__dmul_rn(Ap[sl * kMaxTile], ft[sl * kFtW + ll]),
                                       Wp[sl * kMaxTile]));
               }
+              ft[tl * kFtW + ll + 1] = m;
               F[(size_t)tt * LW + (l - 2)] = m;
             }
+            named_sync(1, inner_threads);
           }
-          __syncthreads();
         }
+        __syncthreads();
       }
     }
     // ---- I_l (mutual_info.cpp:68-70) and the cells
@@ -454,6 +482,21 @@ __global__ void __launch_bounds__(kDpThreads, 1) k_dp(VarSet vs, Tables tb, Pair
   }
 }
 
+// Exact quotient table div[tri(m) + w] = w / m (IEEE, as the reference's
+// c[s] / c[t]), so the span terms need no DDIV.
+__global__ void k_build_div(double* div, int n) {
+  const unsigned long long total = (unsigned long long)(n + 1) * (n + 2) / 2;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < total;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    // invert i = m(m+1)/2 + w
+    unsigned long long m = (unsigned long long)((sqrt(8.0 * (double)i + 1.0) - 1.0) / 2.0);
+    while (m * (m + 1) / 2 > i) --m;
+    while ((m + 1) * (m + 2) / 2 <= i) ++m;
+    const unsigned long long w = i - m * (m + 1) / 2;
+    div[i] = m ? __ddiv_rn((double)w, (double)m) : 0.0;
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -467,30 +510,29 @@ size_t gen_scratch_per_sub(int n, const YParams& yp) {
 
 size_t gen_pf_smem(int n, const YParams& yp) { return pf_layout(n, yp.y, gen_kc(n, yp)).total; }
 
-// F in shared memory only when a CTA then still leaves room for a second one
-// per SM; a bigger F goes to a per-CTA HBM slot (L1/L2-cached), which keeps
-// 2-3 CTAs per SM resident -- measured faster on c3 than 1 CTA with smem F.
-bool gen_dp_f_in_smem(int n, const YParams& yp) {
-  const char* env = getenv("MINE_B200_DP_FSMEM_KB");
-  const size_t limit = (env ? (size_t)atoi(env) : 110) * 1024;
-  return dp_layout(yp.y, gen_kc(n, yp), yp.x_max, true).total <= limit;
-}
+bool gen_dp_f_in_smem(int, const YParams&) { return false; }
 
-size_t gen_dp_smem(int n, const YParams& yp) {
-  return dp_layout(yp.y, gen_kc(n, yp), yp.x_max, gen_dp_f_in_smem(n, yp)).total;
-}
+size_t gen_dp_smem(int n, const YParams& yp) { return dp_layout(yp.y, gen_kc(n, yp)).total; }
 
 size_t gen_fslot_bytes(int n, const YParams& yp) {
   return sizeof(double) * (size_t)(gen_kc(n, yp) + 1) * (yp.x_max - 1);
 }
 
 int gen_dp_grid(int n, const YParams& yp) {
-  int dev = 0, sms = 148, per = 1;
+  int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t sm = gen_dp_smem(n, yp);
-  per = (int)std::max<size_t>(1, std::min<size_t>(8, (228 * 1024) / (sm + 1024)));
+  const int per = (int)std::max<size_t>(1, std::min<size_t>(2, (228 * 1024) / (sm + 1024)));
   return sms * per;
+}
+
+size_t div_table_doubles(int n) { return (size_t)(n + 1) * (n + 2) / 2; }
+
+void launch_build_div(double* div, int n, cudaStream_t s) {
+  const size_t total = div_table_doubles(n);
+  const unsigned blocks = (unsigned)std::min<size_t>(4096, (total + 255) / 256);
+  k_build_div<<<blocks, 256, 0, s>>>(div, n);
 }
 
 void launch_part_f2(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
@@ -510,18 +552,12 @@ void launch_dp(const VarSet& vs, const Tables& tb, const PairSpace& ps, long lon
                const SubDebug* dbg, int orient_only, cudaStream_t s) {
   if (npairs <= 0 || yp.x_max < 3) return;
   const long long nsub = npairs * (orient_only >= 0 ? 1 : 2);
-  const bool fsm = gen_dp_f_in_smem(vs.n, yp);
   const int grid = (int)std::min<long long>(nsub, gen_dp_grid(vs.n, yp));
   SubDebug d{};
   if (dbg) d = *dbg;
   cudaMemsetAsync(gs.queue, 0, sizeof(unsigned long long), s);
-  const size_t sm = gen_dp_smem(vs.n, yp);
-  if (fsm)
-    k_dp<true><<<grid, kDpThreads, sm, s>>>(vs, tb, ps, base, nsub, yp, gs, ocells, d, dbg ? 1 : 0,
-                                            orient_only);
-  else
-    k_dp<false><<<grid, kDpThreads, sm, s>>>(vs, tb, ps, base, nsub, yp, gs, ocells, d, dbg ? 1 : 0,
-                                             orient_only);
+  k_dp<<<grid, kDpThreads, gen_dp_smem(vs.n, yp), s>>>(vs, tb, ps, base, nsub, yp, gs, ocells, d,
+                                                      dbg ? 1 : 0, orient_only);
 }
 
 cudaError_t init_general_attributes(int device) {
@@ -529,8 +565,7 @@ cudaError_t init_general_attributes(int device) {
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (e != cudaSuccess) return e;
   const void* fns[] = {reinterpret_cast<const void*>(k_part_f2),
-                       reinterpret_cast<const void*>(k_dp<true>),
-                       reinterpret_cast<const void*>(k_dp<false>)};
+                       reinterpret_cast<const void*>(k_dp)};
   for (const void* f : fns) {
     cudaFuncAttributes fa{};
     e = cudaFuncGetAttributes(&fa, f);

@@ -9,11 +9,10 @@
 // Pipeline of one call:
 //   K1 k_sort_vars      per variable: stable rank, tie-run structure       (partition.cpp:13-38)
 //   K2 k_equipartition  per (variable, y): greedy row map Q, yhat, H(Q)      (partition.cpp:42-67, A1)
+//   memo tier  k_memo_pairs   n <= 24, B <= 7 (c1): one thread per pair, tabulated F(t,2) candidates
 //   tiny tier  k_tiny_pairs   n <= 32, B <= 7: one thread per pair, all stages in registers
-//   general    k_general      one CTA per (pair, orientation) at one y:
-//                               clumps/superclumps/cell counts (partition.cpp:108-165,
-//                               mutual_info.cpp:9-24) + t-outer exact DP (mutual_info.cpp:26-72)
-//              k_reduce       per pair: max-merge + MIC/MAS/MEV/MCN/MIC_e/TIC (statistics.cpp:10-37)
+//   general    mine_general.cu: k_part_f2 + k_dp per y, then k_reduce here
+//              (max-merge + MIC/MAS/MEV/MCN/MIC_e/TIC, statistics.cpp:10-37)
 #include <algorithm>
 #include <cfloat>
 #include <cstdint>
@@ -729,268 +728,6 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
   if (counters) flush_work(work, counters);
 }
 
-// ---------------------------------------------------------------------------
-// General tier.  One CTA per (pair, orientation) at one row target y.
-constexpr int kGenThreads = 256;
-constexpr int kGenWarps = kGenThreads / 32;
-
-struct GenLayout {
-  size_t f, r1, wv, part, red, cum, cb, cl, sup, lab, fused, misc, total;
-};
-
-__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
-
-__host__ __device__ inline GenLayout gen_layout(int n, int y, int x_max, int k_hat, bool f_smem) {
-  GenLayout L;
-  const int kmax = min(n, k_hat);
-  const int lw = x_max - 1;
-  size_t o = 0;
-  L.f = o;
-  o += f_smem ? align16(sizeof(double) * (size_t)(kmax + 1) * lw) : 0;
-  L.r1 = o;
-  o += align16(sizeof(double) * (kmax + 1));
-  L.wv = o;
-  o += align16(sizeof(double) * (kmax + 1));
-  L.part = o;
-  o += align16(sizeof(double) * kGenWarps * 32);
-  L.red = o;
-  o += align16(sizeof(double) * 32);
-  L.cum = o;
-  o += align16(sizeof(int) * (size_t)y * (kmax + 1));
-  L.cb = o;
-  o += align16(sizeof(int) * (n + 1));
-  L.cl = o;
-  o += align16(sizeof(int) * n);
-  L.sup = o;
-  o += align16(sizeof(int) * (n + 1));
-  L.lab = o;
-  o += align16(sizeof(uint16_t) * n);
-  L.fused = o;
-  o += align16(n);
-  L.misc = o;
-  o += align16(sizeof(int) * 64);
-  L.total = o;
-  return L;
-}
-
-__global__ void __launch_bounds__(kGenThreads) k_general(VarSet vs, Tables tb, PairSpace ps,
-                                                         long long base, YParams yp,
-                                                         double* __restrict__ ocells,
-                                                         double* __restrict__ fscratch,
-                                                         SubDebug dbg, int has_dbg,
-                                                         int orient_only, int f_smem,
-                                                         unsigned long long* counters) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int n = vs.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int norient = orient_only >= 0 ? 1 : 2;
-  const long long pl_ = base + blockIdx.x / norient;
-  const int orient = orient_only >= 0 ? orient_only : (int)(blockIdx.x % 2);
-  int va, vb;
-  pair_vars(ps, ps.first + pl_, va, vb);
-  const int X = orient ? vb : va, Y = orient ? va : vb;
-  const int y = yp.y, yi = yp.yi, x_max = yp.x_max, k_hat = yp.k_hat;
-  const int kmax = min(n, k_hat), LW = x_max - 1;
-
-  const GenLayout L = gen_layout(n, y, x_max, k_hat, f_smem != 0);
-  double* F = f_smem ? reinterpret_cast<double*>(smem + L.f)
-                     : fscratch + (size_t)blockIdx.x * (size_t)(kmax + 1) * LW;
-  double* r1 = reinterpret_cast<double*>(smem + L.r1);
-  double* wv = reinterpret_cast<double*>(smem + L.wv);
-  double* part = reinterpret_cast<double*>(smem + L.part);
-  double* red = reinterpret_cast<double*>(smem + L.red);
-  int* cum = reinterpret_cast<int*>(smem + L.cum);
-  int* cb = reinterpret_cast<int*>(smem + L.cb);
-  int* cl = reinterpret_cast<int*>(smem + L.cl);
-  int* sup = reinterpret_cast<int*>(smem + L.sup);
-  uint16_t* lab = reinterpret_cast<uint16_t*>(smem + L.lab);
-  uint8_t* fused = smem + L.fused;
-  int* misc = reinterpret_cast<int*>(smem + L.misc);
-
-  const int* permX = vs.perm + (size_t)X * n;
-  const int* ridX = vs.runid + (size_t)X * n;
-  const uint16_t* qY = vs.q + ((size_t)Y * vs.ny + yi) * n;
-  const int rows = vs.yhat[(size_t)Y * vs.ny + yi];
-  const double hq = vs.hq[(size_t)Y * vs.ny + yi];
-
-  // --- row labels in x-sorted order (reindex_to_first_order, partition.cpp:94-106)
-  for (int t = tid; t < n; t += kGenThreads) {
-    lab[t] = qY[permX[t]];
-    fused[t] = 0;
-  }
-  __syncthreads();
-  // --- Alg. 1 (partition.cpp:116-133): a tie run of x whose labels change is fused
-  for (int t = tid + 1; t < n; t += kGenThreads)
-    if (ridX[t] == ridX[t - 1] && lab[t] != lab[t - 1]) fused[ridX[t]] = 1;
-  __syncthreads();
-  // --- clump starts (:135-144): label change at a run start, or either run fused
-  for (int t = tid; t < n; t += kGenThreads) {
-    int f = 0;
-    if (t > 0) {
-      const int a = ridX[t], b = ridX[t - 1];
-      f = a != b && (fused[a] || fused[b] || lab[t] != lab[t - 1]);
-    }
-    cl[t] = f;
-  }
-  __syncthreads();
-  const int kraw = block_incl_scan(cl, n, misc) + 1;  // cl[t] = clump index of position t
-  for (int t = tid + 1; t < n; t += kGenThreads)
-    if (cl[t] != cl[t - 1]) cb[cl[t]] = t;
-  if (tid == 0) {
-    cb[0] = 0;
-    cb[kraw] = n;
-  }
-  __syncthreads();
-  // --- Alg. 2 (partition.cpp:148-165): equipartition clump ordinals into <= k_hat
-  int k = kraw;
-  if (kraw > k_hat) {
-    if (tid == 0) {
-      double desired = (double)n / (double)k_hat;
-      int curr = 1, in_row = 0;
-      for (int j = 0; j < kraw; ++j) {
-        const int i = cb[j], run = cb[j + 1] - i;
-        if (in_row != 0 &&
-            fabs((double)(in_row + run) - desired) >= fabs((double)in_row - desired)) {
-          ++curr;
-          in_row = 0;
-          desired = (double)(n - i) / (double)(k_hat - curr + 1);
-          cb[curr - 1] = i;  // in place: curr - 1 <= j
-        }
-        sup[j] = curr - 1;
-        in_row += run;
-      }
-      cb[curr] = n;
-      misc[40] = curr;
-    }
-    __syncthreads();
-    k = misc[40];
-  } else {
-    for (int j = tid; j < kraw; j += kGenThreads) sup[j] = j;
-  }
-  // --- cell counts and cumulative table (mutual_info.cpp:9-24), cum[r][j]
-  const int kk = k + 1;
-  for (int i = tid; i < rows * kk; i += kGenThreads) cum[i] = 0;
-  __syncthreads();
-  for (int t = tid; t < n; t += kGenThreads) atomicAdd(&cum[(lab[t] - 1) * kk + sup[cl[t]] + 1], 1);
-  __syncthreads();
-  for (int r = warp; r < rows; r += kGenWarps) {  // warp-scan each row over clumps
-    int carry = 0;
-    for (int j0 = 1; j0 <= k; j0 += 32) {
-      const int j = j0 + lane;
-      int v = j <= k ? cum[r * kk + j] : 0;
-      v = warp_incl_scan(v) + carry;
-      if (j <= k) cum[r * kk + j] = v;
-      carry = __shfl_sync(0xffffffffu, v, 31);
-    }
-  }
-  __syncthreads();
-
-  if (counters && tid == 0) {
-    unsigned long long w[kNumCounters] = {0, 0, 0, 0, 0, 0};
-    subproblem_work(rows, k, x_max, w);
-    for (int i = 0; i < kNumCounters; ++i)
-      if (w[i]) atomicAdd(counters + i, w[i]);
-  }
-  if (has_dbg && tid == 0) {
-    *dbg.row_count = rows;
-    *dbg.raw_k = kraw;
-    *dbg.k = k;
-    *dbg.h_q = hq;
-  }
-  if (has_dbg) {
-    for (int t = tid; t < n; t += kGenThreads) dbg.q_x[t] = lab[t];
-    for (int j = tid; j <= k; j += kGenThreads) dbg.bounds[j] = cb[j];
-  }
-
-  // --- exact OptimizeXAxis DP (mutual_info.cpp:26-72), t-outer ---------------
-  const int l_max = min(x_max, k);
-  const double* pl = tb.pl;
-  if (k >= 2) {
-    const int t_begin = l_max >= 3 ? 2 : k;  // x_max == 2 needs F(k,2) only
-    for (int t = t_begin; t <= k; ++t) {
-      const int ct = cb[t];
-      const double* plt = pl + tri(ct);
-      // phase A: threads over s -- F(t,2) candidates and, for levels >= 3, the
-      // span terms r1 = c_s/c_t and wv = ((c_t - c_s)/c_t) h_span(s,t).
-      double best = kLowest;
-      for (int s = 1 + tid; s < t; s += kGenThreads) {
-        const int cs = cb[s];
-        double acc2 = plt[cs];
-        acc2 = __dadd_rn(acc2, plt[ct - cs]);
-        double accj = 0.0;
-        for (int r = 0; r < rows; ++r) accj = __dadd_rn(accj, plt[cum[r * kk + s]]);
-        for (int r = 0; r < rows; ++r) accj = __dadd_rn(accj, plt[cum[r * kk + t] - cum[r * kk + s]]);
-        best = dmax(best, __dsub_rn(-acc2, -accj));
-        if (l_max >= 3 && s >= 2) {
-          const double* plm = pl + tri(ct - cs);
-          double acch = 0.0;
-          for (int r = 0; r < rows; ++r) acch = __dadd_rn(acch, plm[cum[r * kk + t] - cum[r * kk + s]]);
-          const double dcs = (double)cs, dct = (double)ct;
-          r1[s] = __ddiv_rn(dcs, dct);
-          wv[s] = __dmul_rn(__ddiv_rn(__dsub_rn(dct, dcs), dct), -acch);
-        }
-      }
-      best = warp_max(best);
-      if (lane == 0) red[warp] = best;
-      __syncthreads();
-      if (tid == 0) {
-        double b = red[0];
-        for (int w = 1; w < kGenWarps; ++w) b = dmax(b, red[w]);
-        F[(size_t)t * LW + 0] = b;
-      }
-      // phase B: levels 3 .. l_hi from F(s, l-1), s in [l-1, t-1]
-      const int l_hi = t == k ? min(t, l_max) : min(t, l_max - 1);
-      const int nlev = l_hi - 2;
-      if (nlev >= 8) {
-        // lanes over levels, warps over s (strided); partial maxima then reduce
-        for (int l0 = 3; l0 <= l_hi; l0 += 32) {
-          const int l = l0 + lane;
-          double pm = kLowest;
-          if (l <= l_hi)
-            for (int s = max(2, l - 1) + warp; s < t; s += kGenWarps)
-              pm = dmax(pm, __dsub_rn(__dmul_rn(r1[s], F[(size_t)s * LW + (l - 3)]), wv[s]));
-          // stagger warps that start below l-1: the loop start differs per lane
-          part[warp * 32 + lane] = pm;
-          __syncthreads();
-          if (warp == 0 && l <= l_hi) {
-            double b = part[lane];
-            for (int w = 1; w < kGenWarps; ++w) b = dmax(b, part[w * 32 + lane]);
-            F[(size_t)t * LW + (l - 2)] = b;
-          }
-          __syncthreads();
-        }
-      } else if (nlev >= 1) {
-        // one warp per level, lanes over s, shuffle max
-        for (int l = 3 + warp; l <= l_hi; l += kGenWarps) {
-          double pm = kLowest;
-          for (int s = l - 1 + lane; s < t; s += 32)
-            pm = dmax(pm, __dsub_rn(__dmul_rn(r1[s], F[(size_t)s * LW + (l - 3)]), wv[s]));
-          pm = warp_max(pm);
-          if (lane == 0) F[(size_t)t * LW + (l - 2)] = pm;
-        }
-        __syncthreads();
-      } else {
-        __syncthreads();
-      }
-    }
-  }
-  __syncthreads();
-  // --- I_l, normalisation and per-orientation cells (char_matrix.cpp:57-64)
-  double* oc = ocells + (size_t)pl_ * 2 * tb.ncell + (size_t)orient * tb.ncell;
-  const double logy = tb.logi[rows];
-  for (int l = 2 + tid; l <= x_max; l += kGenThreads) {
-    double I;
-    if (k < 2) {
-      I = 0.0;
-    } else {
-      const int le = l <= l_max ? l : l_max;
-      I = dmax(0.0, __dadd_rn(hq, F[(size_t)k * LW + (le - 2)]));
-    }
-    if (has_dbg) dbg.values[l - 2] = I;
-    const int cell = orient ? tb.cell_off[l] + (y - 2) : tb.cell_off[y] + (l - 2);
-    oc[cell] = norm_cell(I, tb.logi[l], logy);
-  }
-}
-
 // Per-pair reduction: max-merge of the orientations (update_max,
 // char_matrix.cpp:28-35) and the statistics (statistics.cpp:10-37) plus the
 // extensions MIC_e / TIC.  One warp per pair.
@@ -1056,8 +793,7 @@ cudaError_t init_kernel_attributes(int device) {
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (e != cudaSuccess) return e;
   const void* fns[] = {reinterpret_cast<const void*>(k_sort_vars),
-                       reinterpret_cast<const void*>(k_memo_pairs),
-                       reinterpret_cast<const void*>(k_general)};
+                       reinterpret_cast<const void*>(k_memo_pairs)};
   for (const void* f : fns) {
     cudaFuncAttributes fa{};
     e = cudaFuncGetAttributes(&fa, f);
@@ -1129,28 +865,6 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo, c
   const long long need = (ps.count + threads - 1) / threads;
   const unsigned blocks = (unsigned)std::min<long long>(sms, need);
   k_memo_pairs<<<blocks, threads, sm, s>>>(vs, tb, memo, ps, c, est, out, o_cells, counters);
-}
-
-size_t general_smem_bytes(int n, const YParams& yp, bool f_in_smem) {
-  return gen_layout(n, yp.y, yp.x_max, yp.k_hat, f_in_smem).total;
-}
-
-bool general_f_fits(int n, const YParams& yp) {
-  return general_smem_bytes(n, yp, true) <= 200 * 1024;
-}
-
-void launch_general(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
-                    long long npairs, const YParams& yp, double* ocells, double* fscratch,
-                    const SubDebug* dbg, int orient_only, unsigned long long* counters,
-                    cudaStream_t s) {
-  if (npairs <= 0) return;
-  const bool fs = fscratch == nullptr;
-  const size_t sm = general_smem_bytes(vs.n, yp, fs);
-  const unsigned blocks = (unsigned)(npairs * (orient_only >= 0 ? 1 : 2));
-  SubDebug d{};
-  if (dbg) d = *dbg;
-  k_general<<<blocks, kGenThreads, sm, s>>>(vs, tb, ps, base, yp, ocells, fscratch, d,
-                                            dbg ? 1 : 0, orient_only, fs ? 1 : 0, counters);
 }
 
 void launch_reduce(const Tables& tb, long long npairs, const double* ocells, int est, StatsOut out,

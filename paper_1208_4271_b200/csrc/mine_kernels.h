@@ -44,6 +44,7 @@ struct Tables {
   const int* cell_xy = nullptr;   // x * y of cell c
   const uint8_t* cell_edge = nullptr;  // x == 2 || y == 2
   const int8_t* cell_cmp = nullptr;    // sign(x - y): which orientation feeds MIC_e
+  const double* div = nullptr;    // w / m at tri(m) + w (exact IEEE quotients), n <= 4096 only
   int n = 0;
   int B = 0;
   int ncell = 0;
@@ -118,7 +119,7 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo, c
                        double c, int est, StatsOut out, double* o_cells,
                        unsigned long long* counters, cudaStream_t s);
 
-// General tier v2 (mine_general.cu): k_part_f2 + persistent tiled k_dp per y.
+// General tier (mine_general.cu): k_part_f2 + persistent tiled k_dp per y.
 struct GenScratch {
   int* desc = nullptr;        // nsub x int4 {k, rows, raw k, l_max}
   int* cb = nullptr;          // nsub x (kc+1) clump boundaries
@@ -144,17 +145,9 @@ void launch_dp(const VarSet& vs, const Tables& tb, const PairSpace& ps, long lon
                long long npairs, const YParams& yp, const GenScratch& gs, double* ocells,
                const SubDebug* dbg, int orient_only, cudaStream_t s);
 cudaError_t init_general_attributes(int device);
+size_t div_table_doubles(int n);
+void launch_build_div(double* div, int n, cudaStream_t s);
 
-// General tier v1: one CTA per (pair, orientation) for one row target; writes the
-// normalised per-orientation cells into ocells[(pair - base) * 2 * ncell ...].
-// Returns false if the launch configuration is impossible (caller falls back
-// to nothing: the error surfaces through the C ABI).
-size_t general_smem_bytes(int n, const YParams& yp, bool f_in_smem);
-bool general_f_fits(int n, const YParams& yp);
-void launch_general(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
-                    long long npairs, const YParams& yp, double* ocells, double* fscratch,
-                    const SubDebug* dbg, int orient_only, unsigned long long* counters,
-                    cudaStream_t s);
 void launch_reduce(const Tables& tb, long long npairs, const double* ocells, int est,
                    StatsOut out, long long out_offset, cudaStream_t s);
 
