@@ -288,3 +288,27 @@ def test_errors_like_the_reference(engine):
         engine.compute_statistics([1, 2, 3, 4], [1, 2, 3, 4], Parameters(0.6, -1.0))
     with pytest.raises(MineError):
         engine.pairwise(np.zeros((3, 5)), first=2, count=5)
+
+
+@pytest.mark.slow
+def test_c4_full_size_properties(engine):
+    """c4 at its full size (n = 10,000, alpha = .75, B = 1000, est = MIC_e) --
+    the CPU oracle needs hours per pair here, so size-independent properties:
+    rank invariance and X/Y swap invariance bit-exact, bounds, and
+    functional vs independent separation.  Parity itself is pinned at
+    n = 1500 by test_golden_configs_gpu."""
+    w = datagen.make(4)
+    p = Parameters(w.alpha, w.c, w.est)
+    # Y_0 = 2u-1 + N(0,.05^2) is functional in X_0; pick one replaced (independent) Y
+    sel = [0, 1]
+    X = w.X[:1]
+    Y = w.Y[sel]
+    a = engine.cross(X, Y, p)
+    b = engine.cross(np.exp(X / 4.0), Y ** 3, p)  # strictly monotone transforms
+    for k in STAT_COLS:
+        assert_bit_equal(a[k], b[k], f"c4 monotone {k}")
+    c = engine.cross(Y, X, p)  # swapped roles: Y x X
+    for k in ("mic", "mas", "mev", "mcn", "mic_e"):
+        assert_bit_equal(a[k], c[k], f"c4 swap {k}")
+    assert np.all((a["mic"] >= 0) & (a["mic"] <= 1)) and np.all(a["mas"] <= a["mic"])
+    assert a["mic"][0] > 0.9  # near-noiseless linear relation
