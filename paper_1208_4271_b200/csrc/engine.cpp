@@ -185,7 +185,7 @@ struct mine_b200_ctx {
   std::mutex mu;
   TableSet tables;
   DevBuf vals, perm, runid, runstart, nruns, q, yhat, hq, lw, rsmask;
-  DevBuf ocells, fscratch, stats, flag, idx, counters, memo, rec, gscr, gqueue;
+  DevBuf ocells, fscratch, stats, flag, idx, counters, memo, rec, gscr, gqueue, glists;
   int memo_n = -1;
   std::vector<cudaEvent_t> events;
   long long launches = 0;
@@ -237,7 +237,10 @@ GenScratch gen_scratch(mine_b200_ctx* ctx, int n, const YParams& yp, long long n
   g.desc = reinterpret_cast<int*>(base + f2b);
   g.cb = reinterpret_cast<int*>(base + f2b + descb);
   g.cum = reinterpret_cast<int*>(base + f2b + descb + cbb);
-  g.queue = static_cast<unsigned long long*>(ctx->gqueue.ensure(sizeof(unsigned long long)));
+  g.queue = static_cast<unsigned long long*>(ctx->gqueue.ensure(4 * sizeof(unsigned long long)));
+  g.nsub = nsub;
+  g.lists = static_cast<long long*>(ctx->glists.ensure(2 * sizeof(long long) * (size_t)nsub));
+  g.small_ok = gen_warp_smem_per_warp(yp) <= 24 * 1024;
   if (yp.x_max >= 3)
     g.fslots = static_cast<double*>(
         ctx->fscratch.ensure(gen_fslot_bytes(n, yp) * (size_t)gen_dp_grid(n, yp)));
@@ -431,11 +434,13 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
     } else {
       for (const auto& yp : yps) {
         const GenScratch gs = gen_scratch(ctx, n, yp, 2 * cn);
+        CK(cudaMemsetAsync(gs.queue, 0, 4 * sizeof(unsigned long long), s));
         launch_part_f2(vs, tb, pc, 0, cn, yp, gs, ocells, nullptr, -1, dcnt, s);
         ++ctx->launches;
         if (yp.x_max >= 3) {
+          launch_dp_warp(vs, tb, pc, 0, cn, yp, gs, ocells, nullptr, -1, s);
           launch_dp(vs, tb, pc, 0, cn, yp, gs, ocells, nullptr, -1, s);
-          ++ctx->launches;
+          ctx->launches += gs.small_ok ? 2 : 1;
         }
       }
       launch_reduce(tb, cn, ocells, par->est, so, 0, s);
@@ -638,7 +643,9 @@ int mine_b200_debug_subproblem(mine_b200_ctx* ctx, int n, const double* col_var,
     dbg.bounds = ib + 3 + n;
     double* oc = static_cast<double*>(ctx->ocells.ensure(sizeof(double) * 2 * tb.ncell));
     const GenScratch gs = gen_scratch(ctx, n, yp, 1);
+    CK(cudaMemsetAsync(gs.queue, 0, 4 * sizeof(unsigned long long), s));
     launch_part_f2(vs, tb, ps, 0, 1, yp, gs, oc, &dbg, 0, nullptr, s);
+    launch_dp_warp(vs, tb, ps, 0, 1, yp, gs, oc, &dbg, 0, s);
     launch_dp(vs, tb, ps, 0, 1, yp, gs, oc, &dbg, 0, s);
     CK(cudaGetLastError());
     std::vector<char> h(bytes);

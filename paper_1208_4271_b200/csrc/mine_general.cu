@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kPfThreads) k_part_f2(VarSet vs, Tables tb, Pa
     for (int t = tid; t < n; t += kPfThreads) dbg.q_x[t] = lab[t];
     for (int j = tid; j <= k; j += kPfThreads) dbg.bounds[j] = cb[j];
   }
-  // hand the partition to k_dp
+  // hand the partition to k_dp_warp (k <= kSmallK) or k_dp
   if (l_max >= 3) {
     if (tid == 0) {
       int4 d;
@@ -214,6 +214,10 @@ __global__ void __launch_bounds__(kPfThreads) k_part_f2(VarSet vs, Tables tb, Pa
       d.z = kraw;
       d.w = l_max;
       reinterpret_cast<int4*>(gs.desc)[sub] = d;
+      if (gs.small_ok && k <= kSmallK)
+        gs.lists[atomicAdd(gs.queue + 2, 1ull)] = sub;
+      else
+        gs.lists[gs.nsub + (long long)atomicAdd(gs.queue + 3, 1ull)] = sub;
     }
     int* gcb = gs.cb + (size_t)sub * (kc + 1);
     int* gcum = gs.cum + (size_t)sub * gs.cum_stride;
@@ -354,10 +358,13 @@ __global__ void __launch_bounds__(kDpThreads, 2) k_dp(VarSet vs, Tables tb, Pair
 
   for (;;) {
     __syncthreads();
-    if (tid == 0) s_sub = atomicAdd(gs.queue, 1ull);
+    if (tid == 0) {
+      const unsigned long long i = atomicAdd(gs.queue, 1ull);
+      s_sub = i < gs.queue[3] ? gs.lists[gs.nsub + i] : -1;
+    }
     __syncthreads();
     const long long sub = s_sub;
-    if (sub >= nsub) break;
+    if (sub < 0) break;
     const int4 d = reinterpret_cast<const int4*>(gs.desc)[sub];
     const int k = d.x, rows = d.y, l_max = d.w, kk = k + 1;
     if (l_max < 3) continue;  // finished by k_part_f2
@@ -482,6 +489,121 @@ __global__ void __launch_bounds__(kDpThreads, 2) k_dp(VarSet vs, Tables tb, Pair
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp path: one warp per small subproblem (k <= kSmallK), t-outer with the
+// whole F table, the span column and the partition in this warp's slice of
+// shared memory -- no block-level synchronisation, so 16+ independent
+// subproblems interleave per SM.
+struct WarpLayout {
+  size_t F, A, W, cb, cum, per_warp;
+};
+
+__host__ __device__ inline WarpLayout warp_layout(int y, int x_max) {
+  WarpLayout L;
+  size_t o = 0;
+  L.F = o;
+  o += al16(sizeof(double) * (kSmallK + 1) * (size_t)(x_max - 1));
+  L.A = o;
+  o += al16(sizeof(double) * (kSmallK + 1));
+  L.W = o;
+  o += al16(sizeof(double) * (kSmallK + 1));
+  L.cb = o;
+  o += al16(sizeof(int) * (kSmallK + 1));
+  L.cum = o;
+  o += al16(sizeof(int) * (size_t)y * (kSmallK + 1));
+  L.per_warp = o;
+  return L;
+}
+
+constexpr int kWarpThreads = 256;
+
+__global__ void __launch_bounds__(kWarpThreads) k_dp_warp(VarSet vs, Tables tb, PairSpace ps,
+                                                          long long base, YParams yp,
+                                                          GenScratch gs,
+                                                          double* __restrict__ ocells,
+                                                          SubDebug dbg, int has_dbg,
+                                                          int orient_only) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int y = yp.y, x_max = yp.x_max, LW = x_max - 1, kc = gs.kc;
+  const WarpLayout L = warp_layout(y, x_max);
+  unsigned char* wb = smem + (size_t)wib * L.per_warp;
+  double* F = reinterpret_cast<double*>(wb + L.F);
+  double* A = reinterpret_cast<double*>(wb + L.A);
+  double* W = reinterpret_cast<double*>(wb + L.W);
+  int* cb = reinterpret_cast<int*>(wb + L.cb);
+  int* cum = reinterpret_cast<int*>(wb + L.cum);
+  const int norient = orient_only >= 0 ? 1 : 2;
+  const unsigned long long nsmall = gs.queue[2];
+  for (;;) {
+    unsigned long long i = 0;
+    if (lane == 0) i = atomicAdd(gs.queue + 1, 1ull);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i >= nsmall) break;
+    const long long sub = gs.lists[i];
+    const int4 d = reinterpret_cast<const int4*>(gs.desc)[sub];
+    const int k = d.x, rows = d.y, l_max = d.w, kk = k + 1;
+    {
+      const int* gcb = gs.cb + (size_t)sub * (kc + 1);
+      const int* gcum = gs.cum + (size_t)sub * gs.cum_stride;
+      const double* gf2 = gs.f2 + (size_t)sub * (kc + 1);
+      for (int j = lane; j <= k; j += 32) cb[j] = gcb[j];
+      for (int j = lane; j < rows * kk; j += 32) cum[j] = gcum[j];
+      for (int t = 2 + lane; t <= k; t += 32) F[t * LW] = gf2[t];
+    }
+    __syncwarp();
+    for (int t = 3; t <= k; ++t) {
+      // span column A(s,t), W(s,t) for s in [2, t)
+      const int ct = cb[t];
+      for (int s = 2 + lane; s < t; s += 32) {
+        const int cs = cb[s];
+        const double* plm = tb.pl + tri(ct - cs);
+        double acch = 0.0;
+        for (int r = 0; r < rows; ++r)
+          acch = __dadd_rn(acch, __ldg(plm + (cum[r * kk + t] - cum[r * kk + s])));
+        double a, q;
+        if (tb.div) {
+          const double* dr = tb.div + tri(ct);
+          a = __ldg(dr + cs);
+          q = __ldg(dr + (ct - cs));
+        } else {
+          const double dcs = (double)cs, dct = (double)ct;
+          a = __ddiv_rn(dcs, dct);
+          q = __ddiv_rn(__dsub_rn(dct, dcs), dct);
+        }
+        A[s] = a;
+        W[s] = __dmul_rn(q, -acch);
+      }
+      __syncwarp();
+      const int l_hi = t == k ? min(t, l_max) : min(t, l_max - 1);
+      for (int l = 3 + lane; l <= l_hi; l += 32) {
+        double m = kLowest;
+        const double* fc = F + (l - 3);
+        for (int s = l - 1; s < t; ++s)
+          m = dmax(m, __dsub_rn(__dmul_rn(A[s], fc[s * LW]), W[s]));
+        F[t * LW + (l - 2)] = m;
+      }
+      __syncwarp();
+    }
+    // I_l (mutual_info.cpp:68-70) and the cells (char_matrix.cpp:57-64)
+    const long long pl = base + sub / norient;
+    const int orient = orient_only >= 0 ? orient_only : (int)(sub % 2);
+    int X, Yv;
+    sub_vars(ps, pl, orient, X, Yv);
+    const double hq = vs.hq[(size_t)Yv * vs.ny + yp.yi];
+    double* oc = ocells + (size_t)pl * 2 * tb.ncell + (size_t)orient * tb.ncell;
+    const double logy = tb.logi[rows];
+    for (int l = 2 + lane; l <= x_max; l += 32) {
+      const int le = l <= l_max ? l : l_max;
+      const double v = dmax(0.0, __dadd_rn(hq, F[k * LW + (le - 2)]));
+      if (has_dbg) dbg.values[l - 2] = v;
+      const int cell = orient ? tb.cell_off[l] + (y - 2) : tb.cell_off[y] + (l - 2);
+      oc[cell] = norm_cell(v, tb.logi[l], logy);
+    }
+    __syncwarp();
+  }
+}
+
 // Exact quotient table div[tri(m) + w] = w / m (IEEE, as the reference's
 // c[s] / c[t]), so the span terms need no DDIV.
 __global__ void k_build_div(double* div, int n) {
@@ -527,6 +649,28 @@ int gen_dp_grid(int n, const YParams& yp) {
   return sms * per;
 }
 
+size_t gen_warp_smem_per_warp(const YParams& yp) { return warp_layout(yp.y, yp.x_max).per_warp; }
+
+void launch_dp_warp(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
+                    long long npairs, const YParams& yp, const GenScratch& gs, double* ocells,
+                    const SubDebug* dbg, int orient_only, cudaStream_t s) {
+  if (npairs <= 0 || yp.x_max < 3 || !gs.small_ok) return;
+  const size_t per_warp = gen_warp_smem_per_warp(yp);
+  const int warps = kWarpThreads / 32;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t sm = per_warp * warps;
+  const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / (sm + 1024)));
+  const long long nsub = npairs * (orient_only >= 0 ? 1 : 2);
+  const int grid = (int)std::max<long long>(1, std::min<long long>((nsub + warps - 1) / warps,
+                                                                    (long long)sms * per_sm));
+  SubDebug d{};
+  if (dbg) d = *dbg;
+  k_dp_warp<<<grid, kWarpThreads, sm, s>>>(vs, tb, ps, base, yp, gs, ocells, d, dbg ? 1 : 0,
+                                           orient_only);
+}
+
 size_t div_table_doubles(int n) { return (size_t)(n + 1) * (n + 2) / 2; }
 
 void launch_build_div(double* div, int n, cudaStream_t s) {
@@ -555,7 +699,6 @@ void launch_dp(const VarSet& vs, const Tables& tb, const PairSpace& ps, long lon
   const int grid = (int)std::min<long long>(nsub, gen_dp_grid(vs.n, yp));
   SubDebug d{};
   if (dbg) d = *dbg;
-  cudaMemsetAsync(gs.queue, 0, sizeof(unsigned long long), s);
   k_dp<<<grid, kDpThreads, gen_dp_smem(vs.n, yp), s>>>(vs, tb, ps, base, nsub, yp, gs, ocells, d,
                                                       dbg ? 1 : 0, orient_only);
 }
@@ -565,7 +708,8 @@ cudaError_t init_general_attributes(int device) {
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (e != cudaSuccess) return e;
   const void* fns[] = {reinterpret_cast<const void*>(k_part_f2),
-                       reinterpret_cast<const void*>(k_dp)};
+                       reinterpret_cast<const void*>(k_dp),
+                       reinterpret_cast<const void*>(k_dp_warp)};
   for (const void* f : fns) {
     cudaFuncAttributes fa{};
     e = cudaFuncGetAttributes(&fa, f);

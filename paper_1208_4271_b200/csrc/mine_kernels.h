@@ -126,10 +126,19 @@ struct GenScratch {
   int* cum = nullptr;         // nsub x cum_stride cumulative counts, row-major [r][j]
   double* f2 = nullptr;       // nsub x (kc+1) F(t,2)
   double* fslots = nullptr;   // grid x (kc+1) x (x_max-1) F tables (when not in smem)
-  unsigned long long* queue = nullptr;
+  unsigned long long* queue = nullptr;  // [0] k_dp queue, [1] k_dp_warp queue,
+                                        // [2] small-list length, [3] big-list length
+  long long* lists = nullptr; // [0, nsub): small subproblems, [nsub, 2 nsub): big ones
+  long long nsub = 0;
   int kc = 0;                 // min(n, k_hat)
   size_t cum_stride = 0;      // y * (kc+1)
+  int small_ok = 0;           // the warp path is available at this y
 };
+constexpr int kSmallK = 64;   // subproblems with k <= kSmallK take the warp path
+size_t gen_warp_smem_per_warp(const YParams& yp);
+void launch_dp_warp(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
+                    long long npairs, const YParams& yp, const GenScratch& gs, double* ocells,
+                    const SubDebug* dbg, int orient_only, cudaStream_t s);
 int gen_kc(int n, const YParams& yp);
 size_t gen_scratch_per_sub(int n, const YParams& yp);
 size_t gen_pf_smem(int n, const YParams& yp);
