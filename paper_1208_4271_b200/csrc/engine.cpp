@@ -148,7 +148,9 @@ struct TableSet {
     CK(cudaMemcpyAsync(cell_edge.ensure(std::max(c, 1)), edge.data(), c, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(cell_cmp.ensure(std::max(c, 1)), cmp.data(), c, cudaMemcpyHostToDevice, s));
     // exact c_s / c_t quotients for the general tier's span terms (device-built)
-    has_div = n_ <= 4096;
+    // Measured slower than IEEE DDIV in the span terms on B200 (the lookups
+    // are L2-latency-bound, the FP64 pipe is not busy); kept behind a switch.
+    has_div = n_ <= 4096 && std::getenv("MINE_B200_DIV_TABLE");
     if (has_div) {
       launch_build_div(static_cast<double*>(div.ensure(sizeof(double) * div_table_doubles(n_))), n_, s);
       CK(cudaGetLastError());

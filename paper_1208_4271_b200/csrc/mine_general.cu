@@ -30,8 +30,14 @@ namespace {
 
 constexpr int kPfThreads = 256;
 constexpr int kPfWarps = kPfThreads / 32;
-constexpr int kDpThreads = 256;
-constexpr int kMaxTile = 48;   // t-tile / s-chunk edge
+#ifndef KDP_THREADS
+#define KDP_THREADS 256
+#endif
+#ifndef KDP_TILE
+#define KDP_TILE 32
+#endif
+constexpr int kDpThreads = KDP_THREADS;
+constexpr int kMaxTile = KDP_TILE;  // t-tile / s-chunk edge
 constexpr int kCells = 8;      // accumulators per thread
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -337,7 +343,7 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 // F lives in a per-CTA HBM slot (L2-resident for typical sizes); each outer
 // s-chunk's rows are staged into shared memory with coalesced loads, and the
 // current t-tile's rows are kept in shared memory while its inner part runs.
-__global__ void __launch_bounds__(kDpThreads, 2) k_dp(VarSet vs, Tables tb, PairSpace ps,
+__global__ void __launch_bounds__(kDpThreads, 512 / kDpThreads) k_dp(VarSet vs, Tables tb, PairSpace ps,
                                                       long long base, long long nsub, YParams yp,
                                                       GenScratch gs, double* __restrict__ ocells,
                                                       SubDebug dbg, int has_dbg, int orient_only) {
@@ -645,7 +651,7 @@ int gen_dp_grid(int n, const YParams& yp) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t sm = gen_dp_smem(n, yp);
-  const int per = (int)std::max<size_t>(1, std::min<size_t>(2, (228 * 1024) / (sm + 1024)));
+  const int per = (int)std::max<size_t>(1, std::min<size_t>(512 / kDpThreads * 2, (228 * 1024) / (sm + 1024)));
   return sms * per;
 }
 

@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmine_b200.so")
+LIB_PATH = os.environ.get("MINE_B200_LIB", os.path.join(_PKG, "libmine_b200.so"))
 
 MIC_APPROX = 0
 MIC_E = 1
