@@ -408,7 +408,8 @@ __host__ __device__ inline MemoLayout memo_layout(int n) {
   L.offk = L.pln + n + 1;                     // (n + 2) ints
   L.gq = L.offk + (n + 3) / 2;                // (n + 1) ints: packed (g1, 2 g1 - g2) per c_s
   L.t3o = L.gq + (n + 2) / 2;                 // (n + 1)^2 ints: t3_index(c_s, a0, 0)
-  L.total = L.t3o + ((n + 1) * (n + 1) + 1) / 2;
+  L.std3 = L.t3o + ((n + 1) * (n + 1) + 1) / 2;  // 2 ints: standard 3-row totals (C0, C1)
+  L.total = L.std3 + 1;
   return L;
 }
 
@@ -417,6 +418,7 @@ struct MemoCtx {
   const int* offk;
   const int* gq;
   const int* t3o;
+  int std3[2];
   MemoLayout L;
   int n;
   uint32_t valid;
@@ -468,14 +470,50 @@ __global__ void k_build_memo(Tables tb, double* memo, int n) {
         memo[L.k2 + base + a0 * (ct - cs + 1) + b0] = __dsub_rn(-acc2, -accj);
       }
   }
-  // T3[cs][a0][a1] (c_t = n), W2[cs][u0] (c_t = n), E2, R1, PLn
+  // Row totals (C0, C1, C2) of the 3-row equipartition of n distinct values
+  // (partition.cpp:42-67 with unit runs): the totals of every y = 3 row map of
+  // a variable without ties.
+  int std3[3] = {-1, -1, -1};
+  {
+    double desired = (double)n / 3.0;
+    int curr = 1, in_row = 0;
+    for (int i = 0; i < n; ++i) {
+      if (in_row != 0 && fabs((double)(in_row + 1) - desired) >= fabs((double)in_row - desired)) {
+        if (curr <= 3) std3[curr - 1] = in_row;
+        ++curr;
+        in_row = 0;
+        desired = (double)(n - i) / (double)(3 - curr + 1);
+      }
+      ++in_row;
+    }
+    if (curr == 3) std3[2] = in_row;
+    else std3[0] = std3[1] = -1;
+  }
+  if (threadIdx.x == 0) {
+    int* sd = reinterpret_cast<int*>(memo + L.std3);
+    sd[0] = std3[0];
+    sd[1] = std3[1];
+  }
+  // T3F[cs][a0][a1] (c_t = n): the whole 3-row F(k,2) candidate for the
+  // standard totals -- E2[cs] - (-(((((p a0 + p a1) + p a2) + p b0) + p b1) + p b2)),
+  // the reference's sequence; W2[cs][u0] (c_t = n), E2, R1, PLn
   for (int cs = threadIdx.x; cs < n; cs += blockDim.x) {
+    double acc2 = PL(n, cs);
+    acc2 = __dadd_rn(acc2, PL(n, n - cs));
     for (int a0 = 0; a0 <= cs; ++a0)
       for (int a1 = 0; a0 + a1 <= cs; ++a1) {
-        double acc = PL(n, a0);
-        acc = __dadd_rn(acc, PL(n, a1));
-        acc = __dadd_rn(acc, PL(n, cs - a0 - a1));
-        memo[L.t3 + t3_index(cs, a0, a1)] = acc;
+        const int b0 = std3[0] - a0, b1 = std3[1] - a1, b2 = (n - cs) - b0 - b1;
+        double v = 0.0;
+        if (std3[0] >= 0 && b0 >= 0 && b1 >= 0 && b2 >= 0) {
+          double acc = PL(n, a0);
+          acc = __dadd_rn(acc, PL(n, a1));
+          acc = __dadd_rn(acc, PL(n, cs - a0 - a1));
+          acc = __dadd_rn(acc, PL(n, b0));
+          acc = __dadd_rn(acc, PL(n, b1));
+          acc = __dadd_rn(acc, PL(n, b2));
+          v = __dsub_rn(-acc2, -acc);
+        }
+        memo[L.t3 + t3_index(cs, a0, a1)] = v;
       }
     const int m = n - cs;
     for (int u0 = 0; u0 <= m; ++u0) {
@@ -572,12 +610,6 @@ __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, 
       f2k = dmax(f2k, kb[memo_G(n, cs) + a0 * (n - cs + 1) + (c0 - a0)]);
     }
   } else {
-    int cnt = 0;
-    for (uint32_t s = bnd; s; s &= s - 1, ++cnt) {
-      const int cs = __ffs(s) - 1;
-      const int a0 = __popc(m0 & ((1u << cs) - 1u));  // c_s < n <= 31
-      scr[cnt * sstride] = c.gq[cs] + (a0 << 16) - a0 * cs;
-    }
     const double* W2 = c.tab + c.L.w2;
     const double* R1 = c.tab + c.L.r1;
     int j = 0;
@@ -598,6 +630,9 @@ __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, 
           f2k = f2;
       }
       if (!ts) break;
+      // t becomes a split candidate s for the later t's: stage P_s / Q_s
+      const int a0 = __popc(m0 & ((1u << t) - 1u));  // t < n <= 31
+      scr[(j - 1) * sstride] = c.gq[t] + (a0 << 16) - a0 * t;
     }
   }
   i2 = dmax(0.0, __dadd_rn(hq, f2k));
@@ -613,25 +648,36 @@ __device__ double memo_y3_rows3(const MemoCtx& c, uint32_t m0, uint32_t m1, uint
   const uint32_t bnd = bits_partition(d, rsm, c.valid, n, k_hat, k);
   if (work) {
     subproblem_work(3, k, 2, work, false);
-    if (k >= 2) work[kCntGathers] += 5 * (k - 1);
+    if (k >= 2) work[kCntGathers] += (__popc(m0) == c.std3[0] && __popc(m1) == c.std3[1] ? 1 : 6) * (k - 1);
   }
   if (k < 2) return 0.0;
   const int c0 = __popc(m0), c1 = __popc(m1);
-  const double* T3 = c.tab + c.L.t3;
-  const double* E2 = c.tab + c.L.e2;
-  const double* P = c.tab + c.L.pln;
   double best = kLowest;
   const int* t3o = c.t3o;
-  for (uint32_t s = bnd; s; s &= s - 1) {
-    const int cs = __ffs(s) - 1;
-    const uint32_t pre = (1u << cs) - 1u;  // c_s < n <= 31
-    const int a0 = __popc(m0 & pre), a1 = __popc(m1 & pre);
-    const int b0 = c0 - a0, b1 = c1 - a1, b2 = (n - cs) - b0 - b1;
-    double acc = T3[t3o[cs * (n + 1) + a0] + a1];
-    acc = __dadd_rn(acc, P[b0]);
-    acc = __dadd_rn(acc, P[b1]);
-    acc = __dadd_rn(acc, P[b2]);
-    best = dmax(best, __dsub_rn(E2[cs], -acc));
+  if (c0 == c.std3[0] && c1 == c.std3[1]) {
+    // standard row totals (no ties in the row variable): one gather per candidate
+    const double* T3F = c.tab + c.L.t3;
+    for (uint32_t s = bnd; s; s &= s - 1) {
+      const int cs = __ffs(s) - 1;
+      const uint32_t pre = (1u << cs) - 1u;  // c_s < n <= 31
+      best = dmax(best, T3F[t3o[cs * (n + 1) + __popc(m0 & pre)] + __popc(m1 & pre)]);
+    }
+  } else {
+    const double* E2 = c.tab + c.L.e2;
+    const double* P = c.tab + c.L.pln;
+    for (uint32_t s = bnd; s; s &= s - 1) {
+      const int cs = __ffs(s) - 1;
+      const uint32_t pre = (1u << cs) - 1u;
+      const int a0 = __popc(m0 & pre), a1 = __popc(m1 & pre);
+      const int b0 = c0 - a0, b1 = c1 - a1, b2 = (n - cs) - b0 - b1;
+      double acc = P[a0];
+      acc = __dadd_rn(acc, P[a1]);
+      acc = __dadd_rn(acc, P[cs - a0 - a1]);
+      acc = __dadd_rn(acc, P[b0]);
+      acc = __dadd_rn(acc, P[b1]);
+      acc = __dadd_rn(acc, P[b2]);
+      best = dmax(best, __dsub_rn(E2[cs], -acc));
+    }
   }
   return dmax(0.0, __dadd_rn(hq, best));
 }
@@ -665,6 +711,8 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
   c.offk = reinterpret_cast<const int*>(msm + L.offk);
   c.gq = reinterpret_cast<const int*>(msm + L.gq);
   c.t3o = reinterpret_cast<const int*>(msm + L.t3o);
+  c.std3[0] = reinterpret_cast<const int*>(msm + L.std3)[0];
+  c.std3[1] = reinterpret_cast<const int*>(msm + L.std3)[1];
   c.L = L;
   c.n = n;
   c.valid = prefix(n);

@@ -31,7 +31,7 @@ struct VarSet {
 
 // Memo-tier table layout (offsets in doubles), see mine_kernels.cu.
 struct MemoLayout {
-  int n, k2, t3, w2, e2, r1, pln, offk, gq, t3o, total;
+  int n, k2, t3, w2, e2, r1, pln, offk, gq, t3o, std3, total;
 };
 
 // Host-built constant tables (glibc libm, the reference's own arithmetic).
