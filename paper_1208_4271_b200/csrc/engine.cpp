@@ -187,7 +187,8 @@ struct mine_b200_ctx {
   std::mutex mu;
   TableSet tables;
   DevBuf vals, perm, runid, runstart, nruns, q, yhat, hq, lw, rsmask;
-  DevBuf ocells, fscratch, stats, flag, idx, counters, memo, rec, gscr, gqueue, glists;
+  DevBuf ocells, fscratch, stats, flag, idx, counters, memo, memo_vals, memo_val, rec, gscr,
+      gqueue, glists;
   int memo_n = -1;
   std::vector<cudaEvent_t> events;
   long long launches = 0;
@@ -286,7 +287,9 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   if (memo && ctx->memo_n != n) {
     ctx->memo_n = -1;
     double* mt = static_cast<double*>(ctx->memo.ensure(sizeof(double) * memo_doubles(n)));
-    launch_build_memo(tb, mt, n, s);
+    double* mv = static_cast<double*>(ctx->memo_vals.ensure(sizeof(double) * memo_values(n)));
+    double* mr = static_cast<double*>(ctx->memo_val.ensure(sizeof(double) * memo_values(n)));
+    launch_build_memo(tb, mt, mv, mr, n, s);
     CK(cudaGetLastError());
     ctx->memo_n = n;
   }
@@ -428,7 +431,8 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
     pc.first = first + c0;
     pc.count = cn;
     if (memo) {
-      launch_memo_pairs(vs, tb, ctx->memo.as<double>(), pc, par->c, par->est, so, cells_dst, dcnt, s);
+      launch_memo_pairs(vs, tb, ctx->memo.as<double>(), ctx->memo_val.as<double>(), pc, par->c,
+                        par->est, so, cells_dst, dcnt, s);
       ++ctx->launches;
     } else if (tiny) {
       launch_tiny_pairs(vs, tb, pc, par->c, par->est, so, cells_dst, dcnt, s);

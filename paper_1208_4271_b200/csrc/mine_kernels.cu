@@ -381,14 +381,18 @@ __global__ void __launch_bounds__(128) k_tiny_pairs(VarSet vs, Tables tb, PairSp
 }
 
 // ---------------------------------------------------------------------------
-// Memo tier (n <= 25, B <= 7; the c1 shape).  With two rows every F(t,2)
+// Memo tier (n <= 24, B <= 7; the c1 shape).  With two rows every F(t,2)
 // candidate H(P) - H(P,Q) (mutual_info.cpp:51-52) is a function of (c_t, c_s,
 // a0, b0) only (a1 = c_s - a0, b1 = c_t - c_s - b0), and there are only
 // C(n+4,4)-ish such tuples.  k_build_memo evaluates every candidate ONCE with
 // the reference's exact operation sequence (sequential p*log(p) sums, then
-// (-acc2) - (-accj)), so a candidate becomes one shared-memory gather instead
-// of six, bit-identically.  Likewise the level-3 span term at t = k, and the
-// first three joint-entropy terms of the three-row case.
+// (-acc2) - (-accj)); likewise the whole three-row y = 3 candidate for the
+// standard row totals, and the level-3 span term at t = k.  k_rank_memo then
+// replaces each tabulated candidate by its rank among all tabulated values
+// (an order-preserving int32, equal values -> equal rank) and builds the
+// rank -> value table: the per-candidate max becomes a 4-byte gather and one
+// integer max, and the double is fetched once per t -- exactly the same
+// maximum, since the max rank is the rank of the max value.
 __host__ __device__ __forceinline__ int memo_G(int ct, int cs) {
   // entries of K2 before c_s within block c_t: sum_{u=2}^{cs} u (ct + 2 - u)
   return (ct + 2) * (cs * (cs + 1) / 2 - 1) - (cs * (cs + 1) * (2 * cs + 1) / 6 - 1);
@@ -399,25 +403,29 @@ __host__ __device__ inline MemoLayout memo_layout(int n) {
   int k2 = 0;
   for (int ct = 2; ct <= n; ++ct) k2 += memo_G(ct, ct);
   L.n = n;
-  L.k2 = 0;
-  L.t3 = k2;
-  L.w2 = L.t3 + n * (n + 1) * (n + 2) / 6;
+  L.k2cnt = k2;
+  L.t3cnt = n * (n + 1) * (n + 2) / 6;
+  // doubles
+  L.w2 = 0;
   L.e2 = L.w2 + n * (n + 1) - n * (n - 1) / 2;
   L.r1 = L.e2 + n + 1;
   L.pln = L.r1 + n + 1;
-  L.offk = L.pln + n + 1;                     // (n + 2) ints
-  L.gq = L.offk + (n + 3) / 2;                // (n + 1) ints: packed (g1, 2 g1 - g2) per c_s
-  L.t3o = L.gq + (n + 2) / 2;                 // (n + 1)^2 ints: t3_index(c_s, a0, 0)
-  L.std3 = L.t3o + ((n + 1) * (n + 1) + 1) / 2;  // 2 ints: standard 3-row totals (C0, C1)
-  L.total = L.std3 + 1;
+  L.ib = L.pln + n + 1;  // int region starts here (in doubles)
+  // ints, relative to the int region
+  L.k2r = 0;
+  L.t3r = L.k2r + L.k2cnt;
+  L.offk = L.t3r + L.t3cnt;     // (n + 2)
+  L.gq = L.offk + n + 2;        // (n + 1): packed (g1, 2 g1 - g2) per c_s
+  L.t3o = L.gq + n + 1;         // (n + 1)^2: t3_index(c_s, a0, 0)
+  L.std3 = L.t3o + (n + 1) * (n + 1);  // 2: standard 3-row totals (C0, C1)
+  L.total = L.ib + (L.std3 + 2 + 1) / 2;
   return L;
 }
 
 struct MemoCtx {
   const double* tab;
-  const int* offk;
-  const int* gq;
-  const int* t3o;
+  const int* ints;
+  const double* val;  // rank -> value (global, L1/L2-cached)
   int std3[2];
   MemoLayout L;
   int n;
@@ -432,10 +440,12 @@ __device__ __forceinline__ int w2_index(int n, int cs, int u0) {
 }
 
 // Table builder: one block, the same FP64 op sequence as tiny_cand2 / the
-// general tier (both bit-exact against the reference).
-__global__ void k_build_memo(Tables tb, double* memo, int n) {
+// general tier (both bit-exact against the reference).  Candidate values go
+// to vals[] (K2 first, then T3F) for ranking; the rest into the table image.
+__global__ void k_build_memo(Tables tb, double* memo, double* vals, int n) {
   const MemoLayout L = memo_layout(n);
-  int* offk = reinterpret_cast<int*>(memo + L.offk);
+  int* ints = reinterpret_cast<int*>(memo + L.ib);
+  int* offk = ints + L.offk;
   const double* pl = tb.pl;
   auto PL = [&](int m, int w) { return pl[tri(m) + w]; };
   if (threadIdx.x == 0) {
@@ -445,8 +455,8 @@ __global__ void k_build_memo(Tables tb, double* memo, int n) {
       if (ct >= 2 && ct <= n) off += memo_G(ct, ct);
     }
   }
-  int* gq = reinterpret_cast<int*>(memo + L.gq);
-  int* t3o = reinterpret_cast<int*>(memo + L.t3o);
+  int* gq = ints + L.gq;
+  int* t3o = ints + L.t3o;
   for (int cs = threadIdx.x; cs <= n; cs += blockDim.x) {
     const int g1 = cs * (cs + 1) / 2 - 1;
     const int g2 = cs * (cs + 1) * (2 * cs + 1) / 6 - 1;
@@ -467,7 +477,7 @@ __global__ void k_build_memo(Tables tb, double* memo, int n) {
         accj = __dadd_rn(accj, PL(ct, cs - a0));
         accj = __dadd_rn(accj, PL(ct, b0));
         accj = __dadd_rn(accj, PL(ct, ct - cs - b0));
-        memo[L.k2 + base + a0 * (ct - cs + 1) + b0] = __dsub_rn(-acc2, -accj);
+        vals[base + a0 * (ct - cs + 1) + b0] = __dsub_rn(-acc2, -accj);
       }
   }
   // Row totals (C0, C1, C2) of the 3-row equipartition of n distinct values
@@ -490,9 +500,8 @@ __global__ void k_build_memo(Tables tb, double* memo, int n) {
     else std3[0] = std3[1] = -1;
   }
   if (threadIdx.x == 0) {
-    int* sd = reinterpret_cast<int*>(memo + L.std3);
-    sd[0] = std3[0];
-    sd[1] = std3[1];
+    ints[L.std3] = std3[0];
+    ints[L.std3 + 1] = std3[1];
   }
   // T3F[cs][a0][a1] (c_t = n): the whole 3-row F(k,2) candidate for the
   // standard totals -- E2[cs] - (-(((((p a0 + p a1) + p a2) + p b0) + p b1) + p b2)),
@@ -503,7 +512,7 @@ __global__ void k_build_memo(Tables tb, double* memo, int n) {
     for (int a0 = 0; a0 <= cs; ++a0)
       for (int a1 = 0; a0 + a1 <= cs; ++a1) {
         const int b0 = std3[0] - a0, b1 = std3[1] - a1, b2 = (n - cs) - b0 - b1;
-        double v = 0.0;
+        double v = 0.0;  // unreachable tuple
         if (std3[0] >= 0 && b0 >= 0 && b1 >= 0 && b2 >= 0) {
           double acc = PL(n, a0);
           acc = __dadd_rn(acc, PL(n, a1));
@@ -513,7 +522,7 @@ __global__ void k_build_memo(Tables tb, double* memo, int n) {
           acc = __dadd_rn(acc, PL(n, b2));
           v = __dsub_rn(-acc2, -acc);
         }
-        memo[L.t3 + t3_index(cs, a0, a1)] = v;
+        vals[L.k2cnt + t3_index(cs, a0, a1)] = v;
       }
     const int m = n - cs;
     for (int u0 = 0; u0 <= m; ++u0) {
@@ -529,6 +538,29 @@ __global__ void k_build_memo(Tables tb, double* memo, int n) {
     memo[L.e2 + i] = -acc2;
     memo[L.r1 + i] = __ddiv_rn((double)i, (double)n);
     memo[L.pln + i] = PL(n, i);
+  }
+}
+
+// rank[i] = #{j : vals[j] < vals[i]} (order-preserving; equal values share a
+// rank), written into the table image; val[rank] = vals[i].
+__global__ void k_rank_memo(double* memo, const double* __restrict__ vals, double* val, int n) {
+  __shared__ double chunk[2048];
+  const MemoLayout L = memo_layout(n);
+  const int nv = L.k2cnt + L.t3cnt;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const double v = i < nv ? vals[i] : 0.0;
+  int rank = 0;
+  for (int j0 = 0; j0 < nv; j0 += 2048) {
+    const int m = min(2048, nv - j0);
+    __syncthreads();
+    for (int j = threadIdx.x; j < m; j += blockDim.x) chunk[j] = vals[j0 + j];
+    __syncthreads();
+    for (int j = 0; j < m; ++j) rank += chunk[j] < v;
+  }
+  if (i < nv) {
+    int* ints = reinterpret_cast<int*>(memo + L.ib);
+    ints[i < L.k2cnt ? L.k2r + i : L.t3r + (i - L.k2cnt)] = rank;
+    val[rank] = v;
   }
 }
 
@@ -581,12 +613,11 @@ __device__ __forceinline__ uint32_t byte_of(const uint32_t* w, int s) {
 //   OFFK(c_t) + G(c_t, c_s) + a0 (c_t - c_s + 1) + b0
 //     = [OFFK(c_t) + B0(t)] + c_t * P_s + Q_s,
 //   P_s = g1(c_s) + a0(s),  Q_s = 2 g1(c_s) - g2(c_s) - a0(s) c_s,
-// so P_s / Q_s are computed once per boundary into this thread's column of
-// shared scratch (bank = lane: conflict-free) and the inner loop is one
-// scratch read, one IMAD and one table gather per candidate.
+// so P_s / Q_s are staged once per boundary in this thread's scratch row
+// (odd stride: conflict-free) and the inner loop is one scratch read, one
+// IMAD, one 4-byte rank gather and one integer max per candidate.
 __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, int k_hat,
-                        double hq, double& i2, double& i3, unsigned long long* work,
-                        int* scr, int sstride) {
+                        double hq, double& i2, double& i3, unsigned long long* work, int* scr) {
   const int n = c.n;
   const uint32_t d = (m0 ^ (m0 << 1)) & c.valid & ~1u;
   int k;
@@ -600,30 +631,36 @@ __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, 
     return;
   }
   const int c0 = __popc(m0);
-  const double* K2 = c.tab + c.L.k2;
-  double f2k = kLowest, best3 = kLowest;
+  const int* K2R = c.ints + c.L.k2r;
+  const int* offk = c.ints + c.L.offk;
+  double f2k, best3 = kLowest;
   if (x_max <= 2) {
-    const double* kb = K2 + c.offk[n];
+    const int* kb = K2R + offk[n];
+    int r = -1;
     for (uint32_t s = bnd; s; s &= s - 1) {
       const int cs = __ffs(s) - 1;
       const int a0 = __popc(m0 & prefix(cs));
-      f2k = dmax(f2k, kb[memo_G(n, cs) + a0 * (n - cs + 1) + (c0 - a0)]);
+      r = max(r, kb[memo_G(n, cs) + a0 * (n - cs + 1) + (c0 - a0)]);
     }
+    f2k = __ldg(c.val + r);
   } else {
     const double* W2 = c.tab + c.L.w2;
     const double* R1 = c.tab + c.L.r1;
+    const int* gq = c.ints + c.L.gq;
+    f2k = kLowest;
     int j = 0;
     for (uint32_t ts = bnd;; ts &= ts - 1) {
       const int t = ts ? __ffs(ts) - 1 : n;
       ++j;
+      const int b0t = __popc(m0 & prefix(t));
       if (j >= 2) {
-        const int b0t = __popc(m0 & prefix(t));
-        const double* kb = K2 + (c.offk[t] + b0t - 8192);
-        double f2 = kLowest;
+        const int* kb = K2R + (offk[t] + b0t - 8192);
+        int r = -1;
         for (int i = 0; i < j - 1; ++i) {
-          const int v = scr[i * sstride];
-          f2 = dmax(f2, kb[t * (v >> 16) + (v & 0xffff)]);
+          const int v = scr[i];
+          r = max(r, kb[t * (v >> 16) + (v & 0xffff)]);
         }
+        const double f2 = __ldg(c.val + r);
         if (t < n)
           best3 = dmax(best3, __dsub_rn(__dmul_rn(R1[t], f2), W2[w2_index(n, t, c0 - b0t)]));
         else
@@ -631,8 +668,7 @@ __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, 
       }
       if (!ts) break;
       // t becomes a split candidate s for the later t's: stage P_s / Q_s
-      const int a0 = __popc(m0 & ((1u << t) - 1u));  // t < n <= 31
-      scr[(j - 1) * sstride] = c.gq[t] + (a0 << 16) - a0 * t;
+      scr[j - 1] = gq[t] + (b0t << 16) - b0t * t;
     }
   }
   i2 = dmax(0.0, __dadd_rn(hq, f2k));
@@ -646,22 +682,25 @@ __device__ double memo_y3_rows3(const MemoCtx& c, uint32_t m0, uint32_t m1, uint
   const uint32_t d = ((m0 ^ (m0 << 1)) | (m1 ^ (m1 << 1))) & c.valid & ~1u;
   int k;
   const uint32_t bnd = bits_partition(d, rsm, c.valid, n, k_hat, k);
+  const int c0 = __popc(m0), c1 = __popc(m1);
+  const bool standard = c0 == c.std3[0] && c1 == c.std3[1];
   if (work) {
     subproblem_work(3, k, 2, work, false);
-    if (k >= 2) work[kCntGathers] += (__popc(m0) == c.std3[0] && __popc(m1) == c.std3[1] ? 1 : 6) * (k - 1);
+    if (k >= 2) work[kCntGathers] += (standard ? 1 : 7) * (k - 1);
   }
   if (k < 2) return 0.0;
-  const int c0 = __popc(m0), c1 = __popc(m1);
   double best = kLowest;
-  const int* t3o = c.t3o;
-  if (c0 == c.std3[0] && c1 == c.std3[1]) {
-    // standard row totals (no ties in the row variable): one gather per candidate
-    const double* T3F = c.tab + c.L.t3;
+  const int* t3o = c.ints + c.L.t3o;
+  if (standard) {
+    // standard row totals (no ties in the row variable): one rank gather per candidate
+    const int* T3R = c.ints + c.L.t3r;
+    int r = -1;
     for (uint32_t s = bnd; s; s &= s - 1) {
       const int cs = __ffs(s) - 1;
       const uint32_t pre = (1u << cs) - 1u;  // c_s < n <= 31
-      best = dmax(best, T3F[t3o[cs * (n + 1) + __popc(m0 & pre)] + __popc(m1 & pre)]);
+      r = max(r, T3R[t3o[cs * (n + 1) + __popc(m0 & pre)] + __popc(m1 & pre)]);
     }
+    best = __ldg(c.val + r);
   } else {
     const double* E2 = c.tab + c.L.e2;
     const double* P = c.tab + c.L.pln;
@@ -684,8 +723,11 @@ __device__ double memo_y3_rows3(const MemoCtx& c, uint32_t m0, uint32_t m1, uint
 
 constexpr int kMemoMaxThreads = 768;
 
+__host__ __device__ inline int memo_scr_stride(int n) { return n | 1; }
+
 __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Tables tb,
                                                                const double* __restrict__ memo,
+                                                               const double* __restrict__ memo_val,
                                                                PairSpace ps, double cpar, int est,
                                                                StatsOut out, double* ocells,
                                                                unsigned long long* counters) {
@@ -703,16 +745,14 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
     lg2[threadIdx.x] = threadIdx.x <= B ? tb.log2i[threadIdx.x] : 0.0;
   }
   __syncthreads();
-  // per-thread scratch column after the tables: n ints, stride blockDim.x
-  int* scr = reinterpret_cast<int*>(msm + ((L.total + 1) & ~1)) + threadIdx.x;
-  const int sstride = blockDim.x;
+  // this thread's scratch row after the tables (odd stride: bank = lane)
+  int* scr = reinterpret_cast<int*>(msm + ((L.total + 1) & ~1)) + threadIdx.x * memo_scr_stride(n);
   MemoCtx c;
   c.tab = msm;
-  c.offk = reinterpret_cast<const int*>(msm + L.offk);
-  c.gq = reinterpret_cast<const int*>(msm + L.gq);
-  c.t3o = reinterpret_cast<const int*>(msm + L.t3o);
-  c.std3[0] = reinterpret_cast<const int*>(msm + L.std3)[0];
-  c.std3[1] = reinterpret_cast<const int*>(msm + L.std3)[1];
+  c.ints = reinterpret_cast<const int*>(msm + L.ib);
+  c.val = memo_val;
+  c.std3[0] = c.ints[L.std3];
+  c.std3[1] = c.ints[L.std3 + 1];
   c.L = L;
   c.n = n;
   c.valid = prefix(n);
@@ -758,7 +798,7 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
       const double hq3 = __hiloint2double(hy.w, hy.z);
       if (yh2 >= 2) {
         double i2, i3;
-        memo_y2(c, m2, rsm, x2, kh2, hq2, i2, i3, wk, scr, sstride);
+        memo_y2(c, m2, rsm, x2, kh2, hq2, i2, i3, wk, scr);
         o[orient][0] = norm_cell(i2, lg[2], lg[yh2]);
         if (x2 >= 3) o[orient][orient ? 2 : 1] = norm_cell(i3, lg[3], lg[yh2]);
       }
@@ -767,7 +807,7 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
         if (yh3 == 3)
           i2 = memo_y3_rows3(c, m3a, m3b, rsm, kh3, hq3, wk);
         else
-          memo_y2(c, m3a, rsm, 2, kh3, hq3, i2, dummy, wk, scr, sstride);
+          memo_y2(c, m3a, rsm, 2, kh3, hq3, i2, dummy, wk, scr);
         o[orient][orient ? 1 : 2] = norm_cell(i2, lg[2], lg[yh3]);
       }
     }
@@ -883,36 +923,48 @@ void launch_tiny_pairs(const VarSet& vs, const Tables& tb, const PairSpace& ps, 
 }
 
 size_t memo_doubles(int n) { return (size_t)memo_layout(n).total; }
-
-bool memo_fits(int n, int B) {
-  // tables + at least 8 warps of n-int scratch columns in 226 KB
-  return n >= 2 && n <= 32 && B <= 7 &&
-         (memo_doubles(n) + 1) * sizeof(double) + sizeof(int) * (size_t)n * 256 <= 226 * 1024;
+size_t memo_values(int n) {
+  const MemoLayout L = memo_layout(n);
+  return (size_t)L.k2cnt + L.t3cnt;
 }
 
-void launch_build_memo(const Tables& tb, double* memo, int n, cudaStream_t s) {
-  k_build_memo<<<1, 256, 0, s>>>(tb, memo, n);
+static size_t memo_tab_bytes(int n) { return ((memo_doubles(n) + 1) & ~size_t(1)) * sizeof(double); }
+
+bool memo_fits(int n, int B) {
+  // tables + at least 8 warps of scratch rows in 226 KB
+  return n >= 2 && n <= 32 && B <= 7 &&
+         memo_tab_bytes(n) + sizeof(int) * (size_t)memo_scr_stride(n) * 256 <= 226 * 1024;
+}
+
+void launch_build_memo(const Tables& tb, double* memo, double* vals, double* val, int n,
+                       cudaStream_t s) {
+  k_build_memo<<<1, 256, 0, s>>>(tb, memo, vals, n);
+  const int nv = (int)memo_values(n);
+  k_rank_memo<<<(nv + 255) / 256, 256, 0, s>>>(memo, vals, val, n);
 }
 
 void launch_pack_memo(const VarSet& vs, cudaStream_t s) {
   k_pack_memo<<<(vs.V + 127) / 128, 128, 0, s>>>(vs);
 }
 
-void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo, const PairSpace& ps,
-                       double c, int est, StatsOut out, double* o_cells,
-                       unsigned long long* counters, cudaStream_t s) {
+void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
+                       const double* memo_val, const PairSpace& ps, double c, int est,
+                       StatsOut out, double* o_cells, unsigned long long* counters,
+                       cudaStream_t s) {
   if (ps.count <= 0) return;
-  const size_t tab = ((memo_doubles(vs.n) + 1) & ~size_t(1)) * sizeof(double);
+  const size_t tab = memo_tab_bytes(vs.n);
   const size_t budget = 226 * 1024 - tab;
-  int threads = (int)std::min<size_t>(kMemoMaxThreads, budget / (sizeof(int) * vs.n)) / 32 * 32;
+  const size_t row = sizeof(int) * (size_t)memo_scr_stride(vs.n);
+  int threads = (int)std::min<size_t>(kMemoMaxThreads, budget / row) / 32 * 32;
   threads = std::max(threads, 32);
-  const size_t sm = tab + sizeof(int) * (size_t)vs.n * threads;
+  const size_t sm = tab + row * threads;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long need = (ps.count + threads - 1) / threads;
   const unsigned blocks = (unsigned)std::min<long long>(sms, need);
-  k_memo_pairs<<<blocks, threads, sm, s>>>(vs, tb, memo, ps, c, est, out, o_cells, counters);
+  k_memo_pairs<<<blocks, threads, sm, s>>>(vs, tb, memo, memo_val, ps, c, est, out, o_cells,
+                                           counters);
 }
 
 void launch_reduce(const Tables& tb, long long npairs, const double* ocells, int est, StatsOut out,

@@ -31,7 +31,7 @@ struct VarSet {
 
 // Memo-tier table layout (offsets in doubles), see mine_kernels.cu.
 struct MemoLayout {
-  int n, k2, t3, w2, e2, r1, pln, offk, gq, t3o, std3, total;
+  int n, k2cnt, t3cnt, w2, e2, r1, pln, ib, k2r, t3r, offk, gq, t3o, std3, total;
 };
 
 // Host-built constant tables (glibc libm, the reference's own arithmetic).
@@ -112,12 +112,15 @@ void launch_tiny_pairs(const VarSet& vs, const Tables& tb, const PairSpace& ps, 
 
 // Memo tier (n <= 25, B <= 7): every F(t,2) candidate precomputed per n.
 size_t memo_doubles(int n);
+size_t memo_values(int n);
 bool memo_fits(int n, int B);
-void launch_build_memo(const Tables& tb, double* memo, int n, cudaStream_t s);
+void launch_build_memo(const Tables& tb, double* memo, double* vals, double* val, int n,
+                       cudaStream_t s);
 void launch_pack_memo(const VarSet& vs, cudaStream_t s);
-void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo, const PairSpace& ps,
-                       double c, int est, StatsOut out, double* o_cells,
-                       unsigned long long* counters, cudaStream_t s);
+void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
+                       const double* memo_val, const PairSpace& ps, double c, int est,
+                       StatsOut out, double* o_cells, unsigned long long* counters,
+                       cudaStream_t s);
 
 // General tier (mine_general.cu): k_part_f2 + persistent tiled k_dp per y.
 struct GenScratch {
