@@ -120,12 +120,12 @@ def probe_peaks(device: int):
     import ctypes
     from paper_1208_4271_b200 import _build
     L = ctypes.CDLL(_build.PROBES)
-    L.mine_b200_probe.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double),
-                                  ctypes.POINTER(ctypes.c_double)]
-    a, b = ctypes.c_double(0), ctypes.c_double(0)
-    if L.mine_b200_probe(device, ctypes.byref(a), ctypes.byref(b)) != 0:
-        return None, None
-    return a.value, b.value
+    D = ctypes.POINTER(ctypes.c_double)
+    L.mine_b200_probe.argtypes = [ctypes.c_int, D, D, D]
+    a, b, c = ctypes.c_double(0), ctypes.c_double(0), ctypes.c_double(0)
+    if L.mine_b200_probe(device, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)) != 0:
+        return None, None, None
+    return a.value, b.value, c.value
 
 
 def cpu_reference(w, p, budget_s: float, cores: int):
@@ -267,10 +267,14 @@ def run_ours(args, world, rank, local):
     same = bool(np.array_equal(hout["mic"].view(np.int64), outs["mic"].cpu().numpy().view(np.int64)))
 
     if rank == 0:
-        dadd, lds = probe_peaks(local)
+        dadd, lds, lds2 = probe_peaks(local)
         kern_s = statistics.mean(kern_ms) / 1e3
-        gathers = work["gathers"]
+        g8, g2 = work["gathers"], work["rank_gathers"]
+        gathers = g8 + g2
         achieved = gathers / kern_s / 1e9
+        # mixed-width peak: the rate at which the LSU would serve this exact
+        # mix of 8-byte and 2-byte gathers (time-weighted harmonic mean)
+        lds = gathers / (g8 / lds + g2 / lds2) if lds and lds2 and gathers else None
         traffic = None
         try:
             t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))["k_memo_pairs"]
@@ -283,11 +287,16 @@ def run_ours(args, world, rank, local):
                 "traffic_source": "profiles/ncu_traffic.json (dram read+write bytes per launch, ncu)",
                 "kernel": "k_memo_pairs (the pair-scoring launch of a step)",
                 "per_launch_work": {k: int(v) * world for k, v in work.items()},
-                "work_unit": "8-byte shared-memory table gathers the memo-tier algorithm needs "
-                             "(1 per F(t,2) candidate, 2 per level-3 span term, 5 per 3-row "
-                             "candidate), counted by the kernel; DESIGN.md 'Roofline'",
-                "peak_source": "measured live: probes.cu k_lds (random 8 B gathers from a "
-                               "shared table, 8 streams/thread, all SMs)",
+                "work_unit": "shared-memory table gathers the memo-tier algorithm needs "
+                             "(one 2 B dense candidate rank per F(t,2) candidate, 2 x 8 B per "
+                             "level-3 span term, 4 B row offset + 2 B rank per standard 3-row "
+                             "candidate, 7 x 8 B "
+                             "per other 3-row candidate), counted by the kernel; DESIGN.md "
+                             "'Roofline'",
+                "gathers_8b": int(g8) * world, "gathers_rank": int(g2) * world,
+                "peak_source": "measured live: probes.cu k_lds (random 8 B gathers, 561-entry "
+                               "table) and k_lds2 (random 2 B gathers, 16K-entry table), 8 "
+                               "streams/thread, all SMs; peak = time-weighted mix of the two",
                 "kernel_ms": statistics.mean(kern_ms),
                 "secondary": {"bound": "fp64", "achieved": work["fp64_ops"] / kern_s / 1e12,
                               "peak": dadd / 1e12 if dadd else None, "unit": "TFLOP/s",

@@ -109,15 +109,16 @@ typedef struct mine_b200_opts {
   /* Measurement hooks (bench / profiling), all optional:
    *   counters: host array of MINE_B200_NCOUNTERS realised-work totals
    *             (the reference arithmetic's FP64 ops and p*log(p) lookups, DP
-   *             candidates, span entries, subproblems; then the table gathers
-   *             the executing tier needs), accumulated by the kernels;
+   *             candidates, span entries, subproblems; then the 8-byte and
+   *             rank (2-byte) table gathers the executing tier needs), accumulated
+   *             by the kernels;
    *   ev_begin / ev_end: cudaEvent_t recorded on the stream around the
    *             pair-scoring kernels (the dominant kernels of a call). */
   unsigned long long* counters;
   void* ev_begin;
   void* ev_end;
 } mine_b200_opts;
-#define MINE_B200_NCOUNTERS 6
+#define MINE_B200_NCOUNTERS 7
 
 /* ---- engine API ---------------------------------------------------------- */
 const char* mine_b200_last_error(void);

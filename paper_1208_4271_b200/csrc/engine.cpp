@@ -287,10 +287,11 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   if (memo && ctx->memo_n != n) {
     ctx->memo_n = -1;
     double* mt = static_cast<double*>(ctx->memo.ensure(sizeof(double) * memo_doubles(n)));
-    double* mv = static_cast<double*>(ctx->memo_vals.ensure(sizeof(double) * memo_values(n)));
+    void* mw = ctx->memo_vals.ensure(memo_work_bytes(n));
     double* mr = static_cast<double*>(ctx->memo_val.ensure(sizeof(double) * memo_values(n)));
-    launch_build_memo(tb, mt, mv, mr, n, s);
+    const int nval = launch_build_memo(tb, mt, mw, mr, n, s);
     CK(cudaGetLastError());
+    if (nval <= 0 || nval > 65535) throw Failure("mine_b200: memo table build failed");
     ctx->memo_n = n;
   }
   const int ncell = tb.ncell;

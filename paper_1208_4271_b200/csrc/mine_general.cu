@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kPfThreads) k_part_f2(VarSet vs, Tables tb, Pa
 
   const int l_max = min(x_max, k);
   if (counters && tid == 0) {
-    unsigned long long w[kNumCounters] = {0, 0, 0, 0, 0, 0};
+    unsigned long long w[kNumCounters] = {};
     subproblem_work(rows, k, x_max, w);
     for (int i = 0; i < kNumCounters; ++i)
       if (w[i]) atomicAdd(counters + i, w[i]);

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "device_common.cuh"
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(128) k_tiny_pairs(VarSet vs, Tables tb, PairSp
   }
   __syncthreads();
   const long long wl = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  unsigned long long work[kNumCounters] = {0, 0, 0, 0, 0, 0};
+  unsigned long long work[kNumCounters] = {};
   unsigned long long* wk = counters ? work : nullptr;
   if (wl >= ps.count) {
     if (counters) flush_work(work, counters);
@@ -387,11 +388,12 @@ __global__ void __launch_bounds__(128) k_tiny_pairs(VarSet vs, Tables tb, PairSp
 // C(n+4,4)-ish such tuples.  k_build_memo evaluates every candidate ONCE with
 // the reference's exact operation sequence (sequential p*log(p) sums, then
 // (-acc2) - (-accj)); likewise the whole three-row y = 3 candidate for the
-// standard row totals, and the level-3 span term at t = k.  k_rank_memo then
-// replaces each tabulated candidate by its rank among all tabulated values
-// (an order-preserving int32, equal values -> equal rank) and builds the
-// rank -> value table: the per-candidate max becomes a 4-byte gather and one
-// integer max, and the double is fetched once per t -- exactly the same
+// standard row totals, and the level-3 span term at t = k.  k_rank_memo /
+// k_dense_memo then replace each tabulated candidate by its dense rank (the
+// number of DISTINCT smaller tabulated values: order-preserving, equal values
+// -> equal rank, ~3k distinct values for n = 23, so a uint16) and build the
+// rank -> value table val[]: the per-candidate max becomes a 2-byte gather and
+// one integer max, and the double is fetched once per t -- exactly the same
 // maximum, since the max rank is the rank of the max value.
 __host__ __device__ __forceinline__ int memo_G(int ct, int cs) {
   // entries of K2 before c_s within block c_t: sum_{u=2}^{cs} u (ct + 2 - u)
@@ -410,21 +412,25 @@ __host__ __device__ inline MemoLayout memo_layout(int n) {
   L.e2 = L.w2 + n * (n + 1) - n * (n - 1) / 2;
   L.r1 = L.e2 + n + 1;
   L.pln = L.r1 + n + 1;
-  L.ib = L.pln + n + 1;  // int region starts here (in doubles)
+  L.ib = (L.pln + n + 2) & ~1;  // int region starts here (in doubles, 16-byte aligned)
   // ints, relative to the int region
+  L.offk = 0;                    // (n + 2)
+  // (n + 1) int4 per position t: {OFFK(t), g1(t), 2 g1(t) - g2(t), W2 row of t}, 16-byte aligned
+  L.gq = (L.offk + n + 2 + 3) & ~3;
+  L.t3o = L.gq + 4 * (n + 1);    // (n + 1)^2: t3_index(c_s, a0, 0)
+  L.std3 = L.t3o + (n + 1) * (n + 1);  // 2: standard 3-row totals (C0, C1)
+  L.hb = L.std3 + 2;             // uint16 region, relative to the int region
+  // uint16 dense candidate ranks, relative to the uint16 region
   L.k2r = 0;
   L.t3r = L.k2r + L.k2cnt;
-  L.offk = L.t3r + L.t3cnt;     // (n + 2)
-  L.gq = L.offk + n + 2;        // (n + 1): packed (g1, 2 g1 - g2) per c_s
-  L.t3o = L.gq + n + 1;         // (n + 1)^2: t3_index(c_s, a0, 0)
-  L.std3 = L.t3o + (n + 1) * (n + 1);  // 2: standard 3-row totals (C0, C1)
-  L.total = L.ib + (L.std3 + 2 + 1) / 2;
+  L.total = L.ib + (2 * L.hb + L.t3r + L.t3cnt + 3) / 4;
   return L;
 }
 
 struct MemoCtx {
   const double* tab;
   const int* ints;
+  const uint16_t* ranks;
   const double* val;  // rank -> value (global, L1/L2-cached)
   int std3[2];
   MemoLayout L;
@@ -444,6 +450,10 @@ __device__ __forceinline__ int w2_index(int n, int cs, int u0) {
 // to vals[] (K2 first, then T3F) for ranking; the rest into the table image.
 __global__ void k_build_memo(Tables tb, double* memo, double* vals, int n) {
   const MemoLayout L = memo_layout(n);
+  {  // zero the image (padding included) so every byte is defined
+    for (int i = threadIdx.x; i < L.total; i += blockDim.x) memo[i] = 0.0;
+    __syncthreads();
+  }
   int* ints = reinterpret_cast<int*>(memo + L.ib);
   int* offk = ints + L.offk;
   const double* pl = tb.pl;
@@ -455,12 +465,14 @@ __global__ void k_build_memo(Tables tb, double* memo, double* vals, int n) {
       if (ct >= 2 && ct <= n) off += memo_G(ct, ct);
     }
   }
-  int* gq = ints + L.gq;
+  int4* gq = reinterpret_cast<int4*>(ints + L.gq);
   int* t3o = ints + L.t3o;
   for (int cs = threadIdx.x; cs <= n; cs += blockDim.x) {
     const int g1 = cs * (cs + 1) / 2 - 1;
     const int g2 = cs * (cs + 1) * (2 * cs + 1) / 6 - 1;
-    gq[cs] = (g1 << 16) + (2 * g1 - g2 + 8192);
+    int off = 0;
+    for (int ct = 2; ct < cs; ++ct) off += memo_G(ct, ct);
+    gq[cs] = make_int4(off, g1, 2 * g1 - g2, cs < n ? w2_index(n, cs, 0) : 0);
     for (int a0 = 0; a0 <= n; ++a0) t3o[cs * (n + 1) + a0] = a0 <= cs ? t3_index(cs, a0, 0) : 0;
   }
   // K2[ct][cs][a0][b0]
@@ -541,12 +553,27 @@ __global__ void k_build_memo(Tables tb, double* memo, double* vals, int n) {
   }
 }
 
-// rank[i] = #{j : vals[j] < vals[i]} (order-preserving; equal values share a
-// rank), written into the table image; val[rank] = vals[i].
-__global__ void k_rank_memo(double* memo, const double* __restrict__ vals, double* val, int n) {
-  __shared__ double chunk[2048];
+// Build scratch: candidate values (K2 then T3F), sparse ranks, occupancy flags.
+struct MemoWork {
+  double* vals;
+  int* rk;
+  int* flag;
+  int* nval;
+};
+__host__ __device__ inline MemoWork memo_work(void* base, int n) {
   const MemoLayout L = memo_layout(n);
   const int nv = L.k2cnt + L.t3cnt;
+  MemoWork w;
+  w.vals = static_cast<double*>(base);
+  w.rk = reinterpret_cast<int*>(w.vals + nv);
+  w.flag = w.rk + nv;
+  w.nval = w.flag + nv;
+  return w;
+}
+
+// rk[i] = #{j : vals[j] < vals[i]} (order-preserving, equal values share it)
+__global__ void k_rank_memo(const double* __restrict__ vals, int* rk, int* flag, int nv) {
+  __shared__ double chunk[2048];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const double v = i < nv ? vals[i] : 0.0;
   int rank = 0;
@@ -558,9 +585,43 @@ __global__ void k_rank_memo(double* memo, const double* __restrict__ vals, doubl
     for (int j = 0; j < m; ++j) rank += chunk[j] < v;
   }
   if (i < nv) {
-    int* ints = reinterpret_cast<int*>(memo + L.ib);
-    ints[i < L.k2cnt ? L.k2r + i : L.t3r + (i - L.k2cnt)] = rank;
-    val[rank] = v;
+    rk[i] = rank;
+    flag[rank] = 1;
+  }
+}
+
+// Dense ranks (one block): d(rank) = #occupied sparse ranks below it, so the
+// rank of a candidate is the number of DISTINCT smaller values -- a uint16 in
+// the table image, and val[d] the value (a few thousand entries).
+__global__ void __launch_bounds__(1024) k_dense_memo(double* memo, MemoWork w, double* val, int n) {
+  const MemoLayout L = memo_layout(n);
+  const int nv = L.k2cnt + L.t3cnt;
+  __shared__ int part[1024];
+  const int per = (nv + blockDim.x - 1) / blockDim.x;
+  const int lo = min(nv, (int)threadIdx.x * per), hi = min(nv, lo + per);
+  int sum = 0;
+  for (int j = lo; j < hi; ++j) sum += w.flag[j];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+    const int add = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
+    __syncthreads();
+    part[threadIdx.x] += add;
+    __syncthreads();
+  }
+  int run = part[threadIdx.x] - sum;  // exclusive prefix
+  for (int j = lo; j < hi; ++j) {
+    const int f = w.flag[j];
+    w.flag[j] = run;  // flag -> dense index of sparse rank j
+    run += f;
+  }
+  if (threadIdx.x == blockDim.x - 1) *w.nval = part[threadIdx.x];
+  __syncthreads();
+  uint16_t* ranks = reinterpret_cast<uint16_t*>(reinterpret_cast<int*>(memo + L.ib) + L.hb);
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    const int d = w.flag[w.rk[i]];
+    ranks[i < L.k2cnt ? L.k2r + i : L.t3r + (i - L.k2cnt)] = (uint16_t)d;
+    val[d] = w.vals[i];
   }
 }
 
@@ -604,6 +665,28 @@ __global__ void k_pack_memo(VarSet vs) {
   }
 }
 
+// 2-byte shared load at a 32-bit shared-window byte address (lets the
+// candidate-rank gather fold its base into one LEA).
+__device__ __forceinline__ int lds_u16(uint32_t addr) {  // read-only table
+  int v;
+  asm("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ int4 lds_v4(uint32_t addr) {  // read-only table
+  int4 v;
+  asm("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+// per-thread scratch: volatile so the compiler keeps them in program order
+__device__ __forceinline__ int2 lds_v2(uint32_t addr) {
+  int2 v;
+  asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts_v2(uint32_t addr, int x, int y) {
+  asm volatile("st.shared.v2.s32 [%0], {%1, %2};" ::"r"(addr), "r"(x), "r"(y));
+}
+
 __device__ __forceinline__ uint32_t byte_of(const uint32_t* w, int s) {
   return (w[s >> 2] >> ((s & 3) * 8)) & 0xffu;
 }
@@ -613,29 +696,32 @@ __device__ __forceinline__ uint32_t byte_of(const uint32_t* w, int s) {
 //   OFFK(c_t) + G(c_t, c_s) + a0 (c_t - c_s + 1) + b0
 //     = [OFFK(c_t) + B0(t)] + c_t * P_s + Q_s,
 //   P_s = g1(c_s) + a0(s),  Q_s = 2 g1(c_s) - g2(c_s) - a0(s) c_s,
-// so P_s / Q_s are staged once per boundary in this thread's scratch row
-// (odd stride: conflict-free) and the inner loop is one scratch read, one
-// IMAD, one 4-byte rank gather and one integer max per candidate.
+// so (P_s, Q_s) are staged once per boundary in this thread's scratch row
+// (int2, odd stride: conflict-free) and the inner loop is one 8-byte scratch
+// read, one IMAD, one 2-byte rank gather and one integer max per candidate.
 __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, int k_hat,
-                        double hq, double& i2, double& i3, unsigned long long* work, int* scr) {
+                        double hq, double& i2, double& i3, unsigned long long* work, int2* scr) {
   const int n = c.n;
   const uint32_t d = (m0 ^ (m0 << 1)) & c.valid & ~1u;
   int k;
   const uint32_t bnd = bits_partition(d, rsm, c.valid, n, k_hat, k);
   if (work) {
     subproblem_work(2, k, x_max, work, false);
-    if (k >= 2) work[kCntGathers] += x_max <= 2 ? k - 1 : k * (k - 1) / 2 + 2 * (k - 2);
+    if (k >= 2) {
+      work[kCntRankGathers] += x_max <= 2 ? k - 1 : k * (k - 1) / 2;  // candidate ranks
+      if (x_max > 2) work[kCntGathers] += 2 * (k - 2);          // R1, W2 per span term
+    }
   }
   if (k < 2) {
     i2 = i3 = 0.0;
     return;
   }
   const int c0 = __popc(m0);
-  const int* K2R = c.ints + c.L.k2r;
+  const uint16_t* K2R = c.ranks + c.L.k2r;
   const int* offk = c.ints + c.L.offk;
   double f2k, best3 = kLowest;
   if (x_max <= 2) {
-    const int* kb = K2R + offk[n];
+    const uint16_t* kb = K2R + offk[n];
     int r = -1;
     for (uint32_t s = bnd; s; s &= s - 1) {
       const int cs = __ffs(s) - 1;
@@ -646,29 +732,64 @@ __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, 
   } else {
     const double* W2 = c.tab + c.L.w2;
     const double* R1 = c.tab + c.L.r1;
-    const int* gq = c.ints + c.L.gq;
+    const uint32_t gq_s = (uint32_t)__cvta_generic_to_shared(c.ints + c.L.gq);
+    const uint32_t k2_s = (uint32_t)__cvta_generic_to_shared(K2R);
+    const uint32_t scr_s = (uint32_t)__cvta_generic_to_shared(scr);
     f2k = kLowest;
+    // the rank->value load of level t is consumed one level later (its
+    // global-memory latency overlaps the next level's gathers); best3 still
+    // folds the span terms in ascending t
+    double pf = 0.0;
+    int pt = -1, pw = 0;
     int j = 0;
     for (uint32_t ts = bnd;; ts &= ts - 1) {
       const int t = ts ? __ffs(ts) - 1 : n;
       ++j;
       const int b0t = __popc(m0 & prefix(t));
+      const int4 g = lds_v4(gq_s + 16u * t);
       if (j >= 2) {
-        const int* kb = K2R + (offk[t] + b0t - 8192);
+        const uint32_t kb = k2_s + 2u * (g.x + b0t);
+        // four candidates per trip, not unrolled further: the trip counts
+        // are short and differ across the warp's pairs
         int r = -1;
-        for (int i = 0; i < j - 1; ++i) {
-          const int v = scr[i];
-          r = max(r, kb[t * (v >> 16) + (v & 0xffff)]);
+        uint32_t sp = scr_s;
+        const uint32_t se = scr_s + 8u * (j - 1);
+#pragma unroll 1
+        for (; sp + 24u < se; sp += 32u) {
+          const int2 v0 = lds_v2(sp), v1 = lds_v2(sp + 8u), v2 = lds_v2(sp + 16u), v3 = lds_v2(sp + 24u);
+          const int a0 = lds_u16(kb + (t * v0.x + v0.y));
+          const int a1 = lds_u16(kb + (t * v1.x + v1.y));
+          const int a2 = lds_u16(kb + (t * v2.x + v2.y));
+          const int a3 = lds_u16(kb + (t * v3.x + v3.y));
+          r = max(r, max(a0, a1));
+          r = max(r, max(a2, a3));
+        }
+        if (sp < se) {
+          const int2 v0 = lds_v2(sp);
+          r = max(r, lds_u16(kb + (t * v0.x + v0.y)));
+          if (sp + 8u < se) {
+            const int2 v1 = lds_v2(sp + 8u);
+            r = max(r, lds_u16(kb + (t * v1.x + v1.y)));
+            if (sp + 16u < se) {
+              const int2 v2 = lds_v2(sp + 16u);
+              r = max(r, lds_u16(kb + (t * v2.x + v2.y)));
+            }
+          }
         }
         const double f2 = __ldg(c.val + r);
-        if (t < n)
-          best3 = dmax(best3, __dsub_rn(__dmul_rn(R1[t], f2), W2[w2_index(n, t, c0 - b0t)]));
-        else
+        if (pt >= 0) best3 = dmax(best3, __dsub_rn(__dmul_rn(R1[pt], pf), W2[pw]));
+        if (t < n) {
+          pf = f2;
+          pt = t;
+          pw = g.w + c0 - b0t;
+        } else {
           f2k = f2;
+        }
       }
       if (!ts) break;
-      // t becomes a split candidate s for the later t's: stage P_s / Q_s
-      scr[j - 1] = gq[t] + (b0t << 16) - b0t * t;
+      // t becomes a split candidate s for the later t's: stage (P_s, Q_s),
+      // pre-scaled to byte offsets in the uint16 rank table
+      sts_v2(scr_s + 8u * (j - 1), 2 * (g.y + b0t), 2 * (g.z - b0t * t));
     }
   }
   i2 = dmax(0.0, __dadd_rn(hq, f2k));
@@ -686,14 +807,19 @@ __device__ double memo_y3_rows3(const MemoCtx& c, uint32_t m0, uint32_t m1, uint
   const bool standard = c0 == c.std3[0] && c1 == c.std3[1];
   if (work) {
     subproblem_work(3, k, 2, work, false);
-    if (k >= 2) work[kCntGathers] += (standard ? 1 : 7) * (k - 1);
+    if (k >= 2) {
+      if (standard)
+        work[kCntRankGathers] += 2 * (k - 1);  // row offset + candidate rank
+      else
+        work[kCntGathers] += 7 * (k - 1);   // 6 p*log(p) + E2
+    }
   }
   if (k < 2) return 0.0;
   double best = kLowest;
   const int* t3o = c.ints + c.L.t3o;
   if (standard) {
     // standard row totals (no ties in the row variable): one rank gather per candidate
-    const int* T3R = c.ints + c.L.t3r;
+    const uint16_t* T3R = c.ranks + c.L.t3r;
     int r = -1;
     for (uint32_t s = bnd; s; s &= s - 1) {
       const int cs = __ffs(s) - 1;
@@ -728,12 +854,11 @@ __host__ __device__ inline int memo_scr_stride(int n) { return n | 1; }
 __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Tables tb,
                                                                const double* __restrict__ memo,
                                                                const double* __restrict__ memo_val,
-                                                               PairSpace ps, double cpar, int est,
+                                                               const MemoLayout L, PairSpace ps, double cpar, int est,
                                                                StatsOut out, double* ocells,
                                                                unsigned long long* counters) {
   extern __shared__ __align__(16) double msm[];
   const int n = vs.n, B = tb.B;
-  const MemoLayout L = memo_layout(n);
   {
     const double2* src = reinterpret_cast<const double2*>(memo);
     double2* dst = reinterpret_cast<double2*>(msm);
@@ -746,10 +871,11 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
   }
   __syncthreads();
   // this thread's scratch row after the tables (odd stride: bank = lane)
-  int* scr = reinterpret_cast<int*>(msm + ((L.total + 1) & ~1)) + threadIdx.x * memo_scr_stride(n);
+  int2* scr = reinterpret_cast<int2*>(msm + ((L.total + 1) & ~1)) + threadIdx.x * memo_scr_stride(n);
   MemoCtx c;
   c.tab = msm;
   c.ints = reinterpret_cast<const int*>(msm + L.ib);
+  c.ranks = reinterpret_cast<const uint16_t*>(c.ints + L.hb);
   c.val = memo_val;
   c.std3[0] = c.ints[L.std3];
   c.std3[1] = c.ints[L.std3 + 1];
@@ -760,7 +886,7 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
   const bool has_y3 = B >= 6;
   const int kh2 = max(1, (int)floor(cpar * (double)x2));
   const int kh3 = max(1, (int)floor(cpar * 2.0));
-  unsigned long long work[kNumCounters] = {0, 0, 0, 0, 0, 0};
+  unsigned long long work[kNumCounters] = {};
   unsigned long long* wk = counters ? work : nullptr;
 
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -927,20 +1053,29 @@ size_t memo_values(int n) {
   const MemoLayout L = memo_layout(n);
   return (size_t)L.k2cnt + L.t3cnt;
 }
+size_t memo_work_bytes(int n) { return memo_values(n) * (sizeof(double) + 2 * sizeof(int)) + 16; }
 
 static size_t memo_tab_bytes(int n) { return ((memo_doubles(n) + 1) & ~size_t(1)) * sizeof(double); }
 
 bool memo_fits(int n, int B) {
   // tables + at least 8 warps of scratch rows in 226 KB
   return n >= 2 && n <= 32 && B <= 7 &&
-         memo_tab_bytes(n) + sizeof(int) * (size_t)memo_scr_stride(n) * 256 <= 226 * 1024;
+         memo_tab_bytes(n) + sizeof(int2) * (size_t)memo_scr_stride(n) * 256 <= 226 * 1024;
 }
 
-void launch_build_memo(const Tables& tb, double* memo, double* vals, double* val, int n,
-                       cudaStream_t s) {
-  k_build_memo<<<1, 256, 0, s>>>(tb, memo, vals, n);
+int launch_build_memo(const Tables& tb, double* memo, void* work, double* val, int n,
+                      cudaStream_t s) {
   const int nv = (int)memo_values(n);
-  k_rank_memo<<<(nv + 255) / 256, 256, 0, s>>>(memo, vals, val, n);
+  const MemoWork w = memo_work(work, n);
+  cudaMemsetAsync(w.flag, 0, sizeof(int) * nv, s);
+  k_build_memo<<<1, 256, 0, s>>>(tb, memo, w.vals, n);
+  k_rank_memo<<<(nv + 255) / 256, 256, 0, s>>>(w.vals, w.rk, w.flag, nv);
+  k_dense_memo<<<1, 1024, 0, s>>>(memo, w, val, n);
+  int nval = -1;
+  if (cudaMemcpyAsync(&nval, w.nval, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return -1;
+  return nval;
 }
 
 void launch_pack_memo(const VarSet& vs, cudaStream_t s) {
@@ -953,8 +1088,9 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
                        cudaStream_t s) {
   if (ps.count <= 0) return;
   const size_t tab = memo_tab_bytes(vs.n);
-  const size_t budget = 226 * 1024 - tab;
-  const size_t row = sizeof(int) * (size_t)memo_scr_stride(vs.n);
+  size_t budget = 226 * 1024 - tab;
+  if (const char* e = getenv("MINE_B200_MEMO_SMEM_KB")) budget = std::min<size_t>(budget, atoi(e) * 1024 - tab);
+  const size_t row = sizeof(int2) * (size_t)memo_scr_stride(vs.n);
   int threads = (int)std::min<size_t>(kMemoMaxThreads, budget / row) / 32 * 32;
   threads = std::max(threads, 32);
   const size_t sm = tab + row * threads;
@@ -963,7 +1099,8 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long need = (ps.count + threads - 1) / threads;
   const unsigned blocks = (unsigned)std::min<long long>(sms, need);
-  k_memo_pairs<<<blocks, threads, sm, s>>>(vs, tb, memo, memo_val, ps, c, est, out, o_cells,
+  k_memo_pairs<<<blocks, threads, sm, s>>>(vs, tb, memo, memo_val, memo_layout(vs.n), ps, c, est,
+                                           out, o_cells,
                                            counters);
 }
 

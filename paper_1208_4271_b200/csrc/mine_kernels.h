@@ -31,7 +31,9 @@ struct VarSet {
 
 // Memo-tier table layout (offsets in doubles), see mine_kernels.cu.
 struct MemoLayout {
-  int n, k2cnt, t3cnt, w2, e2, r1, pln, ib, k2r, t3r, offk, gq, t3o, std3, total;
+  // doubles: w2, e2, r1, pln; ints from ib (in doubles): offk, gq, t3o, std3;
+  // uint16 candidate ranks from hb (in ints): k2r, t3r; total in doubles
+  int n, k2cnt, t3cnt, w2, e2, r1, pln, ib, offk, gq, t3o, std3, hb, k2r, t3r, total;
 };
 
 // Host-built constant tables (glibc libm, the reference's own arithmetic).
@@ -75,10 +77,11 @@ struct StatsOut {
 // Realised-work counters: algorithmic FP64 ops of the
 // reference arithmetic, p*log(p) lookups, DP candidates, span entries,
 // subproblems.
-enum { kCntFp64 = 0, kCntLookups, kCntCand, kCntSpans, kCntSub, kCntGathers, kNumCounters };
-// kCntGathers: shared-memory table gathers the executing tier actually needs
-// (memo tier: one per F(t,2) candidate, ...); the other counters describe the
-// reference's own arithmetic, independent of the tier.
+enum { kCntFp64 = 0, kCntLookups, kCntCand, kCntSpans, kCntSub, kCntGathers, kCntRankGathers, kNumCounters };
+// kCntGathers / kCntRankGathers: 8-byte / narrow (rank) shared-memory table
+// gathers the executing tier actually needs (memo tier: one 2-byte rank per F(t,2)
+// candidate, ...); the other counters describe the reference's own
+// arithmetic, independent of the tier.
 
 // Parameters of one row target for the general tier.
 struct YParams {
@@ -112,10 +115,13 @@ void launch_tiny_pairs(const VarSet& vs, const Tables& tb, const PairSpace& ps, 
 
 // Memo tier (n <= 25, B <= 7): every F(t,2) candidate precomputed per n.
 size_t memo_doubles(int n);
-size_t memo_values(int n);
+size_t memo_work_bytes(int n);   // build scratch (candidate values, sparse ranks, flags)
+size_t memo_values(int n);       // upper bound on distinct candidate values
 bool memo_fits(int n, int B);
-void launch_build_memo(const Tables& tb, double* memo, double* vals, double* val, int n,
-                       cudaStream_t s);
+// Builds the table image and the distinct-value table val[]; returns the
+// number of distinct candidate values (synchronises the stream once).
+int launch_build_memo(const Tables& tb, double* memo, void* work, double* val, int n,
+                      cudaStream_t s);
 void launch_pack_memo(const VarSet& vs, cudaStream_t s);
 void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
                        const double* memo_val, const PairSpace& ps, double c, int est,

@@ -1,5 +1,5 @@
 // Measurement probes (bench.py only, not part of the engine ABI): the
-// sustained FP64 add rate and the shared-memory 8-byte gather rate of this
+// sustained FP64 add rate and the shared-memory 8-byte and 2-byte gather rates of this
 // B200, the denominators of the roofline for the exact MINE DP, which is
 // neither HBM- nor tensor-core-bound.
 #include <cuda_runtime.h>
@@ -42,6 +42,31 @@ __global__ void k_lds(double* out, int iters) {
   if (acc == 12345.678) out[0] = acc;
 }
 
+// Random 2-byte gathers from a 16384-entry shared uint16 table (the size
+// class of the memo tier's dense candidate-rank tables) folded with an
+// integer max, 8 independent streams per thread.
+__global__ void k_lds2(int* out, int iters, int key) {
+  extern __shared__ unsigned short htab[];
+  constexpr uint32_t kN = 16384;
+  for (int i = threadIdx.x; i < (int)kN; i += blockDim.x) htab[i] = (unsigned short)(i * 7);
+  __syncthreads();
+  uint32_t st[kChains];
+  int acc[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) st[c] = 2654435761u * (threadIdx.x + 1) + blockIdx.x * 977u + c, acc[c] = 0;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+      st[c] = st[c] * 1664525u + 1013904223u;
+      acc[c] = max(acc[c], (int)htab[(st[c] >> 10) & (kN - 1)]);
+    }
+  }
+  int s = 0;
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) s ^= acc[c];
+  if (s == key) out[0] = s;  // key < 0 at run time: never true, not provable
+}
+
 template <typename F>
 float time_ms(F&& launch) {
   cudaEvent_t a, b;
@@ -61,7 +86,8 @@ float time_ms(F&& launch) {
 
 }  // namespace
 
-extern "C" int mine_b200_probe(int device, double* dadd_per_s, double* lds_per_s) {
+extern "C" int mine_b200_probe(int device, double* dadd_per_s, double* lds_per_s,
+                               double* lds2_per_s) {
   if (cudaSetDevice(device) != cudaSuccess) return -1;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -73,6 +99,10 @@ extern "C" int mine_b200_probe(int device, double* dadd_per_s, double* lds_per_s
   const int liters = 2048;
   ms = time_ms([&] { k_lds<<<blocks, threads>>>(out, liters); });
   *lds_per_s = (double)blocks * threads * liters * kChains / (ms * 1e-3);
+  const size_t sm2 = 16384 * sizeof(unsigned short);
+  const int b2 = sms * 4;  // 4 x 32 KB tables per SM
+  ms = time_ms([&] { k_lds2<<<b2, 512, sm2>>>(reinterpret_cast<int*>(out), liters, -1); });
+  *lds2_per_s = (double)b2 * 512 * liters * kChains / (ms * 1e-3);
   cudaFree(out);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }

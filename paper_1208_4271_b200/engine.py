@@ -39,8 +39,9 @@ class MineStatsOut(ctypes.Structure):
     _fields_ = [(k, _dp) for k in STATS] + [("cells", _dp)]
 
 
-NCOUNTERS = 6
-COUNTERS = ("fp64_ops", "lookups", "dp_candidates", "span_entries", "subproblems", "gathers")
+NCOUNTERS = 7
+COUNTERS = ("fp64_ops", "lookups", "dp_candidates", "span_entries", "subproblems", "gathers",
+            "rank_gathers")
 
 
 class MineOpts(ctypes.Structure):
