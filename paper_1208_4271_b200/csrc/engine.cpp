@@ -189,7 +189,7 @@ struct mine_b200_ctx {
   DevBuf vals, perm, runid, runstart, nruns, q, yhat, hq, lw, rsmask;
   DevBuf ocells, fscratch, stats, flag, idx, counters, memo, memo_vals, memo_val, rec, gscr,
       gqueue, glists;
-  int memo_n = -1;
+  int memo_n = -1, memo_nval = 0;
   std::vector<cudaEvent_t> events;
   long long launches = 0;
 };
@@ -276,11 +276,10 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   const int ny = B / 2 - 1;
   // Tier: 0 auto (memo > tiny > general), 1 tiny, 2 general, 3 memo.
   const bool tiny_ok = n <= 32 && B <= 7;
-  const bool memo_ok = memo_fits(n, B);
+  const bool memo_pre = memo_fits(n, B, 0);
   if (opts.tier == 1 && !tiny_ok) throw Failure("mine_b200: tiny tier needs n <= 32 and B <= 7");
-  if (opts.tier == 3 && !memo_ok) throw Failure("mine_b200: memo tier needs n <= 25 and B <= 7");
-  const bool memo = memo_ok && (opts.tier == 0 || opts.tier == 3);
-  const bool tiny = tiny_ok && (opts.tier == 1 || (opts.tier == 0 && !memo));
+  if (opts.tier == 3 && !memo_pre) throw Failure("mine_b200: memo tier needs n <= 24 and B <= 7");
+  bool memo = memo_pre && (opts.tier == 0 || opts.tier == 3);
 
   ctx->tables.build(n, B, s);
   const Tables tb = ctx->tables.view();
@@ -293,7 +292,14 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
     CK(cudaGetLastError());
     if (nval <= 0 || nval > 65535) throw Failure("mine_b200: memo table build failed");
     ctx->memo_n = n;
+    ctx->memo_nval = nval;
   }
+  // the distinct-value table must fit shared memory too (known after the build)
+  if (memo && !memo_fits(n, B, ctx->memo_nval)) {
+    if (opts.tier == 3) throw Failure("mine_b200: memo tier tables exceed shared memory for this n");
+    memo = false;
+  }
+  const bool tiny = tiny_ok && (opts.tier == 1 || (opts.tier == 0 && !memo));
   const int ncell = tb.ncell;
 
   // ---- variables -> device
@@ -432,7 +438,8 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
     pc.first = first + c0;
     pc.count = cn;
     if (memo) {
-      launch_memo_pairs(vs, tb, ctx->memo.as<double>(), ctx->memo_val.as<double>(), pc, par->c,
+      launch_memo_pairs(vs, tb, ctx->memo.as<double>(), ctx->memo_val.as<double>(), ctx->memo_nval,
+                        pc, par->c,
                         par->est, so, cells_dst, dcnt, s);
       ++ctx->launches;
     } else if (tiny) {

@@ -431,7 +431,7 @@ struct MemoCtx {
   const double* tab;
   const int* ints;
   const uint16_t* ranks;
-  const double* val;  // rank -> value (global, L1/L2-cached)
+  const double* val;  // rank -> value (shared memory)
   int std3[2];
   MemoLayout L;
   int n;
@@ -678,13 +678,19 @@ __device__ __forceinline__ int4 lds_v4(uint32_t addr) {  // read-only table
   return v;
 }
 // per-thread scratch: volatile so the compiler keeps them in program order
-__device__ __forceinline__ int2 lds_v2(uint32_t addr) {
-  int2 v;
-  asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+__device__ __forceinline__ int lds_s32(uint32_t addr) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
-__device__ __forceinline__ void sts_v2(uint32_t addr, int x, int y) {
-  asm volatile("st.shared.v2.s32 [%0], {%1, %2};" ::"r"(addr), "r"(x), "r"(y));
+__device__ __forceinline__ void sts_s32(uint32_t addr, int x) {
+  asm volatile("st.shared.s32 [%0], %1;" ::"r"(addr), "r"(x));
+}
+// byte address of candidate s at level t in one instruction (IDP.2A):
+// base + Q_s * 1 + P_s * t, with (Q_s, P_s) packed as two int16 halves of
+// the scratch word and (1, t) as the low two bytes of bt
+__device__ __forceinline__ uint32_t cand_addr(int packed, int bt, uint32_t base) {
+  return (uint32_t)__dp2a_lo(packed, bt, (int)base);
 }
 
 __device__ __forceinline__ uint32_t byte_of(const uint32_t* w, int s) {
@@ -700,7 +706,7 @@ __device__ __forceinline__ uint32_t byte_of(const uint32_t* w, int s) {
 // (int2, odd stride: conflict-free) and the inner loop is one 8-byte scratch
 // read, one IMAD, one 2-byte rank gather and one integer max per candidate.
 __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, int k_hat,
-                        double hq, double& i2, double& i3, unsigned long long* work, int2* scr) {
+                        double hq, double& i2, double& i3, unsigned long long* work, int* scr) {
   const int n = c.n;
   const uint32_t d = (m0 ^ (m0 << 1)) & c.valid & ~1u;
   int k;
@@ -728,7 +734,7 @@ __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, 
       const int a0 = __popc(m0 & prefix(cs));
       r = max(r, kb[memo_G(n, cs) + a0 * (n - cs + 1) + (c0 - a0)]);
     }
-    f2k = __ldg(c.val + r);
+    f2k = c.val[r];
   } else {
     const double* W2 = c.tab + c.L.w2;
     const double* R1 = c.tab + c.L.r1;
@@ -737,7 +743,7 @@ __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, 
     const uint32_t scr_s = (uint32_t)__cvta_generic_to_shared(scr);
     f2k = kLowest;
     // the rank->value load of level t is consumed one level later (its
-    // global-memory latency overlaps the next level's gathers); best3 still
+    // shared-memory latency overlaps the next level's gathers); best3 still
     // folds the span terms in ascending t
     double pf = 0.0;
     int pt = -1, pw = 0;
@@ -751,32 +757,28 @@ __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, 
         const uint32_t kb = k2_s + 2u * (g.x + b0t);
         // four candidates per trip, not unrolled further: the trip counts
         // are short and differ across the warp's pairs
+        const int bt = (t << 8) | 1;
         int r = -1;
         uint32_t sp = scr_s;
-        const uint32_t se = scr_s + 8u * (j - 1);
+        const uint32_t se = scr_s + 4u * (j - 1);
 #pragma unroll 1
-        for (; sp + 24u < se; sp += 32u) {
-          const int2 v0 = lds_v2(sp), v1 = lds_v2(sp + 8u), v2 = lds_v2(sp + 16u), v3 = lds_v2(sp + 24u);
-          const int a0 = lds_u16(kb + (t * v0.x + v0.y));
-          const int a1 = lds_u16(kb + (t * v1.x + v1.y));
-          const int a2 = lds_u16(kb + (t * v2.x + v2.y));
-          const int a3 = lds_u16(kb + (t * v3.x + v3.y));
+        for (; sp + 12u < se; sp += 16u) {
+          const int v0 = lds_s32(sp), v1 = lds_s32(sp + 4u), v2 = lds_s32(sp + 8u), v3 = lds_s32(sp + 12u);
+          const int a0 = lds_u16(cand_addr(v0, bt, kb));
+          const int a1 = lds_u16(cand_addr(v1, bt, kb));
+          const int a2 = lds_u16(cand_addr(v2, bt, kb));
+          const int a3 = lds_u16(cand_addr(v3, bt, kb));
           r = max(r, max(a0, a1));
           r = max(r, max(a2, a3));
         }
         if (sp < se) {
-          const int2 v0 = lds_v2(sp);
-          r = max(r, lds_u16(kb + (t * v0.x + v0.y)));
-          if (sp + 8u < se) {
-            const int2 v1 = lds_v2(sp + 8u);
-            r = max(r, lds_u16(kb + (t * v1.x + v1.y)));
-            if (sp + 16u < se) {
-              const int2 v2 = lds_v2(sp + 16u);
-              r = max(r, lds_u16(kb + (t * v2.x + v2.y)));
-            }
+          r = max(r, lds_u16(cand_addr(lds_s32(sp), bt, kb)));
+          if (sp + 4u < se) {
+            r = max(r, lds_u16(cand_addr(lds_s32(sp + 4u), bt, kb)));
+            if (sp + 8u < se) r = max(r, lds_u16(cand_addr(lds_s32(sp + 8u), bt, kb)));
           }
         }
-        const double f2 = __ldg(c.val + r);
+        const double f2 = c.val[r];
         if (pt >= 0) best3 = dmax(best3, __dsub_rn(__dmul_rn(R1[pt], pf), W2[pw]));
         if (t < n) {
           pf = f2;
@@ -788,8 +790,9 @@ __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, 
       }
       if (!ts) break;
       // t becomes a split candidate s for the later t's: stage (P_s, Q_s),
-      // pre-scaled to byte offsets in the uint16 rank table
-      sts_v2(scr_s + 8u * (j - 1), 2 * (g.y + b0t), 2 * (g.z - b0t * t));
+      // pre-scaled to byte offsets in the uint16 rank table, as int16 halves
+      // (|Q_s| < 2^15 and P_s < 2^11 for n <= 32)
+      sts_s32(scr_s + 4u * (j - 1), (2 * (g.y + b0t)) << 16 | ((2 * (g.z - b0t * t)) & 0xffff));
     }
   }
   i2 = dmax(0.0, __dadd_rn(hq, f2k));
@@ -826,7 +829,7 @@ __device__ double memo_y3_rows3(const MemoCtx& c, uint32_t m0, uint32_t m1, uint
       const uint32_t pre = (1u << cs) - 1u;  // c_s < n <= 31
       r = max(r, T3R[t3o[cs * (n + 1) + __popc(m0 & pre)] + __popc(m1 & pre)]);
     }
-    best = __ldg(c.val + r);
+    best = c.val[r];
   } else {
     const double* E2 = c.tab + c.L.e2;
     const double* P = c.tab + c.L.pln;
@@ -847,14 +850,24 @@ __device__ double memo_y3_rows3(const MemoCtx& c, uint32_t m0, uint32_t m1, uint
   return dmax(0.0, __dadd_rn(hq, best));
 }
 
-constexpr int kMemoMaxThreads = 768;
+constexpr int kMemoMaxThreads = 1024;
 
 __host__ __device__ inline int memo_scr_stride(int n) { return n | 1; }
 
+// Shared-memory plan: table image | val[] (distinct candidate values) |
+// per-thread scratch rows.
+__host__ __device__ inline int memo_val_off(const MemoLayout& L) { return (L.total + 1) & ~1; }
+__host__ __device__ inline int memo_scr_off(const MemoLayout& L, int nval) {
+  return memo_val_off(L) + ((nval + 1) & ~1);
+}
+
+// kCount: the instrumented (untimed) variant with realised-work counters.
+template <bool kCount>
 __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Tables tb,
                                                                const double* __restrict__ memo,
                                                                const double* __restrict__ memo_val,
-                                                               const MemoLayout L, PairSpace ps, double cpar, int est,
+                                                               int nval, const MemoLayout L,
+                                                               PairSpace ps, double cpar, int est,
                                                                StatsOut out, double* ocells,
                                                                unsigned long long* counters) {
   extern __shared__ __align__(16) double msm[];
@@ -863,6 +876,8 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
     const double2* src = reinterpret_cast<const double2*>(memo);
     double2* dst = reinterpret_cast<double2*>(msm);
     for (int i = threadIdx.x; i < (L.total + 1) / 2; i += blockDim.x) dst[i] = src[i];
+    double* vdst = msm + memo_val_off(L);
+    for (int i = threadIdx.x; i < nval; i += blockDim.x) vdst[i] = memo_val[i];
   }
   __shared__ double lg[8], lg2[8];
   if (threadIdx.x < 8) {
@@ -871,12 +886,12 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
   }
   __syncthreads();
   // this thread's scratch row after the tables (odd stride: bank = lane)
-  int2* scr = reinterpret_cast<int2*>(msm + ((L.total + 1) & ~1)) + threadIdx.x * memo_scr_stride(n);
+  int* scr = reinterpret_cast<int*>(msm + memo_scr_off(L, nval)) + threadIdx.x * memo_scr_stride(n);
   MemoCtx c;
   c.tab = msm;
   c.ints = reinterpret_cast<const int*>(msm + L.ib);
   c.ranks = reinterpret_cast<const uint16_t*>(c.ints + L.hb);
-  c.val = memo_val;
+  c.val = msm + memo_val_off(L);
   c.std3[0] = c.ints[L.std3];
   c.std3[1] = c.ints[L.std3 + 1];
   c.L = L;
@@ -887,7 +902,7 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
   const int kh2 = max(1, (int)floor(cpar * (double)x2));
   const int kh3 = max(1, (int)floor(cpar * 2.0));
   unsigned long long work[kNumCounters] = {};
-  unsigned long long* wk = counters ? work : nullptr;
+  unsigned long long* wk = kCount ? work : nullptr;
 
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long wl = blockIdx.x * (long long)blockDim.x + threadIdx.x; wl < ps.count; wl += stride) {
@@ -939,7 +954,7 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
     }
     small_stats(o, has_y3 ? 3 : 1, est, lg2, out, wl, ocells);
   }
-  if (counters) flush_work(work, counters);
+  if (kCount) flush_work(work, counters);
 }
 
 // Per-pair reduction: max-merge of the orientations (update_max,
@@ -1007,7 +1022,8 @@ cudaError_t init_kernel_attributes(int device) {
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (e != cudaSuccess) return e;
   const void* fns[] = {reinterpret_cast<const void*>(k_sort_vars),
-                       reinterpret_cast<const void*>(k_memo_pairs)};
+                       reinterpret_cast<const void*>(k_memo_pairs<false>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true>)};
   for (const void* f : fns) {
     cudaFuncAttributes fa{};
     e = cudaFuncGetAttributes(&fa, f);
@@ -1057,10 +1073,14 @@ size_t memo_work_bytes(int n) { return memo_values(n) * (sizeof(double) + 2 * si
 
 static size_t memo_tab_bytes(int n) { return ((memo_doubles(n) + 1) & ~size_t(1)) * sizeof(double); }
 
-bool memo_fits(int n, int B) {
-  // tables + at least 8 warps of scratch rows in 226 KB
+static size_t memo_smem_fixed(int n, int nval) {
+  return sizeof(double) * (size_t)memo_scr_off(memo_layout(n), nval);
+}
+
+bool memo_fits(int n, int B, int nval) {
+  // tables + val[] + at least 8 warps of scratch rows in 226 KB
   return n >= 2 && n <= 32 && B <= 7 &&
-         memo_tab_bytes(n) + sizeof(int2) * (size_t)memo_scr_stride(n) * 256 <= 226 * 1024;
+         memo_smem_fixed(n, nval) + sizeof(int) * (size_t)memo_scr_stride(n) * 256 <= 226 * 1024;
 }
 
 int launch_build_memo(const Tables& tb, double* memo, void* work, double* val, int n,
@@ -1083,25 +1103,30 @@ void launch_pack_memo(const VarSet& vs, cudaStream_t s) {
 }
 
 void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
-                       const double* memo_val, const PairSpace& ps, double c, int est,
+                       const double* memo_val, int nval, const PairSpace& ps, double c, int est,
                        StatsOut out, double* o_cells, unsigned long long* counters,
                        cudaStream_t s) {
   if (ps.count <= 0) return;
-  const size_t tab = memo_tab_bytes(vs.n);
-  size_t budget = 226 * 1024 - tab;
-  if (const char* e = getenv("MINE_B200_MEMO_SMEM_KB")) budget = std::min<size_t>(budget, atoi(e) * 1024 - tab);
-  const size_t row = sizeof(int2) * (size_t)memo_scr_stride(vs.n);
+  const size_t fixed = memo_smem_fixed(vs.n, nval);
+  size_t budget = 226 * 1024 - fixed;
+  if (const char* e = getenv("MINE_B200_MEMO_SMEM_KB"))
+    budget = std::min<size_t>(budget, atoi(e) * 1024 - fixed);
+  const size_t row = sizeof(int) * (size_t)memo_scr_stride(vs.n);
   int threads = (int)std::min<size_t>(kMemoMaxThreads, budget / row) / 32 * 32;
   threads = std::max(threads, 32);
-  const size_t sm = tab + row * threads;
+  const size_t sm = fixed + row * threads;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long need = (ps.count + threads - 1) / threads;
   const unsigned blocks = (unsigned)std::min<long long>(sms, need);
-  k_memo_pairs<<<blocks, threads, sm, s>>>(vs, tb, memo, memo_val, memo_layout(vs.n), ps, c, est,
-                                           out, o_cells,
-                                           counters);
+  const MemoLayout L = memo_layout(vs.n);
+  if (counters)
+    k_memo_pairs<true><<<blocks, threads, sm, s>>>(vs, tb, memo, memo_val, nval, L, ps, c, est, out,
+                                                   o_cells, counters);
+  else
+    k_memo_pairs<false><<<blocks, threads, sm, s>>>(vs, tb, memo, memo_val, nval, L, ps, c, est,
+                                                    out, o_cells, nullptr);
 }
 
 void launch_reduce(const Tables& tb, long long npairs, const double* ocells, int est, StatsOut out,

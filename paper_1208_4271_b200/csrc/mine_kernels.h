@@ -117,14 +117,15 @@ void launch_tiny_pairs(const VarSet& vs, const Tables& tb, const PairSpace& ps, 
 size_t memo_doubles(int n);
 size_t memo_work_bytes(int n);   // build scratch (candidate values, sparse ranks, flags)
 size_t memo_values(int n);       // upper bound on distinct candidate values
-bool memo_fits(int n, int B);
+// nval: distinct candidate values (0 before the build: the pre-check)
+bool memo_fits(int n, int B, int nval);
 // Builds the table image and the distinct-value table val[]; returns the
 // number of distinct candidate values (synchronises the stream once).
 int launch_build_memo(const Tables& tb, double* memo, void* work, double* val, int n,
                       cudaStream_t s);
 void launch_pack_memo(const VarSet& vs, cudaStream_t s);
 void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
-                       const double* memo_val, const PairSpace& ps, double c, int est,
+                       const double* memo_val, int nval, const PairSpace& ps, double c, int est,
                        StatsOut out, double* o_cells, unsigned long long* counters,
                        cudaStream_t s);
 
