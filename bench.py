@@ -289,8 +289,7 @@ def run_ours(args, world, rank, local):
                 "per_launch_work": {k: int(v) * world for k, v in work.items()},
                 "work_unit": "shared-memory table gathers the memo-tier algorithm needs "
                              "(one 2 B dense candidate rank per F(t,2) candidate, 2 x 8 B per "
-                             "level-3 span term, 4 B row offset + 2 B rank per standard 3-row "
-                             "candidate, 7 x 8 B "
+                             "level-3 span term, 2 B rank per standard 3-row candidate, 7 x 8 B "
                              "per other 3-row candidate), counted by the kernel; DESIGN.md "
                              "'Roofline'",
                 "gathers_8b": int(g8) * world, "gathers_rank": int(g2) * world,

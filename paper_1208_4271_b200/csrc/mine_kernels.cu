@@ -406,7 +406,7 @@ __host__ __device__ inline MemoLayout memo_layout(int n) {
   for (int ct = 2; ct <= n; ++ct) k2 += memo_G(ct, ct);
   L.n = n;
   L.k2cnt = k2;
-  L.t3cnt = n * (n + 1) * (n + 2) / 6;
+  L.t3cnt = n * (n + 1) * (n + 1);  // dense [c_s][a0][a1]
   // doubles
   L.w2 = 0;
   L.e2 = L.w2 + n * (n + 1) - n * (n - 1) / 2;
@@ -417,8 +417,7 @@ __host__ __device__ inline MemoLayout memo_layout(int n) {
   L.offk = 0;                    // (n + 2)
   // (n + 1) int4 per position t: {OFFK(t), g1(t), 2 g1(t) - g2(t), W2 row of t}, 16-byte aligned
   L.gq = (L.offk + n + 2 + 3) & ~3;
-  L.t3o = L.gq + 4 * (n + 1);    // (n + 1)^2: t3_index(c_s, a0, 0)
-  L.std3 = L.t3o + (n + 1) * (n + 1);  // 2: standard 3-row totals (C0, C1)
+  L.std3 = L.gq + 4 * (n + 1);   // 2: standard 3-row totals (C0, C1)
   L.hb = L.std3 + 2;             // uint16 region, relative to the int region
   // uint16 dense candidate ranks, relative to the uint16 region
   L.k2r = 0;
@@ -438,8 +437,8 @@ struct MemoCtx {
   uint32_t valid;
 };
 
-__device__ __forceinline__ int t3_index(int cs, int a0, int a1) {
-  return cs * (cs + 1) * (cs + 2) / 6 + a0 * (cs + 1) - a0 * (a0 - 1) / 2 + a1;
+__host__ __device__ __forceinline__ int t3_index(int n, int cs, int a0, int a1) {
+  return (cs * (n + 1) + a0) * (n + 1) + a1;
 }
 __device__ __forceinline__ int w2_index(int n, int cs, int u0) {
   return cs * (n + 1) - cs * (cs - 1) / 2 + u0;
@@ -466,14 +465,12 @@ __global__ void k_build_memo(Tables tb, double* memo, double* vals, int n) {
     }
   }
   int4* gq = reinterpret_cast<int4*>(ints + L.gq);
-  int* t3o = ints + L.t3o;
   for (int cs = threadIdx.x; cs <= n; cs += blockDim.x) {
     const int g1 = cs * (cs + 1) / 2 - 1;
     const int g2 = cs * (cs + 1) * (2 * cs + 1) / 6 - 1;
     int off = 0;
     for (int ct = 2; ct < cs; ++ct) off += memo_G(ct, ct);
     gq[cs] = make_int4(off, g1, 2 * g1 - g2, cs < n ? w2_index(n, cs, 0) : 0);
-    for (int a0 = 0; a0 <= n; ++a0) t3o[cs * (n + 1) + a0] = a0 <= cs ? t3_index(cs, a0, 0) : 0;
   }
   // K2[ct][cs][a0][b0]
   for (int idx = threadIdx.x; idx < (n + 1) * (n + 1); idx += blockDim.x) {
@@ -521,11 +518,11 @@ __global__ void k_build_memo(Tables tb, double* memo, double* vals, int n) {
   for (int cs = threadIdx.x; cs < n; cs += blockDim.x) {
     double acc2 = PL(n, cs);
     acc2 = __dadd_rn(acc2, PL(n, n - cs));
-    for (int a0 = 0; a0 <= cs; ++a0)
-      for (int a1 = 0; a0 + a1 <= cs; ++a1) {
+    for (int a0 = 0; a0 <= n; ++a0)
+      for (int a1 = 0; a1 <= n; ++a1) {
         const int b0 = std3[0] - a0, b1 = std3[1] - a1, b2 = (n - cs) - b0 - b1;
         double v = 0.0;  // unreachable tuple
-        if (std3[0] >= 0 && b0 >= 0 && b1 >= 0 && b2 >= 0) {
+        if (a0 + a1 <= cs && std3[0] >= 0 && b0 >= 0 && b1 >= 0 && b2 >= 0) {
           double acc = PL(n, a0);
           acc = __dadd_rn(acc, PL(n, a1));
           acc = __dadd_rn(acc, PL(n, cs - a0 - a1));
@@ -534,7 +531,7 @@ __global__ void k_build_memo(Tables tb, double* memo, double* vals, int n) {
           acc = __dadd_rn(acc, PL(n, b2));
           v = __dsub_rn(-acc2, -acc);
         }
-        vals[L.k2cnt + t3_index(cs, a0, a1)] = v;
+        vals[L.k2cnt + t3_index(n, cs, a0, a1)] = v;
       }
     const int m = n - cs;
     for (int u0 = 0; u0 <= m; ++u0) {
@@ -625,9 +622,11 @@ __global__ void __launch_bounds__(1024) k_dense_memo(double* memo, MemoWork w, d
   }
 }
 
-// Per-variable 96-byte record: rank byte of each sample (x-sorted position),
-// label flags (bit0: y=2 row 1, bit1: y=3 row 1, bit2: y=3 row 2), H(Q) for
-// y = 2, 3, the run-start mask and yhat for y = 2, 3.
+// Per-variable 96-byte record.  As the column variable X: byte t = 32 +
+// perm[t] - t, the funnel-shift amount that moves sample perm[t] (the sample
+// at sorted position t) of a sample-indexed mask to bit t; the run-start mask.
+// As the row variable Y: the sample-indexed label masks (y = 2 row 1, y = 3
+// rows 1 and 2), H(Q) for y = 2, 3 and yhat for y = 2, 3.
 __global__ void k_pack_memo(VarSet vs) {
   const int var = blockIdx.x * blockDim.x + threadIdx.x;
   if (var >= vs.V) return;
@@ -641,14 +640,18 @@ __global__ void k_pack_memo(VarSet vs) {
   const uint16_t* q3 = q2 + n;
   uint32_t rsm = 0;
   for (int t = 0; t < n; ++t) {
-    rec[perm[t]] = (uint8_t)t;
+    // funnel-shift amount that moves bit perm[t] of a sample mask to bit t
+    rec[t] = (uint8_t)(32 + perm[t] - t);
     if (t == 0 || rid[t] != rid[t - 1]) rsm |= 1u << t;
   }
+  uint32_t f2 = 0, f3a = 0, f3b = 0;
   for (int s = 0; s < n; ++s) {
-    uint8_t f = q2[s] == 1 ? 1 : 0;
-    if (vs.ny > 1) f |= (q3[s] == 1 ? 2 : 0) | (q3[s] == 2 ? 4 : 0);
-    rec[32 + s] = f;
+    f2 |= (q2[s] == 1 ? 1u : 0u) << s;
+    if (vs.ny > 1) f3a |= (q3[s] == 1 ? 1u : 0u) << s, f3b |= (q3[s] == 2 ? 1u : 0u) << s;
   }
+  memcpy(rec + 32, &f2, 4);
+  memcpy(rec + 36, &f3a, 4);
+  memcpy(rec + 40, &f3b, 4);
   const double h2 = vs.hq[(size_t)var * vs.ny];
   const double h3 = vs.ny > 1 ? vs.hq[(size_t)var * vs.ny + 1] : 0.0;
   memcpy(rec + 64, &h2, 8);
@@ -693,18 +696,15 @@ __device__ __forceinline__ uint32_t cand_addr(int packed, int bt, uint32_t base)
   return (uint32_t)__dp2a_lo(packed, bt, (int)base);
 }
 
-__device__ __forceinline__ uint32_t byte_of(const uint32_t* w, int s) {
-  return (w[s >> 2] >> ((s & 3) * 8)) & 0xffu;
-}
-
 // y = 2 (two rows; row-1 positions m0): I_2 and, if x_max == 3, I_3.
 // The K2 index of candidate (s, t) factors as
 //   OFFK(c_t) + G(c_t, c_s) + a0 (c_t - c_s + 1) + b0
 //     = [OFFK(c_t) + B0(t)] + c_t * P_s + Q_s,
 //   P_s = g1(c_s) + a0(s),  Q_s = 2 g1(c_s) - g2(c_s) - a0(s) c_s,
 // so (P_s, Q_s) are staged once per boundary in this thread's scratch row
-// (int2, odd stride: conflict-free) and the inner loop is one 8-byte scratch
-// read, one IMAD, one 2-byte rank gather and one integer max per candidate.
+// (packed int16 pair, odd stride: conflict-free) and the inner loop is one
+// scratch read, one IDP.2A (the whole byte address), one 2-byte rank gather
+// and half a 3-way integer max per candidate.
 __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, int k_hat,
                         double hq, double& i2, double& i3, unsigned long long* work, int* scr) {
   const int n = c.n;
@@ -741,59 +741,57 @@ __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, 
     const uint32_t gq_s = (uint32_t)__cvta_generic_to_shared(c.ints + c.L.gq);
     const uint32_t k2_s = (uint32_t)__cvta_generic_to_shared(K2R);
     const uint32_t scr_s = (uint32_t)__cvta_generic_to_shared(scr);
-    f2k = kLowest;
-    // the rank->value load of level t is consumed one level later (its
-    // shared-memory latency overlaps the next level's gathers); best3 still
-    // folds the span terms in ascending t
-    double pf = 0.0;
-    int pt = -1, pw = 0;
-    int j = 0;
-    for (uint32_t ts = bnd;; ts &= ts - 1) {
-      const int t = ts ? __ffs(ts) - 1 : n;
-      ++j;
-      const int b0t = __popc(m0 & prefix(t));
-      const int4 g = lds_v4(gq_s + 16u * t);
-      if (j >= 2) {
-        const uint32_t kb = k2_s + 2u * (g.x + b0t);
-        // four candidates per trip, not unrolled further: the trip counts
-        // are short and differ across the warp's pairs
-        const int bt = (t << 8) | 1;
-        int r = -1;
-        uint32_t sp = scr_s;
-        const uint32_t se = scr_s + 4u * (j - 1);
+    // max candidate rank of level t over the nst staged split points
+    auto level = [&](int t, int b0t, int offk_t, int nst) {
+      const uint32_t kb = k2_s + 2u * (offk_t + b0t);
+      const int bt = (t << 8) | 1;
+      int r = -1;
+      uint32_t sp = scr_s;
+      const uint32_t se = scr_s + 4u * nst;
+      // four candidates per trip, not unrolled further: the trip counts are
+      // short and differ across the warp's pairs
 #pragma unroll 1
-        for (; sp + 12u < se; sp += 16u) {
-          const int v0 = lds_s32(sp), v1 = lds_s32(sp + 4u), v2 = lds_s32(sp + 8u), v3 = lds_s32(sp + 12u);
-          const int a0 = lds_u16(cand_addr(v0, bt, kb));
-          const int a1 = lds_u16(cand_addr(v1, bt, kb));
-          const int a2 = lds_u16(cand_addr(v2, bt, kb));
-          const int a3 = lds_u16(cand_addr(v3, bt, kb));
-          r = max(r, max(a0, a1));
-          r = max(r, max(a2, a3));
-        }
-        if (sp < se) {
-          r = max(r, lds_u16(cand_addr(lds_s32(sp), bt, kb)));
-          if (sp + 4u < se) {
-            r = max(r, lds_u16(cand_addr(lds_s32(sp + 4u), bt, kb)));
-            if (sp + 8u < se) r = max(r, lds_u16(cand_addr(lds_s32(sp + 8u), bt, kb)));
-          }
-        }
-        const double f2 = c.val[r];
-        if (pt >= 0) best3 = dmax(best3, __dsub_rn(__dmul_rn(R1[pt], pf), W2[pw]));
-        if (t < n) {
-          pf = f2;
-          pt = t;
-          pw = g.w + c0 - b0t;
-        } else {
-          f2k = f2;
+      for (; sp + 12u < se; sp += 16u) {
+        const int v0 = lds_s32(sp), v1 = lds_s32(sp + 4u), v2 = lds_s32(sp + 8u), v3 = lds_s32(sp + 12u);
+        const int a0 = lds_u16(cand_addr(v0, bt, kb));
+        const int a1 = lds_u16(cand_addr(v1, bt, kb));
+        const int a2 = lds_u16(cand_addr(v2, bt, kb));
+        const int a3 = lds_u16(cand_addr(v3, bt, kb));
+        r = max(r, max(a0, a1));
+        r = max(r, max(a2, a3));
+      }
+      if (sp < se) {
+        r = max(r, lds_u16(cand_addr(lds_s32(sp), bt, kb)));
+        if (sp + 4u < se) {
+          r = max(r, lds_u16(cand_addr(lds_s32(sp + 4u), bt, kb)));
+          if (sp + 8u < se) r = max(r, lds_u16(cand_addr(lds_s32(sp + 8u), bt, kb)));
         }
       }
-      if (!ts) break;
-      // t becomes a split candidate s for the later t's: stage (P_s, Q_s),
-      // pre-scaled to byte offsets in the uint16 rank table, as int16 halves
-      // (|Q_s| < 2^15 and P_s < 2^11 for n <= 32)
-      sts_s32(scr_s + 4u * (j - 1), (2 * (g.y + b0t)) << 16 | ((2 * (g.z - b0t * t)) & 0xffff));
+      return r;
+    };
+    // t becomes a split point s for the later levels: stage (P_s, Q_s),
+    // pre-scaled to byte offsets in the uint16 rank table, as int16 halves
+    // (|Q_s| < 2^15 and P_s < 2^11 for n <= 32)
+    auto stage = [&](int slot, int t, int b0t, const int4& g) {
+      sts_s32(scr_s + 4u * slot, (2 * (g.y + b0t)) << 16 | ((2 * (g.z - b0t * t)) & 0xffff));
+    };
+    // boundaries t_1 < ... < t_{k-1} (bnd), then t = n; level t_1 has no
+    // split point and only stages; the span terms fold in ascending t
+    uint32_t ts = bnd;
+    {
+      const int t = __ffs(ts) - 1;
+      stage(0, t, __popc(m0 & ((1u << t) - 1u)), lds_v4(gq_s + 16u * t));
     }
+    int nst = 1;
+    for (ts &= ts - 1; ts; ts &= ts - 1, ++nst) {
+      const int t = __ffs(ts) - 1;  // t < n <= 31
+      const int b0t = __popc(m0 & ((1u << t) - 1u));
+      const int4 g = lds_v4(gq_s + 16u * t);
+      const double f2 = c.val[level(t, b0t, g.x, nst)];
+      best3 = dmax(best3, __dsub_rn(__dmul_rn(R1[t], f2), W2[g.w + c0 - b0t]));
+      stage(nst, t, b0t, g);
+    }
+    f2k = c.val[level(n, c0, offk[n], nst)];
   }
   i2 = dmax(0.0, __dadd_rn(hq, f2k));
   i3 = min(x_max, k) >= 3 ? dmax(0.0, __dadd_rn(hq, best3)) : i2;
@@ -812,14 +810,13 @@ __device__ double memo_y3_rows3(const MemoCtx& c, uint32_t m0, uint32_t m1, uint
     subproblem_work(3, k, 2, work, false);
     if (k >= 2) {
       if (standard)
-        work[kCntRankGathers] += 2 * (k - 1);  // row offset + candidate rank
+        work[kCntRankGathers] += k - 1;  // candidate rank (dense [c_s][a0][a1])
       else
         work[kCntGathers] += 7 * (k - 1);   // 6 p*log(p) + E2
     }
   }
   if (k < 2) return 0.0;
   double best = kLowest;
-  const int* t3o = c.ints + c.L.t3o;
   if (standard) {
     // standard row totals (no ties in the row variable): one rank gather per candidate
     const uint16_t* T3R = c.ranks + c.L.t3r;
@@ -827,7 +824,7 @@ __device__ double memo_y3_rows3(const MemoCtx& c, uint32_t m0, uint32_t m1, uint
     for (uint32_t s = bnd; s; s &= s - 1) {
       const int cs = __ffs(s) - 1;
       const uint32_t pre = (1u << cs) - 1u;  // c_s < n <= 31
-      r = max(r, T3R[t3o[cs * (n + 1) + __popc(m0 & pre)] + __popc(m1 & pre)]);
+      r = max(r, T3R[t3_index(n, cs, __popc(m0 & pre), __popc(m1 & pre))]);
     }
     best = c.val[r];
   } else {
@@ -911,25 +908,27 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
     double o[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
 #pragma unroll
     for (int orient = 0; orient < 2; ++orient) {
-      // column variable X: rank bytes + run starts; row variable Y: label
-      // flags, H(Q), yhat.  Loaded per orientation to keep registers low.
+      // column variable X: shift bytes + run starts; row variable Y: label
+      // masks, H(Q), yhat.  Loaded per orientation to keep registers low.
       const uint4* px = vs.rec + (size_t)(orient ? vb : va) * 6;
       const uint4* py = vs.rec + (size_t)(orient ? va : vb) * 6;
-      uint32_t rx[8], fy[8];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const uint4 u = __ldg(px + i), v = __ldg(py + 2 + i);
-        rx[4 * i] = u.x, rx[4 * i + 1] = u.y, rx[4 * i + 2] = u.z, rx[4 * i + 3] = u.w;
-        fy[4 * i] = v.x, fy[4 * i + 1] = v.y, fy[4 * i + 2] = v.z, fy[4 * i + 3] = v.w;
+      uint32_t ax[8];
+      {
+        const uint4 u = __ldg(px), v = __ldg(px + 1);
+        ax[0] = u.x, ax[1] = u.y, ax[2] = u.z, ax[3] = u.w;
+        ax[4] = v.x, ax[5] = v.y, ax[6] = v.z, ax[7] = v.w;
       }
+      const uint4 fy = __ldg(py + 2);
+      // the row-label masks in x-sorted order: bit t = label of sample
+      // perm_X[t]; one 64-bit funnel shift + one LOP3 per mask and position
       uint32_t m2 = 0, m3a = 0, m3b = 0;
 #pragma unroll
-      for (int sidx = 0; sidx < 32; ++sidx) {
-        if (sidx < n) {
-          const uint32_t pos = byte_of(rx, sidx), f = byte_of(fy, sidx);
-          m2 |= (f & 1u) << pos;
-          m3a |= ((f >> 1) & 1u) << pos;
-          m3b |= ((f >> 2) & 1u) << pos;
+      for (int t = 0; t < 32; ++t) {
+        if (t < n) {
+          const uint32_t a = __byte_perm(ax[t >> 2], 0, 0x4440 | (t & 3));
+          m2 |= (uint32_t)(((uint64_t)fy.x << 32) >> a) & (1u << t);
+          m3a |= (uint32_t)(((uint64_t)fy.y << 32) >> a) & (1u << t);
+          m3b |= (uint32_t)(((uint64_t)fy.z << 32) >> a) & (1u << t);
         }
       }
       const uint4 sx = __ldg(px + 5), hy = __ldg(py + 4), sy = __ldg(py + 5);
