@@ -400,13 +400,21 @@ __host__ __device__ __forceinline__ int memo_G(int ct, int cs) {
   return (ct + 2) * (cs * (cs + 1) / 2 - 1) - (cs * (cs + 1) * (2 * cs + 1) / 6 - 1);
 }
 
+// Dense 3-row table [c_s][a0][a1] with padded strides (a0: n + 2, c_s: an odd
+// number of words) so that lanes at different c_s / a0 spread over the banks.
+__host__ __device__ __forceinline__ int memo_t3_as(int n) { return n + 2; }
+__host__ __device__ __forceinline__ int memo_t3_rs(int n) { return memo_t3_as(n) * (n + 1) + 2; }
+__host__ __device__ __forceinline__ int t3_index(int n, int cs, int a0, int a1) {
+  return cs * memo_t3_rs(n) + a0 * memo_t3_as(n) + a1;
+}
+
 __host__ __device__ inline MemoLayout memo_layout(int n) {
   MemoLayout L;
   int k2 = 0;
   for (int ct = 2; ct <= n; ++ct) k2 += memo_G(ct, ct);
   L.n = n;
   L.k2cnt = k2;
-  L.t3cnt = n * (n + 1) * (n + 1);  // dense [c_s][a0][a1]
+  L.t3cnt = n * memo_t3_rs(n);  // dense [c_s][a0][a1], padded (bank spread)
   // doubles
   L.w2 = 0;
   L.e2 = L.w2 + n * (n + 1) - n * (n - 1) / 2;
@@ -415,9 +423,10 @@ __host__ __device__ inline MemoLayout memo_layout(int n) {
   L.ib = (L.pln + n + 2) & ~1;  // int region starts here (in doubles, 16-byte aligned)
   // ints, relative to the int region
   L.offk = 0;                    // (n + 2)
-  // (n + 1) int4 per position t: {OFFK(t), g1(t), 2 g1(t) - g2(t), W2 row of t}, 16-byte aligned
-  L.gq = (L.offk + n + 2 + 3) & ~3;
-  L.std3 = L.gq + 4 * (n + 1);   // 2: standard 3-row totals (C0, C1)
+  // per position t (n + 2 consecutive words each: any gather is conflict-free)
+  L.w2r = L.offk + n + 2;        // first W2 entry of row t
+  L.sb = L.w2r + n + 2;          // staging base word of t (memo_y2)
+  L.std3 = L.sb + n + 2;         // 2: standard 3-row totals (C0, C1)
   L.hb = L.std3 + 2;             // uint16 region, relative to the int region
   // uint16 dense candidate ranks, relative to the uint16 region
   L.k2r = 0;
@@ -437,9 +446,6 @@ struct MemoCtx {
   uint32_t valid;
 };
 
-__host__ __device__ __forceinline__ int t3_index(int n, int cs, int a0, int a1) {
-  return (cs * (n + 1) + a0) * (n + 1) + a1;
-}
 __device__ __forceinline__ int w2_index(int n, int cs, int u0) {
   return cs * (n + 1) - cs * (cs - 1) / 2 + u0;
 }
@@ -464,13 +470,13 @@ __global__ void k_build_memo(Tables tb, double* memo, double* vals, int n) {
       if (ct >= 2 && ct <= n) off += memo_G(ct, ct);
     }
   }
-  int4* gq = reinterpret_cast<int4*>(ints + L.gq);
-  for (int cs = threadIdx.x; cs <= n; cs += blockDim.x) {
+  for (int cs = threadIdx.x; cs <= n + 1; cs += blockDim.x) {
     const int g1 = cs * (cs + 1) / 2 - 1;
     const int g2 = cs * (cs + 1) * (2 * cs + 1) / 6 - 1;
-    int off = 0;
-    for (int ct = 2; ct < cs; ++ct) off += memo_G(ct, ct);
-    gq[cs] = make_int4(off, g1, 2 * g1 - g2, cs < n ? w2_index(n, cs, 0) : 0);
+    ints[L.w2r + cs] = cs < n ? w2_index(n, cs, 0) : 0;
+    // (P, Q') = (2 g1, 2 (2 g1 - g2) + 32768) as unsigned 16-bit halves; the
+    // a0-dependent part is added in memo_y2 (one IMAD)
+    ints[L.sb + cs] = cs <= n ? ((2 * g1) << 16) + 2 * (2 * g1 - g2) + 32768 : 0;
   }
   // K2[ct][cs][a0][b0]
   for (int idx = threadIdx.x; idx < (n + 1) * (n + 1); idx += blockDim.x) {
@@ -675,25 +681,20 @@ __device__ __forceinline__ int lds_u16(uint32_t addr) {  // read-only table
   asm("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
-__device__ __forceinline__ int4 lds_v4(uint32_t addr) {  // read-only table
-  int4 v;
-  asm("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
-  return v;
-}
 // per-thread scratch: volatile so the compiler keeps them in program order
-__device__ __forceinline__ int lds_s32(uint32_t addr) {
-  int v;
-  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr));
+__device__ __forceinline__ uint32_t lds_s32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
 __device__ __forceinline__ void sts_s32(uint32_t addr, int x) {
   asm volatile("st.shared.s32 [%0], %1;" ::"r"(addr), "r"(x));
 }
 // byte address of candidate s at level t in one instruction (IDP.2A):
-// base + Q_s * 1 + P_s * t, with (Q_s, P_s) packed as two int16 halves of
-// the scratch word and (1, t) as the low two bytes of bt
-__device__ __forceinline__ uint32_t cand_addr(int packed, int bt, uint32_t base) {
-  return (uint32_t)__dp2a_lo(packed, bt, (int)base);
+// base + Q'_s * 1 + P_s * t, with (Q'_s, P_s) packed as the two unsigned
+// 16-bit halves of the scratch word and (1, t) as the low two bytes of bt
+__device__ __forceinline__ uint32_t cand_addr(uint32_t packed, uint32_t bt, uint32_t base) {
+  return __dp2a_lo(packed, bt, base);
 }
 
 // y = 2 (two rows; row-1 positions m0): I_2 and, if x_max == 3, I_3.
@@ -738,13 +739,15 @@ __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, 
   } else {
     const double* W2 = c.tab + c.L.w2;
     const double* R1 = c.tab + c.L.r1;
-    const uint32_t gq_s = (uint32_t)__cvta_generic_to_shared(c.ints + c.L.gq);
-    const uint32_t k2_s = (uint32_t)__cvta_generic_to_shared(K2R);
+    const int* w2r = c.ints + c.L.w2r;
+    const int* sb = c.ints + c.L.sb;
+    // Q' = Q + 32768 is staged (unsigned halves); the bias comes off the base
+    const uint32_t k2_s = (uint32_t)__cvta_generic_to_shared(K2R) - 32768u;
     const uint32_t scr_s = (uint32_t)__cvta_generic_to_shared(scr);
     // max candidate rank of level t over the nst staged split points
     auto level = [&](int t, int b0t, int offk_t, int nst) {
       const uint32_t kb = k2_s + 2u * (offk_t + b0t);
-      const int bt = (t << 8) | 1;
+      const uint32_t bt = ((uint32_t)t << 8) | 1u;
       int r = -1;
       uint32_t sp = scr_s;
       const uint32_t se = scr_s + 4u * nst;
@@ -752,7 +755,7 @@ __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, 
       // short and differ across the warp's pairs
 #pragma unroll 1
       for (; sp + 12u < se; sp += 16u) {
-        const int v0 = lds_s32(sp), v1 = lds_s32(sp + 4u), v2 = lds_s32(sp + 8u), v3 = lds_s32(sp + 12u);
+        const uint32_t v0 = lds_s32(sp), v1 = lds_s32(sp + 4u), v2 = lds_s32(sp + 8u), v3 = lds_s32(sp + 12u);
         const int a0 = lds_u16(cand_addr(v0, bt, kb));
         const int a1 = lds_u16(cand_addr(v1, bt, kb));
         const int a2 = lds_u16(cand_addr(v2, bt, kb));
@@ -769,27 +772,27 @@ __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, 
       }
       return r;
     };
-    // t becomes a split point s for the later levels: stage (P_s, Q_s),
-    // pre-scaled to byte offsets in the uint16 rank table, as int16 halves
-    // (|Q_s| < 2^15 and P_s < 2^11 for n <= 32)
-    auto stage = [&](int slot, int t, int b0t, const int4& g) {
-      sts_s32(scr_s + 4u * slot, (2 * (g.y + b0t)) << 16 | ((2 * (g.z - b0t * t)) & 0xffff));
+    // t becomes a split point s for the later levels: stage (P_s, Q'_s),
+    // pre-scaled to byte offsets in the uint16 rank table, as unsigned 16-bit
+    // halves: word = ((2 (g1 + a0)) << 16) + 2 (2 g1 - g2 - a0 c_s) + 32768
+    //              = sb[c_s] + a0 (2^17 - 2 c_s)   (0 <= Q' < 2^16, P < 2^11 for n <= 32)
+    auto stage = [&](int slot, int t, int b0t) {
+      sts_s32(scr_s + 4u * slot, sb[t] + b0t * (131072 - 2 * t));
     };
     // boundaries t_1 < ... < t_{k-1} (bnd), then t = n; level t_1 has no
     // split point and only stages; the span terms fold in ascending t
     uint32_t ts = bnd;
     {
       const int t = __ffs(ts) - 1;
-      stage(0, t, __popc(m0 & ((1u << t) - 1u)), lds_v4(gq_s + 16u * t));
+      stage(0, t, __popc(m0 & ((1u << t) - 1u)));
     }
     int nst = 1;
     for (ts &= ts - 1; ts; ts &= ts - 1, ++nst) {
       const int t = __ffs(ts) - 1;  // t < n <= 31
       const int b0t = __popc(m0 & ((1u << t) - 1u));
-      const int4 g = lds_v4(gq_s + 16u * t);
-      const double f2 = c.val[level(t, b0t, g.x, nst)];
-      best3 = dmax(best3, __dsub_rn(__dmul_rn(R1[t], f2), W2[g.w + c0 - b0t]));
-      stage(nst, t, b0t, g);
+      const double f2 = c.val[level(t, b0t, offk[t], nst)];
+      best3 = dmax(best3, __dsub_rn(__dmul_rn(R1[t], f2), W2[w2r[t] + c0 - b0t]));
+      stage(nst, t, b0t);
     }
     f2k = c.val[level(n, c0, offk[n], nst)];
   }
