@@ -93,6 +93,9 @@ typedef struct mine_stats_out {
   double* mic_e;
   double* tic;
   double* cells;
+  /* statistics.cpp:39-51 (the remaining MineStatistics fields) */
+  double* pearson_r;     /* NaN when either variable has zero variance */
+  double* nonlinearity;  /* mic - pearson_r^2 */
 } mine_stats_out;
 
 /* Engine context: one per host thread (calls on one context are serialised). */

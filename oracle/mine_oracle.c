@@ -437,6 +437,25 @@ int mo_statistics(int n, const double* x, const double* y, double alpha, double 
   return 0;
 }
 
+int mo_pearson(int n, const double* x, const double* y, double* r) {
+  if (n < 2) return fail("pearson: need at least 2 samples");
+  double sx = 0.0, sy = 0.0; /* :42-43 xs.mean() = sum() / size() */
+  for (int i = 0; i < n; ++i) sx += x[i];
+  for (int i = 0; i < n; ++i) sy += y[i];
+  const double mx = sx / (double)n, my = sy / (double)n;
+  double sxx = 0.0, syy = 0.0, sxy = 0.0; /* :44-45, :47 */
+  for (int i = 0; i < n; ++i) sxx += (x[i] - mx) * (x[i] - mx);
+  for (int i = 0; i < n; ++i) syy += (y[i] - my) * (y[i] - my);
+  if (!(sxx > 0.0) || !(syy > 0.0)) { /* :46 */
+    *r = NAN;
+    return 0;
+  }
+  for (int i = 0; i < n; ++i) sxy += (x[i] - mx) * (y[i] - my);
+  const double v = sxy / sqrt(sxx * syy);
+  *r = v < -1.0 ? -1.0 : (1.0 < v ? 1.0 : v); /* :48 std::clamp */
+  return 0;
+}
+
 int mo_subproblem(int n, const double* col_var, const double* row_var, int y_target, int x_max,
                   int k_hat, int* row_count, int* q_x, int* clump_count, int* k, int* bounds,
                   double* h_q, double* values) {

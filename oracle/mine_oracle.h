@@ -66,6 +66,11 @@ int mo_cross(const double* X, int px, const double* Y, int py, int n, double alp
 int mo_pairs(const double* vars, int n, const int* xi, const int* yi, long npairs, double alpha,
              double c, int est, int threads, double* out);
 
+/* pearson (statistics.cpp:39-49): sequential sums in sample order (the
+ * reference's Eigen reductions, as the oracle build's Eigen subset runs them);
+ * NaN when either variance is zero.  Returns 0 / -1 (length / n < 2). */
+int mo_pearson(int n, const double* x, const double* y, double* r);
+
 /* Condensed index -> (i, j), 0-based, the PairSequence::at arithmetic. */
 void mo_pair_at(long p, long w, int* i, int* j);
 

@@ -85,6 +85,7 @@ class Oracle:
                                ctypes.c_double, ctypes.c_int, ctypes.c_int, _dp]
         L.mo_pairs.argtypes = [_dp, ctypes.c_int, _ip, _ip, ctypes.c_long, ctypes.c_double,
                                ctypes.c_double, ctypes.c_int, ctypes.c_int, _dp]
+        L.mo_pearson.argtypes = [ctypes.c_int, _dp, _dp, _dp]
         L.mo_pair_at.argtypes = [ctypes.c_long, ctypes.c_long, _ip, _ip]
         L.mo_pair_at.restype = None
         L.mo_last_error.restype = ctypes.c_char_p
@@ -117,6 +118,15 @@ class Oracle:
         out = np.zeros(NSTAT)
         self._check(self.L.mo_statistics(x.size, _d(x), _d(y), alpha, c, est, _d(out)))
         return out
+
+    def pearson(self, x, y):
+        """statistics.cpp:39-49 (NaN for a zero-variance input)."""
+        x, y = _f64(x), _f64(y)
+        if x.shape != y.shape:
+            raise ValueError("pearson: input lengths differ")
+        r = np.zeros(1)
+        self._check(self.L.mo_pearson(x.size, _d(x), _d(y), _d(r)))
+        return float(r[0])
 
     def reduce(self, bound, o1, o2, est=0):
         out = np.zeros(NSTAT)

@@ -188,7 +188,7 @@ struct mine_b200_ctx {
   TableSet tables;
   DevBuf vals, perm, runid, runstart, nruns, q, yhat, hq, lw, rsmask;
   DevBuf ocells, fscratch, stats, flag, idx, counters, memo, memo_vals, memo_val, rec, gscr,
-      gqueue, glists;
+      gqueue, glists, dx, sxx, micscr;
   int memo_n = -1, memo_nval = 0;
   std::vector<cudaEvent_t> events;
   long long launches = 0;
@@ -372,7 +372,16 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
 
   // ---- outputs: device-resident, or a device staging area drained by the
   // copy stream chunk by chunk while the next chunk computes.
-  double* const user_stat[6] = {out->mic, out->mas, out->mev, out->mcn, out->mic_e, out->tic};
+  constexpr int kStats = 8;  // mic mas mev mcn mic_e tic pearson_r nonlinearity
+  double* const user_stat[kStats] = {out->mic,   out->mas, out->mev,       out->mcn,
+                                     out->mic_e, out->tic, out->pearson_r, out->nonlinearity};
+  const bool want_r = out->pearson_r || out->nonlinearity;
+  if (want_r) {  // per-variable centring, once per call
+    vs.dx = static_cast<double*>(ctx->dx.ensure(sizeof(double) * (size_t)V * n));
+    vs.sxx = static_cast<double*>(ctx->sxx.ensure(sizeof(double) * (size_t)V));
+    launch_center_vars(vs, s);
+    ++ctx->launches;
+  }
   const bool small = tiny || memo;  // one thread per pair, stats written directly
   std::vector<YParams> yps;
   for (int y = 2; y <= B / 2; ++y) {
@@ -400,7 +409,7 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   const long long nchunks = (count + chunk - 1) / chunk;
   const int nslots = dio ? 1 : 2;  // double-buffered staging for host io
   double* stage = nullptr;
-  const size_t stage_stats = 6 * (size_t)chunk;
+  const size_t stage_stats = kStats * (size_t)chunk;
   const size_t stage_cells = out->cells ? 2 * (size_t)ncell * chunk : 0;
   if (!dio) stage = static_cast<double*>(ctx->stats.ensure(sizeof(double) * nslots * (stage_stats + stage_cells)));
   double* ocells = nullptr;
@@ -418,6 +427,8 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
     const long long cn = std::min(chunk, count - c0);
     const int slot = (int)(ci % nslots);
     StatsOut so;
+    double* so_r = nullptr;   // pearson_r
+    double* so_nl = nullptr;  // nonlinearity
     double* cells_dst = nullptr;
     if (dio) {
       so.mic = user_stat[0] ? user_stat[0] + c0 : nullptr;
@@ -426,12 +437,17 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
       so.mcn = user_stat[3] ? user_stat[3] + c0 : nullptr;
       so.mic_e = user_stat[4] ? user_stat[4] + c0 : nullptr;
       so.tic = user_stat[5] ? user_stat[5] + c0 : nullptr;
+      so_r = user_stat[6] ? user_stat[6] + c0 : nullptr;
+      so_nl = user_stat[7] ? user_stat[7] + c0 : nullptr;
+      if (so_nl && !so.mic)  // non-linearity needs MIC even when it is not requested
+        so.mic = static_cast<double*>(ctx->micscr.ensure(sizeof(double) * (size_t)chunk));
       cells_dst = out->cells ? out->cells + (size_t)c0 * 2 * ncell : nullptr;
     } else {
       double* base = stage + (size_t)slot * (stage_stats + stage_cells);
       if (ci >= nslots) CK(cudaStreamWaitEvent(s, ctx_event(ctx, 2 * slot + 1), 0));  // slot drained
-      double** so_p[6] = {&so.mic, &so.mas, &so.mev, &so.mcn, &so.mic_e, &so.tic};
-      for (int k = 0; k < 6; ++k) *so_p[k] = user_stat[k] ? base + (size_t)k * chunk : nullptr;
+      double** so_p[kStats] = {&so.mic, &so.mas, &so.mev, &so.mcn, &so.mic_e, &so.tic, &so_r, &so_nl};
+      for (int k = 0; k < kStats; ++k) *so_p[k] = user_stat[k] ? base + (size_t)k * chunk : nullptr;
+      if (so_nl && !so.mic) so.mic = base;  // MIC for the non-linearity, not drained
       cells_dst = out->cells ? base + stage_stats : nullptr;
     }
     PairSpace pc = ps;
@@ -462,13 +478,17 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
       if (cells_dst)
         CK(cudaMemcpyAsync(cells_dst, ocells, sizeof(double) * 2 * ncell * cn, cudaMemcpyDeviceToDevice, s));
     }
+    if (want_r) {
+      launch_pearson_pairs(vs, pc, so.mic, so_r, so_nl, s);
+      ++ctx->launches;
+    }
     CK(cudaGetLastError());
     if (!dio) {
       // drain this chunk on the copy stream
       CK(cudaEventRecord(ctx_event(ctx, 2 * slot), s));
       CK(cudaStreamWaitEvent(ctx->copy, ctx_event(ctx, 2 * slot), 0));
       const double* base = stage + (size_t)slot * (stage_stats + stage_cells);
-      for (int k = 0; k < 6; ++k)
+      for (int k = 0; k < kStats; ++k)
         if (user_stat[k])
           CK(cudaMemcpyAsync(user_stat[k] + c0, base + (size_t)k * chunk, sizeof(double) * cn,
                              cudaMemcpyDeviceToHost, ctx->copy));

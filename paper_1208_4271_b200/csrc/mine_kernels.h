@@ -27,6 +27,8 @@ struct VarSet {
   uint8_t* lw = nullptr;         // V x n      tiny tier: packed labels (y=2: bits 0-1, y=3: 2-3)
   uint32_t* rsmask = nullptr;    // V          tiny tier: run-start bitmask over sorted positions
   uint4* rec = nullptr;          // V x 6      memo tier: 96-byte per-variable record
+  double* dx = nullptr;          // V x n      Pearson: centred samples (statistics.cpp:42-43)
+  double* sxx = nullptr;         // V          Pearson: sum of squared deviations
 };
 
 // Memo-tier table layout (offsets in doubles), see mine_kernels.cu.
@@ -169,5 +171,10 @@ void launch_build_div(double* div, int n, cudaStream_t s);
 
 void launch_reduce(const Tables& tb, long long npairs, const double* ocells, int est,
                    StatsOut out, long long out_offset, cudaStream_t s);
+
+// Pearson r / non-linearity (pearson.cu, statistics.cpp:39-51).
+void launch_center_vars(const VarSet& vs, cudaStream_t s);
+void launch_pearson_pairs(const VarSet& vs, const PairSpace& ps, const double* mic,
+                          double* pearson, double* nonlin, cudaStream_t s);
 
 }  // namespace mb200

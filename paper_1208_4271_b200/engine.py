@@ -22,6 +22,9 @@ LIB_PATH = os.environ.get("MINE_B200_LIB", os.path.join(_PKG, "libmine_b200.so")
 MIC_APPROX = 0
 MIC_E = 1
 STATS = ("mic", "mas", "mev", "mcn", "mic_e", "tic")
+# statistics.cpp:39-51, computed only when requested
+EXTRA_STATS = ("pearson_r", "nonlinearity")
+ALL_STATS = STATS + EXTRA_STATS
 
 _dp = ctypes.POINTER(ctypes.c_double)
 _ip = ctypes.POINTER(ctypes.c_int)
@@ -36,7 +39,7 @@ class MineParameter(ctypes.Structure):
 
 
 class MineStatsOut(ctypes.Structure):
-    _fields_ = [(k, _dp) for k in STATS] + [("cells", _dp)]
+    _fields_ = [(k, _dp) for k in STATS] + [("cells", _dp)] + [(k, _dp) for k in EXTRA_STATS]
 
 
 NCOUNTERS = 7
@@ -229,9 +232,12 @@ class Engine:
     # -- output plumbing ----------------------------------------------------
     @staticmethod
     def _outputs(count: int, stats, cells: bool, bound: int | None):
+        unknown = set(stats) - set(ALL_STATS)
+        if unknown:
+            raise ValueError(f"unknown statistics {sorted(unknown)}")
         res = {k: np.empty(count) for k in stats}
         so = MineStatsOut()
-        for k in STATS:
+        for k in ALL_STATS:
             setattr(so, k, res[k].ctypes.data_as(_dp) if k in res else None)
         if cells:
             nc = len(cell_shapes(bound))
@@ -293,7 +299,7 @@ class Engine:
         outputs in HBM, enqueued on `stream`.  counters=True returns the
         realised-work totals (synchronises)."""
         so = MineStatsOut()
-        for k in STATS:
+        for k in ALL_STATS:
             setattr(so, k, ctypes.cast(ctypes.c_void_p(out_ptrs[k]), _dp) if out_ptrs.get(k) else None)
         o = self._opts(first, count, tier)
         o.device_io, o.async_, o.stream = 1, int(async_), ctypes.c_void_p(stream)
@@ -312,7 +318,7 @@ class Engine:
         variables, scoring, D2H of the requested statistics into `outs`
         (preallocated, ideally pinned, numpy arrays)."""
         so = MineStatsOut()
-        for k in STATS:
+        for k in ALL_STATS:
             setattr(so, k, outs[k].ctypes.data_as(_dp) if k in outs else None)
         p, n = vars_np.shape
         self._check(self.L.mine_b200_pairwise(self.ctx, _ptr(vars_np), p, n, ctypes.byref(params._c()),
@@ -350,12 +356,12 @@ class Engine:
         return CharacteristicMatrix(b, res["cells"][0, 0], res["cells"][0, 1])
 
     def compute_statistics(self, xs, ys, params: Parameters = Parameters(), tier: int = 0) -> dict:
-        """mine::compute_statistics (statistics.cpp:53-63) minus Pearson, plus
-        MIC_e and TIC."""
+        """mine::compute_statistics (statistics.cpp:53-63): MIC, MAS, MEV, MCN,
+        pearson_r, nonlinearity, plus MIC_e and TIC."""
         xs, ys = _f64(xs), _f64(ys)
         if xs.shape != ys.shape:
             raise MineError("compute_score: input lengths differ")
-        res = self.pairs(np.stack([xs, ys]), [0], [1], params, tier=tier)
+        res = self.pairs(np.stack([xs, ys]), [0], [1], params, stats=ALL_STATS, tier=tier)
         return {k: float(v[0]) for k, v in res.items()}
 
 

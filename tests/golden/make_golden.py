@@ -40,14 +40,15 @@ def pairs_fixture(R):
         ys.append(y)
         meta.append((n, alpha, c, b))
         cells.append(m)
-        stats.append(s[:4])
+        stats.append(s[:6])
     off = np.cumsum([0] + [len(x) for x in xs])
     coff = np.cumsum([0] + [len(m) for m in cells])
     np.savez_compressed(os.path.join(HERE, "ref_pairs.npz"),
                         x=np.concatenate(xs), y=np.concatenate(ys), off=off,
                         n=np.array([m[0] for m in meta]), alpha=np.array([m[1] for m in meta]),
                         c=np.array([m[2] for m in meta]), bound=np.array([m[3] for m in meta]),
-                        cells=np.concatenate(cells), coff=coff, stats=np.array(stats))
+                        cells=np.concatenate(cells), coff=coff, stats=np.array(stats)[:, :4],
+                        stats6=np.array(stats))
 
 
 def subproblem_fixture(R):
@@ -80,7 +81,9 @@ def configs_fixture(R):
     out = {}
     w1 = datagen.make(1)
     out["c1_vars"] = w1.X[:60]
-    out["c1_stats"] = R.run_analysis(w1.X[:60], w1.alpha, w1.c, workers=8)[:, :4]
+    c1 = R.run_analysis(w1.X[:60], w1.alpha, w1.c, workers=8)
+    out["c1_stats"] = c1[:, :4]
+    out["c1_stats6"] = c1[:, :6]  # + pearson_r, nonlinearity (statistics.cpp:39-51)
     w0 = datagen.make(0, npairs=10)
     out["c0_vars"] = w0.X
     out["c0_stats"] = np.array([R.statistics(w0.X[2 * i], w0.X[2 * i + 1], 0.6, 15.0)[:4]

@@ -192,6 +192,32 @@ def test_golden_configs_gpu(engine):
     assert_bit_equal(stats_matrix(r)[:, :4], g["c4r_stats"], "c4 (n=1500)")
 
 
+def _same(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    nan = np.isnan(a) & np.isnan(b)
+    return bool(((a.view(np.int64) == b.view(np.int64)) | nan).all())
+
+
+def test_golden_pearson_gpu(engine):
+    """pearson_r / nonlinearity (statistics.cpp:39-51) on the device against
+    the reference's compute_statistics: the golden pairs one by one, and the c1
+    slice through the batch path (bit-exact: both sum sequentially)."""
+    g = _golden("ref_pairs.npz")
+    for i in range(len(g["n"])):
+        x = g["x"][g["off"][i]:g["off"][i + 1]]
+        y = g["y"][g["off"][i]:g["off"][i + 1]]
+        s = engine.compute_statistics(x, y, Parameters(float(g["alpha"][i]), float(g["c"][i])))
+        assert _same(s["pearson_r"], g["stats6"][i, 4]), i
+        assert _same(s["nonlinearity"], g["stats6"][i, 5]), i
+    c = _golden("ref_configs.npz")
+    r = engine.pairwise(c["c1_vars"], stats=("mic", "pearson_r", "nonlinearity"))
+    assert _same(r["pearson_r"], c["c1_stats6"][:, 4])
+    assert _same(r["nonlinearity"], c["c1_stats6"][:, 5])
+    # non-linearity alone (MIC computed internally), and the general tier
+    r2 = engine.pairwise(c["c1_vars"], stats=("nonlinearity",), tier=2)
+    assert _same(r2["nonlinearity"], c["c1_stats6"][:, 5])
+
+
 # --- config-scale parity and size-independent properties ---------------------
 def test_c2_poisson_ties_slice(engine, oracle):
     """c2 (heavy ties / zeros): 12 variables -> 66 pairs, est = MIC_e."""

@@ -256,3 +256,25 @@ def test_golden_configs(oracle):
     assert (bits(oracle.pairwise(g["c3_vars"])[:, :4]) == bits(g["c3_stats"])).all()
     got = oracle.cross(g["c4r_X"], g["c4r_Y"], 0.75, 15.0, 1)
     assert (bits(got[:, :4]) == bits(g["c4r_stats"])).all()
+
+
+def _same(a, b):
+    """Bit-equal, treating any two NaNs as equal (NaN payloads are not part
+    of the reference's contract: pearson returns quiet_NaN, statistics.cpp:46)."""
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    nan = np.isnan(a) & np.isnan(b)
+    return bool(((bits(a) == bits(b)) | nan).all())
+
+
+def test_golden_pearson(oracle):
+    """statistics.cpp:39-51 against the reference's own compute_statistics
+    (pearson_r, nonlinearity columns of the golden fixture)."""
+    g = _load("ref_pairs.npz")
+    s6 = g["stats6"]
+    for i in range(len(g["n"])):
+        x = g["x"][g["off"][i]:g["off"][i + 1]]
+        y = g["y"][g["off"][i]:g["off"][i + 1]]
+        r = oracle.pearson(x, y)
+        assert _same(r, s6[i, 4]), i
+        assert _same(s6[i, 0] - r * r, s6[i, 5]), i
+    assert np.isnan(s6[:, 4]).any() and not np.isnan(s6[:, 4]).all()
