@@ -120,6 +120,12 @@ typedef struct mine_b200_opts {
   unsigned long long* counters;
   void* ev_begin;
   void* ev_end;
+  /* 1: the variables are the SAME as in the previous call on this context
+   * (same pointers, shapes, alpha; contents unchanged): skip their upload and
+   * the per-variable stages (rank, equipartition, packing -- SURVEY 8f rank 1,
+   * e.g. successive windows of one pairwise job, or master_vs_all over many
+   * masters against one Y).  A call whose variables differ fails. */
+  int reuse_vars;
 } mine_b200_opts;
 #define MINE_B200_NCOUNTERS 7
 

@@ -6,13 +6,13 @@ the reference (/root/reference/proj/src) -- runs as hand-written sm_100a CUDA
 kernels in libmine_b200.so behind the C ABI of include/mine_b200.h.
 """
 from .engine import (  # noqa: F401
-    MIC_APPROX, MIC_E, STATS, CharacteristicMatrix, Engine, MineError, Parameters,
+    ALL_STATS, MIC_APPROX, MIC_E, STATS, CharacteristicMatrix, Engine, MineError, Parameters,
     cell_shapes, compute_score, compute_statistics, default_engine, grid_bound,
     load_library, validate_parameters,
 )
 
 __all__ = [
-    "MIC_APPROX", "MIC_E", "STATS", "CharacteristicMatrix", "Engine", "MineError", "Parameters",
+    "ALL_STATS", "MIC_APPROX", "MIC_E", "STATS", "CharacteristicMatrix", "Engine", "MineError", "Parameters",
     "cell_shapes", "compute_score", "compute_statistics", "default_engine", "grid_bound",
     "load_library", "validate_parameters",
 ]

@@ -190,6 +190,15 @@ struct mine_b200_ctx {
   DevBuf ocells, fscratch, stats, flag, idx, counters, memo, memo_vals, memo_val, rec, gscr,
       gqueue, glists, dx, sxx, micscr;
   int memo_n = -1, memo_nval = 0;
+  // per-variable state of the previous call (opts.reuse_vars)
+  struct Prep {
+    bool valid = false;
+    int kind = -1, va = 0, vb = 0, n = 0, B = 0;
+    const void* a = nullptr;
+    const void* b = nullptr;
+    bool dio = false, memo = false, tiny = false, centred = false;
+    const double* dvals = nullptr;
+  } prep;
   std::vector<cudaEvent_t> events;
   long long launches = 0;
 };
@@ -250,6 +259,30 @@ GenScratch gen_scratch(mine_b200_ctx* ctx, int n, const YParams& yp, long long n
   return g;
 }
 
+// The per-variable state a successful call leaves on its context.
+struct CtxPrepared {
+  const Call& call;
+  const double* dvals;
+  int B;
+  bool dio, memo, tiny, centred = false;
+  template <typename PrepT>
+  void commit(PrepT& P) const {
+    P.valid = true;
+    P.kind = call.kind;
+    P.a = call.a;
+    P.b = call.b;
+    P.va = call.va;
+    P.vb = call.vb;
+    P.n = call.n;
+    P.B = B;
+    P.dio = dio;
+    P.memo = memo;
+    P.tiny = tiny;
+    P.centred = centred;
+    P.dvals = dvals;
+  }
+};
+
 // Runs one batch call.  Everything from the input upload to the statistic
 // drain is enqueued on the context streams; host work is limited to tables
 // (cached) and launch bookkeeping.
@@ -305,12 +338,22 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   // ---- variables -> device
   const int V = call.va + call.vb;
   const size_t vbytes = sizeof(double) * (size_t)V * n;
+  auto& P = ctx->prep;
+  const bool reuse = opts.reuse_vars != 0;
+  if (reuse) {
+    if (!P.valid || (P.kind == kCross) != (call.kind == kCross) || P.a != call.a || P.b != call.b ||
+        P.va != call.va || P.vb != call.vb || P.n != n || P.B != B || P.dio != dio)
+      throw Failure("reuse_vars: the variables differ from the previous call on this context");
+  } else {
+    P.valid = false;
+  }
   const double* dvals;
-  if (dio && call.kind != kCross) {
+  if (reuse) {
+    dvals = P.dvals;
+  } else if (dio && call.kind != kCross) {
     dvals = call.a;
   } else {
-    double* d = ctx->vals.as<double>();
-    d = static_cast<double*>(ctx->vals.ensure(vbytes));
+    double* d = static_cast<double*>(ctx->vals.ensure(vbytes));
     const cudaMemcpyKind kind = dio ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     CK(cudaMemcpyAsync(d, call.a, sizeof(double) * (size_t)call.va * n, kind, s));
     if (call.kind == kCross)
@@ -318,9 +361,11 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
     dvals = d;
   }
   int* flag = static_cast<int*>(ctx->flag.ensure(sizeof(int)));
-  CK(cudaMemsetAsync(flag, 0, sizeof(int), s));
-  launch_check_finite(dvals, (long long)V * n, flag, s);
-  ++ctx->launches;
+  if (!reuse) {  // a reused set passed this check in the call that prepared it
+    CK(cudaMemsetAsync(flag, 0, sizeof(int), s));
+    launch_check_finite(dvals, (long long)V * n, flag, s);
+    ++ctx->launches;
+  }
 
   VarSet vs;
   vs.vals = dvals;
@@ -334,19 +379,28 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   vs.q = static_cast<uint16_t*>(ctx->q.ensure(sizeof(uint16_t) * (size_t)V * ny * n));
   vs.yhat = static_cast<int*>(ctx->yhat.ensure(sizeof(int) * (size_t)V * ny));
   vs.hq = static_cast<double*>(ctx->hq.ensure(sizeof(double) * (size_t)V * ny));
-  launch_sort_vars(vs, s);
-  launch_equipartition(vs, tb, s);
-  ctx->launches += 2;
+  if (!reuse) {
+    launch_sort_vars(vs, s);
+    launch_equipartition(vs, tb, s);
+    ctx->launches += 2;
+    P.memo = P.tiny = P.centred = false;
+  }
   if (memo) {
     vs.rec = static_cast<uint4*>(ctx->rec.ensure(sizeof(uint4) * 6 * (size_t)V));
-    launch_pack_memo(vs, s);
-    ++ctx->launches;
+    if (!P.memo) {
+      launch_pack_memo(vs, s);
+      ++ctx->launches;
+    }
   } else if (tiny) {
     vs.lw = static_cast<uint8_t*>(ctx->lw.ensure((size_t)V * n));
     vs.rsmask = static_cast<uint32_t*>(ctx->rsmask.ensure(sizeof(uint32_t) * V));
-    launch_pack_tiny(vs, s);
-    ++ctx->launches;
+    if (!P.tiny) {
+      launch_pack_tiny(vs, s);
+      ++ctx->launches;
+    }
   }
+  // what this call leaves prepared (committed once the call succeeds)
+  CtxPrepared done{call, dvals, B, dio, memo || P.memo, tiny || P.tiny};
 
   // ---- pair space
   PairSpace ps;
@@ -376,12 +430,15 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   double* const user_stat[kStats] = {out->mic,   out->mas, out->mev,       out->mcn,
                                      out->mic_e, out->tic, out->pearson_r, out->nonlinearity};
   const bool want_r = out->pearson_r || out->nonlinearity;
-  if (want_r) {  // per-variable centring, once per call
+  if (want_r) {  // per-variable centring, once per variable set
     vs.dx = static_cast<double*>(ctx->dx.ensure(sizeof(double) * (size_t)V * n));
     vs.sxx = static_cast<double*>(ctx->sxx.ensure(sizeof(double) * (size_t)V));
-    launch_center_vars(vs, s);
-    ++ctx->launches;
+    if (!(reuse && P.centred)) {
+      launch_center_vars(vs, s);
+      ++ctx->launches;
+    }
   }
+  done.centred = want_r || (reuse && P.centred);
   const bool small = tiny || memo;  // one thread per pair, stats written directly
   std::vector<YParams> yps;
   for (int y = 2; y <= B / 2; ++y) {
@@ -499,7 +556,10 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
     }
   }
   if (opts.ev_end) CK(cudaEventRecord(static_cast<cudaEvent_t>(opts.ev_end), s));
-  if (dio && opts.async && !opts.counters) return;
+  if (dio && opts.async && !opts.counters) {
+    done.commit(P);
+    return;
+  }
   if (!dio) CK(cudaStreamSynchronize(ctx->copy));
   CK(cudaStreamSynchronize(s));
   if (opts.counters)
@@ -507,6 +567,7 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   int h_flag = 0;
   CK(cudaMemcpy(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost));
   if (h_flag) throw Failure("compute_score: inputs must be finite");
+  done.commit(P);
 }
 
 template <typename F>

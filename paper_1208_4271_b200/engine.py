@@ -51,7 +51,7 @@ class MineOpts(ctypes.Structure):
     _fields_ = [("device_io", ctypes.c_int), ("async_", ctypes.c_int), ("stream", ctypes.c_void_p),
                 ("tier", ctypes.c_int), ("first", ctypes.c_longlong), ("count", ctypes.c_longlong),
                 ("counters", ctypes.POINTER(ctypes.c_ulonglong)), ("ev_begin", ctypes.c_void_p),
-                ("ev_end", ctypes.c_void_p)]
+                ("ev_end", ctypes.c_void_p), ("reuse_vars", ctypes.c_int)]
 
 
 class MineProblem(ctypes.Structure):
@@ -246,27 +246,30 @@ class Engine:
         return res, so
 
     @staticmethod
-    def _opts(first=0, count=0, tier=0) -> MineOpts:
+    def _opts(first=0, count=0, tier=0, reuse_vars=False) -> MineOpts:
         o = MineOpts()
         o.first, o.count, o.tier = int(first), int(count), int(tier)
+        o.reuse_vars = int(bool(reuse_vars))
         return o
 
     # -- batch calls ----------------------------------------------------------
     def pairwise(self, vars_, params: Parameters = Parameters(), first: int = 0, count: int | None = None,
-                 stats=STATS, cells: bool = False, tier: int = 0):
-        """All pairs i<j in PairSequence order (analysis.cpp:66-81)."""
+                 stats=STATS, cells: bool = False, tier: int = 0, reuse_vars: bool = False):
+        """All pairs i<j in PairSequence order (analysis.cpp:66-81).
+        reuse_vars: `vars_` is the same array as in the previous call (e.g. the
+        next window of one job): skip the per-variable stages."""
         v = _f64(vars_)
         p, n = v.shape
         total = p * (p - 1) // 2
         count = total - first if count is None else count
         res, so = self._outputs(count, stats, cells, grid_bound(n, params.alpha))
         self._check(self.L.mine_b200_pairwise(self.ctx, _ptr(v), p, n, ctypes.byref(params._c()),
-                                              ctypes.byref(self._opts(first, count, tier)),
+                                              ctypes.byref(self._opts(first, count, tier, reuse_vars)),
                                               ctypes.byref(so)))
         return res
 
     def cross(self, X, Y, params: Parameters = Parameters(), stats=STATS, cells: bool = False,
-              tier: int = 0, first: int = 0, count: int | None = None):
+              tier: int = 0, first: int = 0, count: int | None = None, reuse_vars: bool = False):
         X, Y = _f64(X), _f64(Y)
         if X.shape[1] != Y.shape[1]:
             raise MineError("compute_score: input lengths differ")
@@ -275,19 +278,41 @@ class Engine:
         res, so = self._outputs(count, stats, cells, grid_bound(X.shape[1], params.alpha))
         self._check(self.L.mine_b200_cross(self.ctx, _ptr(X), X.shape[0], _ptr(Y), Y.shape[0],
                                            X.shape[1], ctypes.byref(params._c()),
-                                           ctypes.byref(self._opts(first, count, tier)),
+                                           ctypes.byref(self._opts(first, count, tier, reuse_vars)),
                                            ctypes.byref(so)))
         return res
 
     def pairs(self, vars_, xi, yi, params: Parameters = Parameters(), stats=STATS,
-              cells: bool = False, tier: int = 0):
+              cells: bool = False, tier: int = 0, reuse_vars: bool = False):
         v = _f64(vars_)
         xi = np.ascontiguousarray(xi, dtype=np.int32)
         yi = np.ascontiguousarray(yi, dtype=np.int32)
         res, so = self._outputs(xi.size, stats, cells, grid_bound(v.shape[1], params.alpha))
         self._check(self.L.mine_b200_pairs(self.ctx, _ptr(v), v.shape[0], v.shape[1], _ptr(xi),
                                            _ptr(yi), xi.size, ctypes.byref(params._c()),
-                                           ctypes.byref(self._opts(0, xi.size, tier)),
+                                           ctypes.byref(self._opts(0, xi.size, tier, reuse_vars)),
+                                           ctypes.byref(so)))
+        return res
+
+    def master_vs_all(self, vars_, master: int, params: Parameters = Parameters(), stats=STATS,
+                      tier: int = 0, reuse_vars: bool = False):
+        """AnalysisMode::master_vs_all (analysis.cpp:25-30, PairSequence::at
+        :82-85): the pairs (master, j) for every j != master in index order,
+        each oriented lower index first (score_pair, :117-129).  `master` is
+        0-based here.  With reuse_vars=True over the same `vars_` array, the
+        per-variable stages run once for a whole sweep of masters (SURVEY 8f
+        rank 1)."""
+        v = _f64(vars_)
+        p = v.shape[0]
+        if not 0 <= master < p:
+            raise MineError("expand_pairs: master index out of range")
+        others = np.array([j for j in range(p) if j != master], dtype=np.int32)
+        xi = np.minimum(others, master).astype(np.int32)
+        yi = np.maximum(others, master).astype(np.int32)
+        res, so = self._outputs(xi.size, stats, False, grid_bound(v.shape[1], params.alpha))
+        self._check(self.L.mine_b200_pairs(self.ctx, _ptr(v), p, v.shape[1], _ptr(xi), _ptr(yi),
+                                           xi.size, ctypes.byref(params._c()),
+                                           ctypes.byref(self._opts(0, xi.size, tier, reuse_vars)),
                                            ctypes.byref(so)))
         return res
 

@@ -7,7 +7,8 @@ import pytest
 
 from conftest import bits, random_pair
 
-from paper_1208_4271_b200 import MIC_E, Parameters, cell_shapes, datagen, grid_bound
+from paper_1208_4271_b200 import (ALL_STATS, MIC_E, MineError, Parameters, cell_shapes, datagen,
+                                  grid_bound)
 
 pytestmark = pytest.mark.gpu
 
@@ -216,6 +217,31 @@ def test_golden_pearson_gpu(engine):
     # non-linearity alone (MIC computed internally), and the general tier
     r2 = engine.pairwise(c["c1_vars"], stats=("nonlinearity",), tier=2)
     assert _same(r2["nonlinearity"], c["c1_stats6"][:, 5])
+
+
+def test_reuse_vars_and_master_vs_all(engine, oracle):
+    """windows of one job with the per-variable stages run
+    once (reuse_vars), and master_vs_all (analysis.cpp:25-30,82-85) -- both
+    bit-identical to the single full call / the oracle, and a reuse request
+    with different variables fails instead of scoring stale state."""
+    w = datagen.make(1)
+    V = np.ascontiguousarray(w.X[:80])
+    full = engine.pairwise(V, stats=ALL_STATS)
+    total = 80 * 79 // 2
+    parts = [engine.pairwise(V, first=0, count=1000, stats=ALL_STATS)]
+    for first in range(1000, total, 1000):
+        parts.append(engine.pairwise(V, first=first, count=min(1000, total - first),
+                                     stats=ALL_STATS, reuse_vars=True))
+    for k in ALL_STATS:
+        assert _same(np.concatenate([p[k] for p in parts]), full[k]), k
+    for tier in (0, 2):
+        for m in (0, 37, 79):
+            got = engine.master_vs_all(V, m, tier=tier, reuse_vars=(m != 0))
+            others = [j for j in range(80) if j != m]
+            want = oracle.pairs(V, np.minimum(others, m), np.maximum(others, m))
+            assert_bit_equal(stats_matrix(got), want[:, :6], f"master {m} tier {tier}")
+    with pytest.raises(MineError):
+        engine.pairwise(np.ascontiguousarray(w.X[:81]), reuse_vars=True)
 
 
 # --- config-scale parity and size-independent properties ---------------------
