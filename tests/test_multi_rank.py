@@ -21,7 +21,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, V, result_path):
+def _worker(rank, world, port, V, result_path, strategy="range", chunk=4096):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import torch.distributed as dist
@@ -38,7 +38,7 @@ def _worker(rank, world, port, V, result_path):
         out = orc.pairwise(V, first=first, count=count, threads=1)
         return {k: out[:, i] for i, k in enumerate(("mic", "mas", "mev", "mcn", "mic_e", "tic"))}
 
-    full = sharding.score_sharded(score_range, total, dist)
+    full = sharding.score_sharded(score_range, total, dist, strategy=strategy, chunk=chunk)
     if rank == 0:
         np.save(result_path, np.stack([full[k] for k in ("mic", "mas", "mev", "mcn", "mic_e", "tic")], 1))
     dist.barrier()
@@ -56,3 +56,27 @@ def test_sharded_pairwise_equals_single_rank(tmp_path, oracle, world):
     want = oracle.pairwise(V, threads=1)
     assert got.shape == want.shape
     assert np.array_equal(got.view(np.int64), want.view(np.int64))
+
+
+@pytest.mark.parametrize("chunk", [7, 64, 1000])
+def test_cyclic_sharding_equals_single_rank(tmp_path, oracle, chunk):
+    """SURVEY 8e balance: round-robin chunks (incl. a rank with fewer chunks
+    and, at chunk=1000 > 253 pairs, a rank with none) re-interleave exactly."""
+    rng = np.random.default_rng(6)
+    V = rng.normal(size=(23, 23))
+    V[7] = np.repeat(np.arange(5.0), 5)[:23]
+    path = str(tmp_path / "res.npy")
+    mp.spawn(_worker, args=(2, _free_port(), V, path, "cyclic", chunk), nprocs=2, join=True)
+    got = np.load(path)
+    want = oracle.pairwise(V, threads=1)
+    assert np.array_equal(got.view(np.int64), want.view(np.int64))
+
+
+def test_shard_chunks_cover_exactly_once():
+    from paper_1208_4271_b200 import sharding
+    for total, world, chunk in [(0, 3, 5), (1, 4, 2), (253, 2, 7), (4096, 8, 64), (10, 3, 100)]:
+        seen = np.zeros(total, int)
+        for r in range(world):
+            for f, c in sharding.shard_chunks(total, world, r, chunk):
+                seen[f:f + c] += 1
+        assert (seen == 1).all()
