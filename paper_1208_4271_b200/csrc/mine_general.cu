@@ -147,25 +147,45 @@ __global__ void __launch_bounds__(kPfThreads) k_part_f2(VarSet vs, Tables tb, Pa
     cb[kraw] = n;
   }
   __syncthreads();
-  // --- Alg. 2 (partition.cpp:148-165): equipartition the clump ordinals
+  // --- Alg. 2 (partition.cpp:148-165): equipartition the clump ordinals.
+  // The greedy scan (equipartition_runs, partition.cpp:42-67) closes the
+  // current group before clump j iff |in_row + run_j - desired| >=
+  // |in_row - desired|.  For a group starting at clump i0, in_row = cb[j] -
+  // cb[i0] grows with j, so that test is false ... false, true ... true
+  // (also in FP64: the integers are exact and rounding is monotone).  Warp 0
+  // therefore tests 32 clumps per step and takes the first true one (ballot):
+  // the same group boundaries as the sequential scan, in ~k/32 + groups steps.
   int k = kraw;
   if (kraw > k_hat) {
-    if (tid == 0) {
+    if (warp == 0) {
       double desired = (double)n / (double)k_hat;
-      int curr = 1, in_row = 0;
-      for (int j = 0; j < kraw; ++j) {
-        const int i = cb[j], run = cb[j + 1] - i;
-        if (in_row != 0 &&
-            fabs((double)(in_row + run) - desired) >= fabs((double)in_row - desired)) {
-          ++curr;
-          in_row = 0;
-          desired = (double)(n - i) / (double)(k_hat - curr + 1);
-          cb[curr - 1] = i;  // in place: curr - 1 <= j
+      int curr = 1, i0 = 0, j = 1;
+      while (j < kraw) {
+        const int jj = j + lane;
+        bool close = false;
+        if (jj < kraw) {
+          const int in_row = cb[jj] - cb[i0], run = cb[jj + 1] - cb[jj];
+          close = fabs((double)(in_row + run) - desired) >= fabs((double)in_row - desired);
         }
-        in_row += run;
+        const unsigned m = __ballot_sync(0xffffffffu, close);
+        if (m) {
+          const int jc = j + __ffs(m) - 1;  // the next group starts at clump jc
+          const int i = cb[jc];
+          ++curr;
+          desired = (double)(n - i) / (double)(k_hat - curr + 1);
+          __syncwarp();
+          if (lane == 0) cb[curr - 1] = i;  // in place: curr - 1 <= jc, and cb[jc] keeps its value
+          __syncwarp();
+          i0 = jc;
+          j = jc + 1;
+        } else {
+          j += 32;
+        }
       }
-      cb[curr] = n;
-      misc[40] = curr;
+      if (lane == 0) {
+        cb[curr] = n;
+        misc[40] = curr;
+      }
     }
     __syncthreads();
     k = misc[40];
