@@ -63,8 +63,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if force or not _newer(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lpthread"])
     probe_src = os.path.join(CSRC, "probes.cu")
-    if force or not _newer(PROBES, [probe_src]):
-        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+    if force or not _newer(PROBES, [probe_src] + [os.path.normpath(os.path.join(CSRC, h)) for h in HEADERS]):
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
               "-cudart", "static", "-o", PROBES, probe_src])
     return LIB
 

@@ -135,4 +135,18 @@ __device__ __forceinline__ double norm_cell(double I, double logl, double logy) 
   return 0.0 < v ? v : 0.0;
 }
 
+// Correctly rounded a / b for integers 0 <= a <= b <= 65535 (the span-term
+// quotients c_s/c_t and (c_t - c_s)/c_t, mutual_info.cpp:62) from
+// rcp = __drcp_rn(b), computed once per b: q0 = a*rcp, r = a - q0*b (exact
+// with one FMA), q = q0 + r*rcp (Markstein's correction).  Bitwise equal to
+// __ddiv_rn(a, b), i.e. to the reference's IEEE division, on the whole domain:
+// checked exhaustively (all 2.1e9 pairs) by probes.cu
+// mine_b200_check_quotients (tests/test_gpu_parity.py).  Three FP64 ops
+// instead of a DDIV sequence.
+__device__ __forceinline__ double int_quot(double a, double b, double rcp) {
+  const double q0 = __dmul_rn(a, rcp);
+  const double r = __fma_rn(-q0, b, a);
+  return __fma_rn(r, rcp, q0);
+}
+
 }  // namespace mb200

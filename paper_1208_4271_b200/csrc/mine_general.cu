@@ -330,29 +330,31 @@ __device__ __forceinline__ void span_terms(const Tables& tb, const int* cb, cons
                                            int rows, int k, int s0, int ns, int t0, int nt,
                                            double* A, double* W) {
   const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  // a lane keeps one t (nt <= 32): c_t and its reciprocal once per call
+  const int tl = lane, t = t0 + tl;
+  if (tl >= nt || t > k) return;
+  const int ct = cb[t];
+  const double dct = (double)ct, rct = __drcp_rn(dct);
   for (int sl = threadIdx.x >> 5; sl < ns; sl += nw) {
-    const int s = s0 + sl, cs = cb[s];
-    for (int tl = lane; tl < nt; tl += 32) {
-      const int t = t0 + tl;
-      if (s >= t || t > k) continue;
-      const int ct = cb[t];
-      const double* plm = tb.pl + tri(ct - cs);
-      double acch = 0.0;
-      for (int r = 0; r < rows; ++r)
-        acch = __dadd_rn(acch, __ldg(plm + (cum[r * kk + t] - cum[r * kk + s])));
-      double a, q;
-      if (tb.div) {
-        const double* dr = tb.div + tri(ct);
-        a = __ldg(dr + cs);
-        q = __ldg(dr + (ct - cs));
-      } else {
-        const double dcs = (double)cs, dct = (double)ct;
-        a = __ddiv_rn(dcs, dct);
-        q = __ddiv_rn(__dsub_rn(dct, dcs), dct);
-      }
-      A[sl * kMaxTile + tl] = a;
-      W[sl * kMaxTile + tl] = __dmul_rn(q, -acch);
+    const int s = s0 + sl;
+    if (s >= t) continue;
+    const int cs = cb[s];
+    const double* plm = tb.pl + tri(ct - cs);
+    double acch = 0.0;
+    for (int r = 0; r < rows; ++r)
+      acch = __dadd_rn(acch, __ldg(plm + (cum[r * kk + t] - cum[r * kk + s])));
+    double a, q;
+    if (tb.div) {
+      const double* dr = tb.div + tri(ct);
+      a = __ldg(dr + cs);
+      q = __ldg(dr + (ct - cs));
+    } else {
+      const double dcs = (double)cs;
+      a = int_quot(dcs, dct, rct);
+      q = int_quot(__dsub_rn(dct, dcs), dct, rct);
     }
+    A[sl * kMaxTile + tl] = a;
+    W[sl * kMaxTile + tl] = __dmul_rn(q, -acch);
   }
 }
 
@@ -581,6 +583,7 @@ __global__ void __launch_bounds__(kWarpThreads) k_dp_warp(VarSet vs, Tables tb, 
     for (int t = 3; t <= k; ++t) {
       // span column A(s,t), W(s,t) for s in [2, t)
       const int ct = cb[t];
+      const double dct = (double)ct, rct = __drcp_rn(dct);
       for (int s = 2 + lane; s < t; s += 32) {
         const int cs = cb[s];
         const double* plm = tb.pl + tri(ct - cs);
@@ -593,9 +596,9 @@ __global__ void __launch_bounds__(kWarpThreads) k_dp_warp(VarSet vs, Tables tb, 
           a = __ldg(dr + cs);
           q = __ldg(dr + (ct - cs));
         } else {
-          const double dcs = (double)cs, dct = (double)ct;
-          a = __ddiv_rn(dcs, dct);
-          q = __ddiv_rn(__dsub_rn(dct, dcs), dct);
+          const double dcs = (double)cs;
+          a = int_quot(dcs, dct, rct);
+          q = int_quot(__dsub_rn(dct, dcs), dct, rct);
         }
         A[s] = a;
         W[s] = __dmul_rn(q, -acch);

@@ -255,8 +255,9 @@ __device__ void tiny_subproblem(const TinyCtx& c, const uint32_t* m, int rows, u
 #pragma unroll
           for (int r = 0; r < 3; ++r)
             if (r < rows) acch = __dadd_rn(acch, PLs(c, mm, __popc(m[r] & tail)));
-          const double r1 = __ddiv_rn((double)t, (double)n);
-          const double wv = __dmul_rn(__ddiv_rn(__dsub_rn((double)n, (double)t), (double)n), -acch);
+          const double dn = (double)n, rn = __drcp_rn(dn);
+          const double r1 = int_quot((double)t, dn, rn);
+          const double wv = __dmul_rn(int_quot(__dsub_rn(dn, (double)t), dn, rn), -acch);
           best3 = dmax(best3, __dsub_rn(__dmul_rn(r1, f2), wv));
         } else {
           f2k = f2;

@@ -6,6 +6,8 @@
 
 #include <cstdint>
 
+#include "device_common.cuh"  // mb200::int_quot, the engine's quotient
+
 namespace {
 
 constexpr int kChains = 8;
@@ -67,6 +69,22 @@ __global__ void k_lds2(int* out, int iters, int key) {
   if (s == key) out[0] = s;  // key < 0 at run time: never true, not provable
 }
 
+// Exhaustive check of the engine's integer quotient (device_common.cuh
+// int_quot) against IEEE division: every 0 <= a <= b, 1 <= b <= nmax.
+__global__ void k_check_quot(int nmax, unsigned long long* out) {
+  unsigned long long bad = 0, cnt = 0;
+  for (int b = blockIdx.x + 1; b <= nmax; b += gridDim.x) {
+    const double db = (double)b, rcp = __drcp_rn(db);
+    for (int a = threadIdx.x; a <= b; a += blockDim.x) {
+      const double da = (double)a;
+      bad += __double_as_longlong(mb200::int_quot(da, db, rcp)) != __double_as_longlong(__ddiv_rn(da, db));
+      ++cnt;
+    }
+  }
+  atomicAdd(out, bad);
+  atomicAdd(out + 1, cnt);
+}
+
 template <typename F>
 float time_ms(F&& launch) {
   cudaEvent_t a, b;
@@ -104,5 +122,20 @@ extern "C" int mine_b200_probe(int device, double* dadd_per_s, double* lds_per_s
   ms = time_ms([&] { k_lds2<<<b2, 512, sm2>>>(reinterpret_cast<int*>(out), liters, -1); });
   *lds2_per_s = (double)b2 * 512 * liters * kChains / (ms * 1e-3);
   cudaFree(out);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+extern "C" int mine_b200_check_quotients(int device, int nmax, unsigned long long* mismatches,
+                                         unsigned long long* checked) {
+  if (cudaSetDevice(device) != cudaSuccess) return -1;
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, 2 * sizeof(unsigned long long)) != cudaSuccess) return -1;
+  cudaMemset(d, 0, 2 * sizeof(unsigned long long));
+  k_check_quot<<<4096, 256>>>(nmax, d);
+  unsigned long long h[2] = {0, 0};
+  cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  *mismatches = h[0];
+  *checked = h[1];
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }

@@ -364,3 +364,17 @@ def test_c4_full_size_properties(engine):
         assert_bit_equal(a[k], c[k], f"c4 swap {k}")
     assert np.all((a["mic"] >= 0) & (a["mic"] <= 1)) and np.all(a["mas"] <= a["mic"])
     assert a["mic"][0] > 0.9  # near-noiseless linear relation
+
+
+def test_span_quotients_match_ieee_division_exhaustively():
+    """The engine's span-term quotients c_s/c_t (mutual_info.cpp:62) use one
+    reciprocal per c_t plus a Markstein correction (device_common.cuh
+    int_quot) instead of a DDIV: bitwise equal to IEEE a/b for EVERY
+    0 <= a <= b <= 65535 (the whole supported n), checked here on the GPU."""
+    import ctypes
+    from paper_1208_4271_b200 import _build
+    L = ctypes.CDLL(_build.PROBES)
+    bad, cnt = ctypes.c_ulonglong(0), ctypes.c_ulonglong(0)
+    assert L.mine_b200_check_quotients(0, 65535, ctypes.byref(bad), ctypes.byref(cnt)) == 0
+    assert cnt.value == 65536 * 65537 // 2 - 1
+    assert bad.value == 0
