@@ -335,26 +335,51 @@ __device__ __forceinline__ void span_terms(const Tables& tb, const int* cb, cons
   if (tl >= nt || t > k) return;
   const int ct = cb[t];
   const double dct = (double)ct, rct = __drcp_rn(dct);
-  for (int sl = threadIdx.x >> 5; sl < ns; sl += nw) {
-    const int s = s0 + sl;
-    if (s >= t) continue;
-    const int cs = cb[s];
-    const double* plm = tb.pl + tri(ct - cs);
-    double acch = 0.0;
-    for (int r = 0; r < rows; ++r)
-      acch = __dadd_rn(acch, __ldg(plm + (cum[r * kk + t] - cum[r * kk + s])));
-    double a, q;
-    if (tb.div) {
-      const double* dr = tb.div + tri(ct);
-      a = __ldg(dr + cs);
-      q = __ldg(dr + (ct - cs));
-    } else {
-      const double dcs = (double)cs;
-      a = int_quot(dcs, dct, rct);
-      q = int_quot(__dsub_rn(dct, dcs), dct, rct);
+  // four rows s per pass with interleaved row sums: their L2 gathers of the
+  // p*log(p) table are in flight together (each sum keeps the reference's
+  // row order)
+  const int w0 = threadIdx.x >> 5;
+  for (int base = 0; base < ns; base += 4 * nw) {
+    int cs[4];
+    const double* plm[4];
+    bool ok[4];
+    double acch[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int sl = base + w0 + e * nw, s = s0 + sl;
+      ok[e] = sl < ns && s < t;
+      cs[e] = ok[e] ? cb[s] : ct;
+      plm[e] = tb.pl + tri(ct - cs[e]);
+      acch[e] = 0.0;
     }
-    A[sl * kMaxTile + tl] = a;
-    W[sl * kMaxTile + tl] = __dmul_rn(q, -acch);
+    for (int r = 0; r < rows; ++r) {
+      const int ctr = cum[r * kk + t];
+      double v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int s = s0 + base + w0 + e * nw;
+        v[e] = ok[e] ? __ldg(plm[e] + (ctr - cum[r * kk + s])) : 0.0;
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acch[e] = __dadd_rn(acch[e], v[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (!ok[e]) continue;
+      const int sl = base + w0 + e * nw;
+      double a, q;
+      if (tb.div) {
+        const double* dr = tb.div + tri(ct);
+        a = __ldg(dr + cs[e]);
+        q = __ldg(dr + (ct - cs[e]));
+      } else {
+        const double dcs = (double)cs[e];
+        a = int_quot(dcs, dct, rct);
+        q = int_quot(__dsub_rn(dct, dcs), dct, rct);
+      }
+      A[sl * kMaxTile + tl] = a;
+      W[sl * kMaxTile + tl] = __dmul_rn(q, -acch[e]);
+    }
   }
 }
 
