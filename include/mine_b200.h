@@ -192,6 +192,40 @@ mine_cstats* mine_compute_cstats(mine_matrix* X, mine_matrix* Y, mine_parameter*
 void mine_free_pstats(mine_pstats** p);
 void mine_free_cstats(mine_cstats** c);
 
+/* ---- analysis front end (io.cpp, analysis.cpp) ----- */
+/* A dataset as read_dataset builds it (io.cpp:48-120): p variables x n
+ * samples, variable-major values, labels with duplicates suffixed. */
+typedef struct mine_b200_dataset {
+  int p;
+  int n;
+  double* values; /* p x n */
+  char** names;   /* p NUL-terminated labels */
+} mine_b200_dataset;
+
+/* AnalysisTask (analysis.hpp:27-35). */
+typedef struct mine_b200_task {
+  int mode;                 /* 0 all_pairs, 1 master_vs_all, 2 single_pair */
+  int master, first, second; /* 1-based variable indices */
+  double alpha, c;          /* Parameters */
+  int has_min_variance;     /* apply filter_low_variance(min_variance) first */
+  double min_variance;
+  int workers;              /* host threads formatting records (>= 1) */
+} mine_b200_task;
+
+/* read_dataset: 0 / -1 (message: mine_b200_last_error, as io.cpp throws). */
+int mine_b200_read_dataset(const char* path, mine_b200_dataset** out);
+void mine_b200_free_dataset(mine_b200_dataset* ds);
+/* Sample variance of each variable on the GPU (analysis.cpp:98-100). */
+int mine_b200_variances(mine_b200_ctx* ctx, const double* vars, int p, int n, double* var_out);
+/* filter_low_variance (analysis.cpp:92-113): a new dataset of the kept variables. */
+int mine_b200_filter_low_variance(mine_b200_ctx* ctx, const mine_b200_dataset* in,
+                                  double threshold, mine_b200_dataset** out);
+/* run_analysis + write_results (analysis.cpp:133-191, io.cpp:122-154): the
+ * header and one format_record line per pair of the task, written through
+ * "<out_path>.tmp" renamed into place.  Returns the record count, or -1. */
+long long mine_b200_run_analysis(mine_b200_ctx* ctx, const mine_b200_dataset* ds,
+                                 const mine_b200_task* task, const char* out_path);
+
 #ifdef __cplusplus
 }
 #endif

@@ -212,6 +212,12 @@ class Reference:
         L.ref_brute_force.argtypes = [_ip, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp,
                                       ctypes.POINTER(ctypes.c_longlong)]
         L.ref_entropy.argtypes = [_dp, ctypes.c_int, _dp]
+        L.ref_analysis_file.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                        ctypes.c_double, ctypes.c_uint, ctypes.POINTER(ctypes.c_long)]
+        L.ref_read_dataset.argtypes = [ctypes.c_char_p, _ip, _ip, _dp, ctypes.c_long, ctypes.c_char_p,
+                                       ctypes.c_long]
+        L.ref_filter_low_variance.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_double, _ip, _ip]
         self.L = L
 
     def _check(self, rc):
@@ -303,3 +309,41 @@ class Reference:
         out = np.zeros(1)
         self._check(self.L.ref_entropy(_d(w), w.size, _d(out)))
         return float(out[0])
+
+
+def _ref_methods():
+    """File-level front end of the reference (io.cpp / analysis.cpp)."""
+
+    def analysis_file(self, in_path, out_path, mode=0, a=0, b=0, alpha=0.6, c=15.0,
+                      min_variance=None, workers=4):
+        """read_dataset -> run_analysis -> ResultWriter, as run_cli does."""
+        rec = ctypes.c_long(0)
+        self._check(self.L.ref_analysis_file(str(in_path).encode(), str(out_path).encode(), mode, a, b,
+                                             alpha, c, -1.0 if min_variance is None else min_variance,
+                                             workers, ctypes.byref(rec)))
+        return rec.value
+
+    def read_dataset(self, path):
+        p, n = np.zeros(1, np.int32), np.zeros(1, np.int32)
+        self._check(self.L.ref_read_dataset(str(path).encode(), _i(p), _i(n), None, 0, None, 0))
+        vals = np.zeros(int(p[0]) * int(n[0]))
+        buf = ctypes.create_string_buffer(1 << 22)
+        self._check(self.L.ref_read_dataset(str(path).encode(), _i(p), _i(n), _d(vals), vals.size,
+                                            buf, len(buf)))
+        names = buf.value.decode().split("\n")[:-1]
+        return names, vals.reshape(int(p[0]), int(n[0]))
+
+    def filter_low_variance(self, values, threshold):
+        v = _f64(values)
+        keep = np.zeros(v.shape[0], np.int32)
+        nk = np.zeros(1, np.int32)
+        self._check(self.L.ref_filter_low_variance(_d(v), v.shape[0], v.shape[1], threshold,
+                                                   _i(keep), _i(nk)))
+        return keep[: int(nk[0])]
+
+    Reference.analysis_file = analysis_file
+    Reference.read_dataset = read_dataset
+    Reference.filter_low_variance = filter_low_variance
+
+
+_ref_methods()

@@ -13,6 +13,7 @@
 
 #include "mine/analysis.hpp"
 #include "mine/char_matrix.hpp"
+#include "mine/io.hpp"
 #include "mine/mutual_info.hpp"
 #include "mine/oracle.hpp"
 #include "mine/partition.hpp"
@@ -135,6 +136,68 @@ int ref_run_analysis(const double* values, int p, int n, int mode, int a, int b,
       ++w;
     });
     *records = w;
+  });
+}
+
+// The reference's file-to-file batch path (what run_cli does after parsing,
+// cli.cpp:108-118): read_dataset -> run_analysis (optional variance filter)
+// -> ResultWriter.  mode / a / b as ref_run_analysis; min_variance < 0: none.
+int ref_analysis_file(const char* in_path, const char* out_path, int mode, int a, int b,
+                      double alpha, double c, double min_variance, unsigned workers, long* records) {
+  return guarded([&] {
+    const Dataset ds = read_dataset(in_path);
+    AnalysisTask task;
+    task.mode = mode == 0 ? AnalysisMode::all_pairs
+                          : (mode == 1 ? AnalysisMode::master_vs_all : AnalysisMode::single_pair);
+    task.master = a;
+    task.first = a;
+    task.second = b;
+    task.params = Parameters{alpha, c};
+    task.workers = workers;
+    if (min_variance >= 0.0) task.min_variance = min_variance;
+    ResultWriter writer(out_path);
+    long w = 0;
+    run_analysis(ds, task, [&](const ResultRecord& rec) {
+      writer.write(rec);
+      ++w;
+    });
+    writer.close();
+    *records = w;
+  });
+}
+
+// read_dataset (io.cpp:48-120): dimensions, then values (variable-major) and
+// the '\n'-joined names.
+int ref_read_dataset(const char* path, int* p, int* n, double* values, long cap_values,
+                     char* names, long cap_names) {
+  return guarded([&] {
+    const Dataset ds = read_dataset(path);
+    *p = static_cast<int>(ds.p());
+    *n = static_cast<int>(ds.n());
+    if (values && cap_values >= static_cast<long>(ds.p() * ds.n()))
+      for (long j = 0; j < ds.p(); ++j)
+        for (long i = 0; i < ds.n(); ++i) values[j * ds.n() + i] = ds.values(i, j);
+    std::string joined;
+    for (const auto& nm : ds.names) joined += nm + "\n";
+    if (names && cap_names > static_cast<long>(joined.size()))
+      std::memcpy(names, joined.c_str(), joined.size() + 1);
+  });
+}
+
+// filter_low_variance (analysis.cpp:92-113) on a variable-major matrix: the
+// kept variable indices (0-based) in keep[], their count in *nkeep.
+int ref_filter_low_variance(const double* values, int p, int n, double threshold, int* keep,
+                            int* nkeep) {
+  return guarded([&] {
+    Dataset ds;
+    ds.values.resize(n, p);
+    for (int j = 0; j < p; ++j) {
+      ds.names.push_back(std::to_string(j));
+      for (int i = 0; i < n; ++i) ds.values(i, j) = values[static_cast<long>(j) * n + i];
+    }
+    const Dataset out = filter_low_variance(ds, threshold);
+    *nkeep = static_cast<int>(out.p());
+    for (int j = 0; j < out.p(); ++j) keep[j] = std::stoi(out.names[static_cast<std::size_t>(j)]);
   });
 }
 

@@ -24,7 +24,7 @@ CUDA_INC = "/usr/local/cuda/include"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 KERNEL_SRCS = ["mine_kernels.cu", "mine_general.cu", "pearson.cu"]
-HOST_SRCS = ["engine.cpp"]
+HOST_SRCS = ["engine.cpp", "records.cpp"]
 HEADERS = ["mine_kernels.h", "device_common.cuh", os.path.join("..", "..", "include", "mine_b200.h")]
 
 

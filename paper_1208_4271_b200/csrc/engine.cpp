@@ -595,6 +595,12 @@ mine_b200_ctx* default_ctx() {
 }  // namespace
 
 // ===========================================================================
+namespace mb200 {
+// for the host front end (records.cpp): the thread-local message the C ABI
+// reports through mine_b200_last_error
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace mb200
+
 extern "C" {
 
 const char* mine_b200_last_error(void) { return g_err.c_str(); }
@@ -675,6 +681,32 @@ int mine_b200_pairs(mine_b200_ctx* ctx, const double* vars, int nvars, int n, co
     std::lock_guard<std::mutex> lk(ctx->mu);
     Call call{kList, vars, nullptr, nvars, 0, n, xi, yi, npairs};
     run_call(ctx, call, param, opts, out);
+  });
+}
+
+int mine_b200_variances(mine_b200_ctx* ctx, const double* vars, int p, int n, double* var_out) {
+  return guarded([&] {
+    if (!ctx) throw Failure("mine_b200: null context");
+    if (p < 0 || n < 2) throw Failure("mine_b200_variances: need p >= 0 and n >= 2");
+    if (p == 0) return;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    ctx->prep.valid = false;  // the variable buffers are reused below
+    VarSet vs;
+    vs.V = p;
+    vs.n = n;
+    double* d = static_cast<double*>(ctx->vals.ensure(sizeof(double) * (size_t)p * n));
+    CK(cudaMemcpyAsync(d, vars, sizeof(double) * (size_t)p * n, cudaMemcpyHostToDevice, s));
+    vs.vals = d;
+    vs.dx = static_cast<double*>(ctx->dx.ensure(sizeof(double) * (size_t)p * n));
+    vs.sxx = static_cast<double*>(ctx->sxx.ensure(sizeof(double) * (size_t)p));
+    double* var = static_cast<double*>(ctx->micscr.ensure(sizeof(double) * (size_t)p));
+    launch_center_vars(vs, s);
+    launch_variances(vs, var, s);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(var_out, var, sizeof(double) * (size_t)p, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
   });
 }
 

@@ -174,6 +174,8 @@ void launch_reduce(const Tables& tb, long long npairs, const double* ocells, int
 
 // Pearson r / non-linearity (pearson.cu, statistics.cpp:39-51).
 void launch_center_vars(const VarSet& vs, cudaStream_t s);
+// filter_low_variance's per-variable variance (analysis.cpp:98-100), after launch_center_vars
+void launch_variances(const VarSet& vs, double* var, cudaStream_t s);
 void launch_pearson_pairs(const VarSet& vs, const PairSpace& ps, const double* mic,
                           double* pearson, double* nonlin, cudaStream_t s);
 

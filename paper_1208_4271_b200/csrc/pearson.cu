@@ -66,7 +66,17 @@ __global__ void k_pearson_pairs(VarSet vs, PairSpace ps, const double* __restric
   if (nonlin) nonlin[w] = __dsub_rn(mic[w], __dmul_rn(r, r));
 }
 
+// analysis.cpp:98-100: sample variance = sum((x - mean)^2) / (n - 1)
+__global__ void k_variances(VarSet vs, double* var) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < vs.V) var[v] = __ddiv_rn(vs.sxx[v], (double)(vs.n - 1));
+}
+
 }  // namespace
+
+void launch_variances(const VarSet& vs, double* var, cudaStream_t s) {
+  k_variances<<<(vs.V + 127) / 128, 128, 0, s>>>(vs, var);
+}
 
 void launch_center_vars(const VarSet& vs, cudaStream_t s) {
   k_center_vars<<<(vs.V + 127) / 128, 128, 0, s>>>(vs);

@@ -1,0 +1,361 @@
+// Analysis front end around the GPU batch path:
+//   * read_dataset (io.cpp:48-120): the comma-delimited dataset, same
+//     validation, messages and duplicate-label suffixing;
+//   * filter_low_variance (analysis.cpp:92-113) with the variances computed on
+//     the GPU (pearson.cu k_center_vars / k_variances);
+//   * run_analysis + ResultWriter (analysis.cpp:133-191, io.cpp:122-154): the
+//     pair sequence of an AnalysisTask scored on the GPU in blocks (per-variable
+//     stages once per job: reuse_vars), every record formatted exactly like
+//     format_record (io.cpp:17-47: "%.6g", "nan") by `workers` host threads,
+//     written through a temporary file renamed into place on success.
+// Host C++ only; it calls the engine through the public C ABI.
+#include <algorithm>
+#include <charconv>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <filesystem>
+#include <fstream>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <system_error>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "mine_b200.h"
+
+namespace mb200 {
+void set_last_error(const std::string& msg);
+}
+
+namespace {
+
+template <typename F>
+auto guarded(F&& f, decltype(f()) on_error) -> decltype(f()) {
+  try {
+    return f();
+  } catch (const std::exception& e) {
+    mb200::set_last_error(e.what());
+    return on_error;
+  }
+}
+
+std::string_view trim(std::string_view s) {
+  while (!s.empty() && (s.front() == ' ' || s.front() == '\t')) s.remove_prefix(1);
+  while (!s.empty() && (s.back() == ' ' || s.back() == '\t')) s.remove_suffix(1);
+  return s;
+}
+
+[[noreturn]] void fail_line(const std::string& path, size_t line_no, const std::string& what) {
+  throw std::runtime_error(path + ": line " + std::to_string(line_no) + ": " + what);
+}
+
+mine_b200_dataset* new_dataset(int p, int n, std::vector<double>&& values,
+                               const std::vector<std::string>& names) {
+  auto* ds = new mine_b200_dataset{};
+  ds->p = p;
+  ds->n = n;
+  ds->values = new double[(size_t)p * n];
+  std::copy(values.begin(), values.end(), ds->values);
+  ds->names = new char*[(size_t)p];
+  for (int j = 0; j < p; ++j) {
+    ds->names[j] = new char[names[j].size() + 1];
+    std::memcpy(ds->names[j], names[j].c_str(), names[j].size() + 1);
+  }
+  return ds;
+}
+
+// io.cpp:48-120
+mine_b200_dataset* read_dataset(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw std::runtime_error(path + ": cannot open for reading");
+  std::vector<std::string> names;
+  std::vector<double> values;  // row after row == variable-major
+  long long n = -1;
+  std::string line;
+  size_t line_no = 0;
+  while (std::getline(in, line)) {
+    ++line_no;
+    if (!line.empty() && line.back() == '\r') line.pop_back();
+    if (line.empty()) continue;
+    std::vector<std::string_view> fields;
+    std::string_view rest = line;
+    while (true) {
+      const size_t comma = rest.find(',');
+      fields.push_back(rest.substr(0, comma));
+      if (comma == std::string_view::npos) break;
+      rest.remove_prefix(comma + 1);
+    }
+    if (fields.size() < 2) fail_line(path, line_no, "expected a label followed by at least one value");
+    if (n == -1)
+      n = (long long)fields.size() - 1;
+    else if ((long long)fields.size() - 1 != n)
+      fail_line(path, line_no,
+                "expected " + std::to_string(n) + " values, got " + std::to_string(fields.size() - 1));
+    const std::string_view label = trim(fields[0]);
+    if (label.empty()) fail_line(path, line_no, "empty variable label");
+    names.emplace_back(label);
+    for (size_t f = 1; f < fields.size(); ++f) {
+      const std::string_view tok = trim(fields[f]);
+      double v = 0.0;
+      const auto [ptr, ec] = std::from_chars(tok.data(), tok.data() + tok.size(), v);
+      if (ec != std::errc{} || ptr != tok.data() + tok.size() || !std::isfinite(v))
+        fail_line(path, line_no,
+                  "field " + std::to_string(f + 1) + ": cannot parse '" + std::string(tok) +
+                      "' as a finite number");
+      values.push_back(v);
+    }
+  }
+  if (names.empty()) throw std::runtime_error(path + ": no variables found");
+  if (n < 2) throw std::runtime_error(path + ": need at least 2 samples per variable");
+  // duplicate labels get an occurrence suffix (io.cpp:101-113)
+  std::unordered_map<std::string, int> seen;
+  for (auto& name : names) {
+    int& count = seen[name];
+    ++count;
+    if (count > 1) {
+      int suffix = count;
+      std::string candidate = name + "_" + std::to_string(suffix);
+      while (seen.count(candidate)) candidate = name + "_" + std::to_string(++suffix);
+      seen[candidate] = 1;
+      name = candidate;
+    }
+  }
+  return new_dataset((int)names.size(), (int)n, std::move(values), names);
+}
+
+// analysis.cpp:92-113, variances on the GPU
+mine_b200_dataset* filter_low_variance(mine_b200_ctx* ctx, const mine_b200_dataset* in,
+                                       double threshold) {
+  if (threshold < 0.0) throw std::invalid_argument("filter_low_variance: threshold must be >= 0");
+  std::vector<double> var((size_t)in->p);
+  if (mine_b200_variances(ctx, in->values, in->p, in->n, var.data()) != 0)
+    throw std::runtime_error(mine_b200_last_error());
+  std::vector<int> keep;
+  for (int j = 0; j < in->p; ++j)
+    if (!(var[(size_t)j] < threshold)) keep.push_back(j);
+  if (keep.empty()) throw std::invalid_argument("filter_low_variance: no variables pass the threshold");
+  std::vector<double> values;
+  values.reserve(keep.size() * (size_t)in->n);
+  std::vector<std::string> names;
+  for (int j : keep) {
+    values.insert(values.end(), in->values + (size_t)j * in->n, in->values + (size_t)(j + 1) * in->n);
+    names.emplace_back(in->names[j]);
+  }
+  return new_dataset((int)keep.size(), in->n, std::move(values), names);
+}
+
+// io.cpp:17-22
+void append_value(std::string& out, double v) {
+  if (std::isnan(v)) {
+    out += "nan";
+    return;
+  }
+  char buf[32];
+  std::snprintf(buf, sizeof buf, "%.6g", v);
+  out += buf;
+}
+
+// The pair sequence of a task (analysis.cpp:43-90), each record oriented with
+// the lower index first (score_pair, :117-129); 0-based (lo, hi).
+struct Sequence {
+  int mode = 0;
+  long long p = 0, master = 0, first = 0, second = 0, size = 0;
+  void at(long long w, int& lo, int& hi) const {
+    long long i, j;
+    if (mode == 0) {
+      const long long total = p * (p - 1) / 2, r = total - w;
+      long long m = (long long)((std::sqrt(8.0 * (double)r + 1.0) - 1.0) / 2.0);
+      while (m * (m + 1) / 2 < r) ++m;
+      while (m >= 1 && (m - 1) * m / 2 >= r) --m;
+      i = p - m;
+      j = i + 1 + (w - (total - m * (m + 1) / 2));
+    } else if (mode == 1) {
+      const long long jj = w + 1;
+      i = master;
+      j = jj < master ? jj : jj + 1;
+    } else {
+      i = first;
+      j = second;
+    }
+    lo = (int)std::min(i, j) - 1;
+    hi = (int)std::max(i, j) - 1;
+  }
+};
+
+Sequence make_sequence(const mine_b200_task& t, long long p) {
+  Sequence s;
+  s.mode = t.mode;
+  s.p = p;
+  s.master = t.master;
+  s.first = t.first;
+  s.second = t.second;
+  auto check = [&](long long idx, const char* what) {
+    if (idx < 1 || idx > p) throw std::out_of_range(std::string("expand_pairs: ") + what + " index out of range");
+  };
+  if (t.mode == 0) {
+    s.size = p * (p - 1) / 2;
+  } else if (t.mode == 1) {
+    check(t.master, "master");
+    s.size = p - 1;
+  } else if (t.mode == 2) {
+    check(t.first, "first");
+    check(t.second, "second");
+    if (t.first == t.second) throw std::invalid_argument("expand_pairs: pair indices must differ");
+    s.size = 1;
+  } else {
+    throw std::invalid_argument("run_analysis: unknown mode");
+  }
+  return s;
+}
+
+long long run_analysis(mine_b200_ctx* ctx, const mine_b200_dataset* dataset,
+                       const mine_b200_task& task, const std::string& out_path) {
+  if (task.workers < 1) throw std::invalid_argument("run_analysis: workers must be positive");
+  const mine_b200_dataset* ds = dataset;
+  mine_b200_dataset* filtered = nullptr;
+  struct Free {
+    mine_b200_dataset*& d;
+    ~Free() { mine_b200_free_dataset(d); }
+  } free_filtered{filtered};
+  if (task.has_min_variance) {
+    filtered = filter_low_variance(ctx, dataset, task.min_variance);
+    ds = filtered;
+  }
+  const Sequence seq = make_sequence(task, ds->p);
+
+  // ResultWriter (io.cpp:122-154): temporary file, renamed into place on success
+  const std::string tmp = out_path + ".tmp";
+  std::FILE* f = std::fopen(tmp.c_str(), "wb");
+  if (!f) throw std::runtime_error(tmp + ": cannot open for writing");
+  struct Tmp {
+    std::FILE*& f;
+    const std::string& path;
+    bool keep = false;
+    ~Tmp() {
+      if (f) std::fclose(f);
+      if (!keep) {
+        std::error_code ec;
+        std::filesystem::remove(path, ec);
+      }
+    }
+  } guard{f, tmp};
+  static const char kHeader[] = "var1,var2,MIC,MAS,MEV,MCN,pearson,nonlinearity\n";
+  std::fwrite(kHeader, 1, sizeof kHeader - 1, f);
+
+  const mine_parameter par{task.alpha, task.c, MINE_EST_MIC_APPROX};
+  const long long block = 1LL << 20;
+  std::vector<double> st[6];
+  std::vector<int> xi, yi;
+  const unsigned nthreads = (unsigned)std::max(1, task.workers);
+  std::vector<std::string> text(nthreads);
+  for (long long base = 0; base < seq.size; base += block) {
+    const long long count = std::min(block, seq.size - base);
+    for (auto& v : st) v.resize((size_t)count);
+    mine_stats_out out{};
+    out.mic = st[0].data();
+    out.mas = st[1].data();
+    out.mev = st[2].data();
+    out.mcn = st[3].data();
+    out.pearson_r = st[4].data();
+    out.nonlinearity = st[5].data();
+    mine_b200_opts opt{};
+    opt.reuse_vars = base > 0;  // the per-variable stages run once per job
+    int rc;
+    if (seq.mode == 0) {
+      opt.first = base;
+      opt.count = count;
+      rc = mine_b200_pairwise(ctx, ds->values, ds->p, ds->n, &par, &opt, &out);
+    } else {
+      xi.resize((size_t)count);
+      yi.resize((size_t)count);
+      for (long long w = 0; w < count; ++w) seq.at(base + w, xi[(size_t)w], yi[(size_t)w]);
+      opt.count = count;
+      rc = mine_b200_pairs(ctx, ds->values, ds->p, ds->n, xi.data(), yi.data(), count, &par, &opt,
+                           &out);
+    }
+    if (rc != 0) throw std::runtime_error(mine_b200_last_error());
+    // format_record (io.cpp:37-47) for this block, `workers` threads
+    auto format = [&](unsigned t) {
+      const long long lo_w = count * t / nthreads, hi_w = count * (t + 1) / nthreads;
+      std::string& s = text[t];
+      s.clear();
+      for (long long w = lo_w; w < hi_w; ++w) {
+        int lo, hi;
+        seq.at(base + w, lo, hi);
+        s += ds->names[lo];
+        s += ',';
+        s += ds->names[hi];
+        for (int k = 0; k < 6; ++k) {
+          s += ',';
+          append_value(s, st[k][(size_t)w]);
+        }
+        s += '\n';
+      }
+    };
+    if (nthreads == 1) {
+      format(0);
+    } else {
+      std::vector<std::thread> pool;
+      for (unsigned t = 0; t < nthreads; ++t) pool.emplace_back(format, t);
+      for (auto& th : pool) th.join();
+    }
+    for (const auto& s : text)
+      if (std::fwrite(s.data(), 1, s.size(), f) != s.size()) throw std::runtime_error(tmp + ": write failed");
+  }
+  if (std::fflush(f) != 0 || std::ferror(f)) throw std::runtime_error(tmp + ": write failed");
+  std::fclose(f);
+  f = nullptr;
+  std::error_code ec;
+  std::filesystem::rename(tmp, out_path, ec);
+  if (ec) throw std::runtime_error(out_path + ": cannot replace output: " + ec.message());
+  guard.keep = true;
+  return seq.size;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mine_b200_read_dataset(const char* path, mine_b200_dataset** out) {
+  return guarded(
+      [&] {
+        if (!path || !out) throw std::invalid_argument("read_dataset: null argument");
+        *out = read_dataset(path);
+        return 0;
+      },
+      -1);
+}
+
+void mine_b200_free_dataset(mine_b200_dataset* ds) {
+  if (!ds) return;
+  for (int j = 0; j < ds->p; ++j) delete[] ds->names[j];
+  delete[] ds->names;
+  delete[] ds->values;
+  delete ds;
+}
+
+int mine_b200_filter_low_variance(mine_b200_ctx* ctx, const mine_b200_dataset* in, double threshold,
+                                  mine_b200_dataset** out) {
+  return guarded(
+      [&] {
+        if (!ctx || !in || !out) throw std::invalid_argument("filter_low_variance: null argument");
+        *out = filter_low_variance(ctx, in, threshold);
+        return 0;
+      },
+      -1);
+}
+
+long long mine_b200_run_analysis(mine_b200_ctx* ctx, const mine_b200_dataset* ds,
+                                 const mine_b200_task* task, const char* out_path) {
+  return guarded(
+      [&] {
+        if (!ctx || !ds || !task || !out_path) throw std::invalid_argument("run_analysis: null argument");
+        return run_analysis(ctx, ds, *task, out_path);
+      },
+      -1LL);
+}
+
+}  // extern "C"

@@ -54,6 +54,21 @@ class MineOpts(ctypes.Structure):
                 ("ev_end", ctypes.c_void_p), ("reuse_vars", ctypes.c_int)]
 
 
+class MineDataset(ctypes.Structure):
+    _fields_ = [("p", ctypes.c_int), ("n", ctypes.c_int), ("values", _dp),
+                ("names", ctypes.POINTER(ctypes.c_char_p))]
+
+
+class MineTask(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int), ("master", ctypes.c_int), ("first", ctypes.c_int),
+                ("second", ctypes.c_int), ("alpha", ctypes.c_double), ("c", ctypes.c_double),
+                ("has_min_variance", ctypes.c_int), ("min_variance", ctypes.c_double),
+                ("workers", ctypes.c_int)]
+
+
+MODES = {"all_pairs": 0, "master_vs_all": 1, "single_pair": 2}
+
+
 class MineProblem(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int), ("x", _dp), ("y", _dp)]
 
@@ -107,8 +122,48 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.mine_mcn.restype = ctypes.c_double
     L.mine_tic.argtypes = [P(MineScore), ctypes.c_int]
     L.mine_tic.restype = ctypes.c_double
+    L.mine_b200_read_dataset.argtypes = [ctypes.c_char_p, P(P(MineDataset))]
+    L.mine_b200_free_dataset.argtypes = [P(MineDataset)]
+    L.mine_b200_free_dataset.restype = None
+    L.mine_b200_variances.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, _dp]
+    L.mine_b200_filter_low_variance.argtypes = [vp, P(MineDataset), ctypes.c_double,
+                                                P(P(MineDataset))]
+    L.mine_b200_run_analysis.argtypes = [vp, P(MineDataset), P(MineTask), ctypes.c_char_p]
+    L.mine_b200_run_analysis.restype = ctypes.c_longlong
     _LIB = L
     return L
+
+
+def _dataset_to_py(ds_p) -> tuple[list[str], np.ndarray]:
+    ds = ds_p.contents
+    values = np.ctypeslib.as_array(ds.values, (ds.p, ds.n)).copy()
+    names = [ds.names[j].decode() for j in range(ds.p)]
+    return names, values
+
+
+class _NativeDataset:
+    """A mine_b200_dataset built from Python names / values (kept alive here)."""
+
+    def __init__(self, names, values):
+        self.values = _f64(values)
+        if self.values.ndim != 2 or len(names) != self.values.shape[0]:
+            raise ValueError("dataset: one name per variable row expected")
+        self._names = (ctypes.c_char_p * len(names))(*[str(s).encode() for s in names])
+        self.ds = MineDataset(self.values.shape[0], self.values.shape[1],
+                              self.values.ctypes.data_as(_dp), self._names)
+
+
+def read_dataset(path: str) -> tuple[list[str], np.ndarray]:
+    """mine::read_dataset (io.cpp:48-120), host-only: (names, p x n values).
+    Raises MineError with the reference's message on a malformed file."""
+    L = load_library()
+    out = ctypes.POINTER(MineDataset)()
+    if L.mine_b200_read_dataset(str(path).encode(), ctypes.byref(out)) != 0:
+        raise MineError(L.mine_b200_last_error().decode())
+    try:
+        return _dataset_to_py(out)
+    finally:
+        L.mine_b200_free_dataset(out)
 
 
 def exported_symbols() -> list[str]:
@@ -315,6 +370,44 @@ class Engine:
                                            ctypes.byref(self._opts(0, xi.size, tier, reuse_vars)),
                                            ctypes.byref(so)))
         return res
+
+    # -- analysis front end (io.cpp / analysis.cpp) ----------------------------
+    def variances(self, vars_) -> np.ndarray:
+        """Per-variable sample variance on the GPU (analysis.cpp:98-100)."""
+        v = _f64(vars_)
+        out = np.empty(v.shape[0])
+        self._check(self.L.mine_b200_variances(self.ctx, _ptr(v), v.shape[0], v.shape[1],
+                                               out.ctypes.data_as(_dp)))
+        return out
+
+    def filter_low_variance(self, names, values, threshold: float):
+        """filter_low_variance (analysis.cpp:92-113): (names, values) kept."""
+        src = _NativeDataset(names, values)
+        out = ctypes.POINTER(MineDataset)()
+        self._check(self.L.mine_b200_filter_low_variance(self.ctx, ctypes.byref(src.ds),
+                                                         float(threshold), ctypes.byref(out)))
+        try:
+            return _dataset_to_py(out)
+        finally:
+            self.L.mine_b200_free_dataset(out)
+
+    def run_analysis(self, names, values, out_path: str, mode: str = "all_pairs",
+                     master: int = 0, first: int = 0, second: int = 0,
+                     params: Parameters = Parameters(), min_variance: float | None = None,
+                     workers: int = 0) -> int:
+        """run_analysis + write_results (analysis.cpp:133-191, io.cpp:122-154):
+        writes the results file the reference's CLI writes (1-based indices
+        as AnalysisTask).  Returns the record count."""
+        src = _NativeDataset(names, values)
+        t = MineTask(MODES[mode], int(master), int(first), int(second), float(params.alpha),
+                     float(params.c), int(min_variance is not None),
+                     float(min_variance if min_variance is not None else 0.0),
+                     int(workers or os.cpu_count() or 1))
+        rc = self.L.mine_b200_run_analysis(self.ctx, ctypes.byref(src.ds), ctypes.byref(t),
+                                           str(out_path).encode())
+        if rc < 0:
+            raise MineError(self.L.mine_b200_last_error().decode())
+        return int(rc)
 
     def pairwise_device(self, vars_ptr: int, p: int, n: int, params: Parameters, out_ptrs: dict,
                         stream: int = 0, first: int = 0, count: int = 0, tier: int = 0,
