@@ -11,6 +11,8 @@
 // Host C++ only; it calls the engine through the public C ABI.
 #include <algorithm>
 #include <charconv>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -147,6 +149,109 @@ mine_b200_dataset* filter_low_variance(mine_b200_ctx* ctx, const mine_b200_datas
   return new_dataset((int)keep.size(), in->n, std::move(values), names);
 }
 
+// "%.6g" of v without the C library, bit-for-bit the text glibc's printf
+// writes (exact decimal rounding, ties to even, exponent chosen after
+// rounding, trailing zeros stripped).  v = m 2^e is scaled EXACTLY by a power
+// of ten in 128-bit integers: D = round(|v| 10^p) with 10^5 <= D < 10^6.
+// Covers 1e-17 <= |v| < 1e15 (every MINE statistic); returns 0 outside, and
+// the caller falls back to snprintf.  mine_b200_check_format compares it
+// with snprintf on random and boundary values (tests/test_frontend.py).
+int fmt6g_fast(double v, char* out) {
+  const double a = std::fabs(v);
+  if (!(a >= 1e-17) || !(a < 1e15)) return 0;
+  int e2;
+  const double fr = std::frexp(a, &e2);                  // a = fr 2^e2, fr in [0.5, 1)
+  const unsigned long long m = (unsigned long long)std::ldexp(fr, 53);  // exact
+  const int e = e2 - 53;                                 // a = m 2^e
+  static const unsigned __int128 kPow10[] = {
+      1ULL, 10ULL, 100ULL, 1000ULL, 10000ULL, 100000ULL, 1000000ULL, 10000000ULL, 100000000ULL,
+      1000000000ULL, 10000000000ULL, 100000000000ULL, 1000000000000ULL, 10000000000000ULL,
+      100000000000000ULL, 1000000000000000ULL, 10000000000000000ULL, 100000000000000000ULL,
+      1000000000000000000ULL, (unsigned __int128)1000000000000000000ULL * 10,
+      (unsigned __int128)1000000000000000000ULL * 100, (unsigned __int128)1000000000000000000ULL * 1000,
+      (unsigned __int128)1000000000000000000ULL * 10000};
+  // decimal exponent from the binary one: a in [2^(e2-1), 2^e2), so X is
+  // this estimate or one more (the loop below settles it exactly)
+  int X = (int)std::floor((e2 - 1) * 0.30102999566398120);
+  unsigned long long D = 0;
+  for (int iter = 0; iter < 4; ++iter) {
+    const int p = 5 - X;  // -9 .. 22 for the covered range
+    if (p < -9 || p > 22) return 0;
+    unsigned __int128 q, r, den;
+    if (p >= 0 && e < 0) {  // |v| < 1e6: the divisor is 2^-e, a shift
+      const unsigned __int128 num = (unsigned __int128)m * kPow10[p];
+      const int s = -e;
+      if (s >= 127) return 0;
+      q = num >> s;
+      r = num - (q << s);
+      den = (unsigned __int128)1 << s;
+    } else {
+      unsigned __int128 num = m;
+      den = 1;
+      if (p >= 0)
+        num *= kPow10[p];
+      else
+        den = kPow10[-p];
+      if (e >= 0)
+        num <<= e;  // |v| < 1e15 < 2^53 keeps e < 0 in practice
+      else
+        den <<= -e;
+      q = num / den;
+      r = num - q * den;
+    }
+    if (q < 100000) {  // X was one too large
+      --X;
+      continue;
+    }
+    if (q >= 1000000) {  // X was one too small
+      ++X;
+      continue;
+    }
+    D = (unsigned long long)q;
+    if (2 * r > den || (2 * r == den && (D & 1))) ++D;  // round half to even
+    if (D == 1000000) {  // rounding carried into a new decade
+      D = 100000;
+      ++X;
+    }
+    break;
+  }
+  if (D == 0) return 0;
+  char dig[6];
+  for (int i = 5; i >= 0; --i, D /= 10) dig[i] = (char)('0' + D % 10);
+  int nd = 6;
+  while (nd > 1 && dig[nd - 1] == '0') --nd;  // %g strips trailing zeros
+  char* o = out;
+  if (std::signbit(v)) *o++ = '-';
+  if (X >= -4 && X < 6) {  // %f style, precision 5 - X
+    if (X >= 0) {
+      for (int i = 0; i <= X; ++i) *o++ = i < nd ? dig[i] : '0';
+      if (nd > X + 1) {
+        *o++ = '.';
+        for (int i = X + 1; i < nd; ++i) *o++ = dig[i];
+      }
+    } else {
+      *o++ = '0';
+      *o++ = '.';
+      for (int i = 0; i < -X - 1; ++i) *o++ = '0';
+      for (int i = 0; i < nd; ++i) *o++ = dig[i];
+    }
+  } else {  // %e style, precision 5
+    *o++ = dig[0];
+    if (nd > 1) {
+      *o++ = '.';
+      for (int i = 1; i < nd; ++i) *o++ = dig[i];
+    }
+    *o++ = 'e';
+    *o++ = X < 0 ? '-' : '+';
+    const int ax = X < 0 ? -X : X;
+    if (ax >= 100) *o++ = (char)('0' + ax / 100);
+    *o++ = (char)('0' + ax / 10 % 10);
+    *o++ = (char)('0' + ax % 10);
+  }
+  *o = 0;
+  return (int)(o - out);
+}
+
 // io.cpp:17-22
 void append_value(std::string& out, double v) {
   if (std::isnan(v)) {
@@ -154,6 +259,14 @@ void append_value(std::string& out, double v) {
     return;
   }
   char buf[32];
+  if (v == 0.0) {
+    out += std::signbit(v) ? "-0" : "0";
+    return;
+  }
+  if (fmt6g_fast(v, buf)) {
+    out += buf;
+    return;
+  }
   std::snprintf(buf, sizeof buf, "%.6g", v);
   out += buf;
 }
@@ -251,8 +364,13 @@ long long run_analysis(mine_b200_ctx* ctx, const mine_b200_dataset* dataset,
   std::vector<int> xi, yi;
   const unsigned nthreads = (unsigned)std::max(1, task.workers);
   std::vector<std::string> text(nthreads);
+  const bool timing = std::getenv("MINE_B200_TIMING") != nullptr;
+  double t_gpu = 0, t_fmt = 0, t_io = 0;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto secs = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
   for (long long base = 0; base < seq.size; base += block) {
     const long long count = std::min(block, seq.size - base);
+    const auto c0 = now();
     for (auto& v : st) v.resize((size_t)count);
     mine_stats_out out{};
     out.mic = st[0].data();
@@ -277,14 +395,25 @@ long long run_analysis(mine_b200_ctx* ctx, const mine_b200_dataset* dataset,
                            &out);
     }
     if (rc != 0) throw std::runtime_error(mine_b200_last_error());
+    const auto c1 = now();
     // format_record (io.cpp:37-47) for this block, `workers` threads
     auto format = [&](unsigned t) {
       const long long lo_w = count * t / nthreads, hi_w = count * (t + 1) / nthreads;
       std::string& s = text[t];
       s.clear();
+      int lo = 0, hi = 0;
+      if (lo_w < hi_w) seq.at(base + lo_w, lo, hi);
       for (long long w = lo_w; w < hi_w; ++w) {
-        int lo, hi;
-        seq.at(base + w, lo, hi);
+        if (w > lo_w) {
+          if (seq.mode == 0) {  // next (i, j) of the condensed order
+            if (++hi == seq.p) {
+              ++lo;
+              hi = lo + 1;
+            }
+          } else {
+            seq.at(base + w, lo, hi);
+          }
+        }
         s += ds->names[lo];
         s += ',';
         s += ds->names[hi];
@@ -302,9 +431,16 @@ long long run_analysis(mine_b200_ctx* ctx, const mine_b200_dataset* dataset,
       for (unsigned t = 0; t < nthreads; ++t) pool.emplace_back(format, t);
       for (auto& th : pool) th.join();
     }
+    const auto c2 = now();
     for (const auto& s : text)
       if (std::fwrite(s.data(), 1, s.size(), f) != s.size()) throw std::runtime_error(tmp + ": write failed");
+    const auto c3 = now();
+    t_gpu += secs(c0, c1);
+    t_fmt += secs(c1, c2);
+    t_io += secs(c2, c3);
   }
+  if (timing)
+    std::fprintf(stderr, "run_analysis: gpu %.3f s, format %.3f s, write %.3f s\n", t_gpu, t_fmt, t_io);
   if (std::fflush(f) != 0 || std::ferror(f)) throw std::runtime_error(tmp + ": write failed");
   std::fclose(f);
   f = nullptr;
@@ -356,6 +492,53 @@ long long mine_b200_run_analysis(mine_b200_ctx* ctx, const mine_b200_dataset* ds
         return run_analysis(ctx, ds, *task, out_path);
       },
       -1LL);
+}
+
+// Self-test of the exact "%.6g" (records.cpp fmt6g_fast) against snprintf:
+// `count` values (random magnitudes 1e-18 .. 1e16, values near rounding ties
+// and decade boundaries, small rationals); returns the number of mismatches.
+long long mine_b200_check_format(long long count, unsigned long long seed) {
+  unsigned long long st = seed * 6364136223846793005ULL + 1442695040888963407ULL;
+  auto next = [&] {
+    st = st * 6364136223846793005ULL + 1442695040888963407ULL;
+    return st >> 11;  // 53 random bits
+  };
+  long long bad = 0;
+  for (long long i = 0; i < count; ++i) {
+    double v;
+    switch (i % 4) {
+      case 0: {  // log-uniform magnitude, random sign
+        const double u = (double)next() / 9007199254740992.0;
+        v = std::pow(10.0, -18.0 + 34.0 * u) * ((next() & 1) ? -1 : 1);
+        break;
+      }
+      case 1: {  // 6-digit decimals +- a few ulps: the rounding ties
+        const double d = 100000.0 + (double)(next() % 900000);
+        const int x = (int)(next() % 30) - 17;
+        v = (d + 0.5) * std::pow(10.0, x - 5);
+        for (int k = (int)(next() % 7) - 3; k != 0; k += k > 0 ? -1 : 1)
+          v = std::nextafter(v, k > 0 ? 1e300 : -1e300);
+        break;
+      }
+      case 2: {  // near decade boundaries (9.999995..)
+        const int x = (int)(next() % 30) - 17;
+        v = std::pow(10.0, x) * (1.0 - 5e-7 * ((double)(next() % 2000) / 1000.0));
+        break;
+      }
+      default: {  // small rationals, like the statistics (k/m, log2 of integers)
+        const double num = (double)(next() % 100000), den = (double)(1 + next() % 100000);
+        v = (next() & 1) ? num / den : std::log2(1.0 + (double)(next() % 100000));
+        break;
+      }
+    }
+    char a[40], b[40];
+    std::snprintf(b, sizeof b, "%.6g", v);
+    std::string s;
+    append_value(s, v);
+    std::snprintf(a, sizeof a, "%s", s.c_str());
+    if (std::strcmp(a, b) != 0) ++bad;
+  }
+  return bad;
 }
 
 }  // extern "C"

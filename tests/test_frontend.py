@@ -66,6 +66,20 @@ def test_read_dataset_missing_file(tmp_path, reference):
     assert str(ours.value) == str(ref.value)
 
 
+def test_record_number_format_matches_printf():
+    """format_record's "%.6g" (io.cpp:17-22) is produced by an exact integer
+    formatter (records.cpp fmt6g_fast); it must equal glibc's snprintf on
+    random magnitudes, 6-digit rounding ties +- a few ulps, decade boundaries
+    and small rationals."""
+    import ctypes
+    from paper_1208_4271_b200.engine import load_library
+    L = load_library()
+    L.mine_b200_check_format.restype = ctypes.c_longlong
+    L.mine_b200_check_format.argtypes = [ctypes.c_longlong, ctypes.c_ulonglong]
+    for seed in (1, 2, 3):
+        assert L.mine_b200_check_format(1_000_000, seed) == 0
+
+
 # --- GPU: variance filter and the results file ------------------------------
 def _dataset_csv(path, names, values):
     lines = [n + "," + ",".join(repr(float(v)) for v in row) for n, row in zip(names, values)]
