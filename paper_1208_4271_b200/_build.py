@@ -23,7 +23,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CUDA_INC = "/usr/local/cuda/include"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-KERNEL_SRCS = ["mine_kernels.cu", "mine_general.cu", "pearson.cu"]
+KERNEL_SRCS = ["mine_kernels.cu", "mine_general.cu", "pearson.cu", "format.cu"]
 HOST_SRCS = ["engine.cpp", "records.cpp"]
 HEADERS = ["mine_kernels.h", "device_common.cuh", os.path.join("..", "..", "include", "mine_b200.h")]
 

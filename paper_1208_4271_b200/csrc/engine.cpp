@@ -599,6 +599,7 @@ namespace mb200 {
 // for the host front end (records.cpp): the thread-local message the C ABI
 // reports through mine_b200_last_error
 void set_last_error(const std::string& msg) { g_err = msg; }
+int ctx_device(const mine_b200_ctx* ctx) { return ctx->device; }
 }  // namespace mb200
 
 extern "C" {

@@ -1,0 +1,222 @@
+// Results-file records on the device: format_record
+// (io.cpp:37-47) for a block of pairs, straight from the HBM-resident
+// statistics -- "name_x,name_y,MIC,MAS,MEV,MCN,pearson,nonlinearity\n" with
+// "%.6g" values and "nan" -- into one contiguous text buffer, so only the
+// text crosses PCIe and the host only writes it.
+//
+// "%.6g" is the exact integer algorithm of records.cpp fmt6g_fast (the same
+// text glibc's printf produces: exact scaling of v = m 2^e by a power of ten in
+// 128-bit integers, ties to even, exponent after rounding, trailing zeros
+// stripped).  Values outside 1e-17 <= |v| < 1e15 raise a flag and the host
+// formats that block instead (no MINE statistic gets there).
+//
+//   k_rec_len   one thread per record: its byte length (and the fallback flag)
+//   (exclusive scan of the lengths, cub)
+//   k_rec_write one thread per record: the bytes at its offset
+#include <cub/device/device_scan.cuh>
+
+#include "device_common.cuh"
+#include "mine_kernels.h"
+
+namespace mb200 {
+namespace {
+
+__device__ __forceinline__ int fmt6g_dev(double v, char* out, bool& fallback) {
+  if (isnan(v)) {
+    out[0] = 'n', out[1] = 'a', out[2] = 'n';
+    return 3;
+  }
+  char* o = out;
+  if (signbit(v)) *o++ = '-';
+  if (v == 0.0) {
+    *o++ = '0';
+    return (int)(o - out);
+  }
+  const double a = fabs(v);
+  if (!(a >= 1e-17) || !(a < 1e15)) {
+    fallback = true;
+    return 0;
+  }
+  int e2;
+  const double fr = frexp(a, &e2);
+  const unsigned long long m = (unsigned long long)ldexp(fr, 53);  // exact
+  const int e = e2 - 53;
+  int X = (int)floor((e2 - 1) * 0.30102999566398120);
+  unsigned long long D = 0;
+  for (int iter = 0; iter < 4; ++iter) {
+    const int p = 5 - X;
+    if (p < -9 || p > 22 || e >= 0) {
+      fallback = true;
+      return 0;
+    }
+    unsigned __int128 num = m, den = 1;
+    const int pp = p >= 0 ? p : -p;
+    unsigned __int128 p10 = 1;
+    for (int i = 0; i < pp; ++i) p10 *= 10u;
+    unsigned __int128 q, r;
+    const int s = -e;
+    if (p >= 0) {
+      num = (unsigned __int128)m * p10;
+      if (s >= 127) {
+        fallback = true;
+        return 0;
+      }
+      q = num >> s;
+      r = num - (q << s);
+      den = (unsigned __int128)1 << s;
+    } else {
+      den = p10 << s;
+      q = num / den;
+      r = num - q * den;
+    }
+    if (q < 100000) {
+      --X;
+      continue;
+    }
+    if (q >= 1000000) {
+      ++X;
+      continue;
+    }
+    D = (unsigned long long)q;
+    if (2 * r > den || (2 * r == den && (D & 1))) ++D;
+    if (D == 1000000) {
+      D = 100000;
+      ++X;
+    }
+    break;
+  }
+  if (D == 0) {
+    fallback = true;
+    return 0;
+  }
+  char dig[6];
+  for (int i = 5; i >= 0; --i, D /= 10) dig[i] = (char)('0' + D % 10);
+  int nd = 6;
+  while (nd > 1 && dig[nd - 1] == '0') --nd;
+  if (X >= -4 && X < 6) {
+    if (X >= 0) {
+      for (int i = 0; i <= X; ++i) *o++ = i < nd ? dig[i] : '0';
+      if (nd > X + 1) {
+        *o++ = '.';
+        for (int i = X + 1; i < nd; ++i) *o++ = dig[i];
+      }
+    } else {
+      *o++ = '0';
+      *o++ = '.';
+      for (int i = 0; i < -X - 1; ++i) *o++ = '0';
+      for (int i = 0; i < nd; ++i) *o++ = dig[i];
+    }
+  } else {
+    *o++ = dig[0];
+    if (nd > 1) {
+      *o++ = '.';
+      for (int i = 1; i < nd; ++i) *o++ = dig[i];
+    }
+    *o++ = 'e';
+    *o++ = X < 0 ? '-' : '+';
+    const int ax = X < 0 ? -X : X;
+    if (ax >= 100) *o++ = (char)('0' + ax / 100);
+    *o++ = (char)('0' + ax / 10 % 10);
+    *o++ = (char)('0' + ax % 10);
+  }
+  return (int)(o - out);
+}
+
+struct RecArgs {
+  PairSpace ps;                 // pair w -> (x, y) of the call; records print min/max
+  const double* stat[6];        // mic mas mev mcn pearson nonlinearity (indexed w - 0)
+  const char* names;            // concatenated labels
+  const long long* name_off;    // p + 1 offsets into names
+  long long count;
+};
+
+// The record of pair w into out (<= 2 names + 6 x 13 + 8 bytes); returns the
+// byte count.  out == nullptr: length only.
+__device__ int record(const RecArgs& a, long long w, char* out, bool& fallback) {
+  int x, y;
+  pair_vars(a.ps, a.ps.first + w, x, y);
+  const int lo = min(x, y), hi = max(x, y);
+  char buf[16];
+  int len = 0;
+  auto put_name = [&](int v) {
+    const long long b = a.name_off[v], e = a.name_off[v + 1];
+    if (out)
+      for (long long i = b; i < e; ++i) out[len + (i - b)] = a.names[i];
+    len += (int)(e - b);
+  };
+  put_name(lo);
+  if (out) out[len] = ',';
+  ++len;
+  put_name(hi);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    if (out) out[len] = ',';
+    ++len;
+    const int n = fmt6g_dev(a.stat[k][w], buf, fallback);
+    if (out)
+      for (int i = 0; i < n; ++i) out[len + i] = buf[i];
+    len += n;
+  }
+  if (out) out[len] = '\n';
+  return len + 1;
+}
+
+__global__ void k_rec_len(RecArgs a, unsigned long long* len, int* fallback) {
+  const long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (w >= a.count) return;
+  bool fb = false;
+  len[w] = (unsigned long long)record(a, w, nullptr, fb);
+  if (fb) *fallback = 1;
+}
+
+__global__ void k_rec_write(RecArgs a, const unsigned long long* off, char* text) {
+  const long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (w >= a.count) return;
+  bool fb = false;
+  record(a, w, text + off[w], fb);
+}
+
+}  // namespace
+
+size_t format_scratch_bytes(long long count) {
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, (unsigned long long*)nullptr,
+                                (unsigned long long*)nullptr, (int)count + 1);
+  return tmp + 2 * sizeof(unsigned long long) * (size_t)(count + 1) + 256;
+}
+
+// Formats records [0, count) of the pair space; returns the text size in
+// bytes (in *bytes) once the stream is synchronised, or *fallback != 0.
+cudaError_t launch_format_records(const PairSpace& ps, const double* const stat[6],
+                                  const char* names, const long long* name_off, long long count,
+                                  void* scratch, char* text, size_t text_cap, size_t* bytes,
+                                  int* d_flag, int* h_fallback, cudaStream_t s) {
+  RecArgs a;
+  a.ps = ps;
+  for (int k = 0; k < 6; ++k) a.stat[k] = stat[k];
+  a.names = names;
+  a.name_off = name_off;
+  a.count = count;
+  auto* len = static_cast<unsigned long long*>(scratch);
+  auto* off = len + (count + 1);
+  void* cub_tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(off + (count + 1)) + 255) &
+                                          ~uintptr_t(255));
+  size_t cub_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, len, off, (int)count + 1, s);
+  cudaMemsetAsync(d_flag, 0, sizeof(int), s);
+  cudaMemsetAsync(len + count, 0, sizeof(unsigned long long), s);
+  const unsigned blocks = (unsigned)((count + 255) / 256);
+  k_rec_len<<<blocks, 256, 0, s>>>(a, len, d_flag);
+  cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, len, off, (int)count + 1, s);
+  unsigned long long total = 0;
+  cudaMemcpyAsync(&total, off + count, sizeof total, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(h_fallback, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  *bytes = (size_t)total;
+  if (*h_fallback || total > text_cap) return cudaSuccess;
+  k_rec_write<<<blocks, 256, 0, s>>>(a, off, text);
+  return cudaGetLastError();
+}
+
+}  // namespace mb200

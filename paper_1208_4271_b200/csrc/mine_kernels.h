@@ -179,4 +179,11 @@ void launch_variances(const VarSet& vs, double* var, cudaStream_t s);
 void launch_pearson_pairs(const VarSet& vs, const PairSpace& ps, const double* mic,
                           double* pearson, double* nonlin, cudaStream_t s);
 
+// Results-file records on the device (format.cu, io.cpp:37-47).
+size_t format_scratch_bytes(long long count);
+cudaError_t launch_format_records(const PairSpace& ps, const double* const stat[6],
+                                  const char* names, const long long* name_off, long long count,
+                                  void* scratch, char* text, size_t text_cap, size_t* bytes,
+                                  int* d_flag, int* h_fallback, cudaStream_t s);
+
 }  // namespace mb200

@@ -6,9 +6,11 @@
 //   * run_analysis + ResultWriter (analysis.cpp:133-191, io.cpp:122-154): the
 //     pair sequence of an AnalysisTask scored on the GPU in blocks (per-variable
 //     stages once per job: reuse_vars), every record formatted exactly like
-//     format_record (io.cpp:17-47: "%.6g", "nan") by `workers` host threads,
-//     written through a temporary file renamed into place on success.
-// Host C++ only; it calls the engine through the public C ABI.
+//     format_record (io.cpp:17-47: "%.6g", "nan") -- on the GPU from the
+//     HBM-resident statistics (format.cu; only the text crosses PCIe), or by
+//     `workers` host threads with MINE_B200_HOST_FORMAT -- and written through
+//     a temporary file renamed into place on success.
+// Host C++; it drives the engine through the public C ABI.
 #include <algorithm>
 #include <charconv>
 #include <chrono>
@@ -18,6 +20,7 @@
 #include <cstring>
 #include <filesystem>
 #include <fstream>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <string_view>
@@ -26,10 +29,14 @@
 #include <unordered_map>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "mine_b200.h"
+#include "mine_kernels.h"
 
 namespace mb200 {
 void set_last_error(const std::string& msg);
+int ctx_device(const mine_b200_ctx* ctx);
 }
 
 namespace {
@@ -324,6 +331,82 @@ Sequence make_sequence(const mine_b200_task& t, long long p) {
   return s;
 }
 
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// The device side of run_analysis: the dataset, the labels and each block's
+// statistics stay in HBM; format.cu turns a block into its text, and only
+// the text is copied back (pinned).
+struct DeviceRecords {
+  int dev = 0;
+  cudaStream_t s = nullptr;
+  double* vals = nullptr;
+  char* names = nullptr;
+  long long* noff = nullptr;
+  double* st[6] = {};
+  int *xi = nullptr, *yi = nullptr, *flag = nullptr, *h_fb = nullptr;
+  void* scr = nullptr;
+  char *text = nullptr, *h_text = nullptr;
+  size_t cap = 0;
+
+  DeviceRecords(mine_b200_ctx* ctx, const mine_b200_dataset* ds, long long block) {
+    dev = mb200::ctx_device(ctx);
+    cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    const size_t nv = (size_t)ds->p * ds->n;
+    cuda_check(cudaMalloc(&vals, sizeof(double) * nv), "cudaMalloc");
+    cuda_check(cudaMemcpy(vals, ds->values, sizeof(double) * nv, cudaMemcpyHostToDevice), "cudaMemcpy");
+    std::vector<long long> off(1, 0);
+    std::string all;
+    size_t longest = 0;
+    for (int j = 0; j < ds->p; ++j) {
+      const size_t l = std::strlen(ds->names[j]);
+      all.append(ds->names[j], l);
+      off.push_back((long long)all.size());
+      longest = std::max(longest, l);
+    }
+    cuda_check(cudaMalloc(&names, all.size() + 1), "cudaMalloc");
+    cuda_check(cudaMemcpy(names, all.data(), all.size(), cudaMemcpyHostToDevice), "cudaMemcpy");
+    cuda_check(cudaMalloc(&noff, sizeof(long long) * off.size()), "cudaMalloc");
+    cuda_check(cudaMemcpy(noff, off.data(), sizeof(long long) * off.size(), cudaMemcpyHostToDevice),
+               "cudaMemcpy");
+    for (auto& p : st) cuda_check(cudaMalloc(&p, sizeof(double) * (size_t)block), "cudaMalloc");
+    cuda_check(cudaMalloc(&xi, sizeof(int) * (size_t)block), "cudaMalloc");
+    cuda_check(cudaMalloc(&yi, sizeof(int) * (size_t)block), "cudaMalloc");
+    cuda_check(cudaMalloc(&flag, sizeof(int)), "cudaMalloc");
+    cuda_check(cudaMallocHost(&h_fb, sizeof(int)), "cudaMallocHost");
+    cuda_check(cudaMalloc(&scr, mb200::format_scratch_bytes(block)), "cudaMalloc");
+    // a record is at most 2 labels + 6 values of <= 13 bytes + 8 separators
+    grow((size_t)block * (2 * longest + 6 * 13 + 8));
+  }
+  void grow(size_t bytes) {
+    if (bytes <= cap) return;
+    if (text) cudaFree(text);
+    if (h_text) cudaFreeHost(h_text);
+    text = nullptr;
+    h_text = nullptr;
+    cuda_check(cudaMalloc(&text, bytes), "cudaMalloc");
+    cuda_check(cudaMallocHost(&h_text, bytes), "cudaMallocHost");
+    cap = bytes;
+  }
+  ~DeviceRecords() {
+    cudaSetDevice(dev);
+    for (auto p : st) cudaFree(p);
+    cudaFree(vals);
+    cudaFree(names);
+    cudaFree(noff);
+    cudaFree(xi);
+    cudaFree(yi);
+    cudaFree(flag);
+    cudaFreeHost(h_fb);
+    cudaFree(scr);
+    cudaFree(text);
+    cudaFreeHost(h_text);
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
 long long run_analysis(mine_b200_ctx* ctx, const mine_b200_dataset* dataset,
                        const mine_b200_task& task, const std::string& out_path) {
   if (task.workers < 1) throw std::invalid_argument("run_analysis: workers must be positive");
@@ -368,33 +451,107 @@ long long run_analysis(mine_b200_ctx* ctx, const mine_b200_dataset* dataset,
   double t_gpu = 0, t_fmt = 0, t_io = 0;
   auto now = [] { return std::chrono::steady_clock::now(); };
   auto secs = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+  // records are formatted on the GPU unless MINE_B200_HOST_FORMAT is set
+  std::unique_ptr<DeviceRecords> dr;
+  const auto s0 = now();
+  if (!std::getenv("MINE_B200_HOST_FORMAT") && seq.size > 0) dr.reset(new DeviceRecords(ctx, ds, block));
+  const double t_setup = secs(s0, now());
   for (long long base = 0; base < seq.size; base += block) {
     const long long count = std::min(block, seq.size - base);
     const auto c0 = now();
-    for (auto& v : st) v.resize((size_t)count);
-    mine_stats_out out{};
-    out.mic = st[0].data();
-    out.mas = st[1].data();
-    out.mev = st[2].data();
-    out.mcn = st[3].data();
-    out.pearson_r = st[4].data();
-    out.nonlinearity = st[5].data();
-    mine_b200_opts opt{};
-    opt.reuse_vars = base > 0;  // the per-variable stages run once per job
-    int rc;
-    if (seq.mode == 0) {
-      opt.first = base;
-      opt.count = count;
-      rc = mine_b200_pairwise(ctx, ds->values, ds->p, ds->n, &par, &opt, &out);
-    } else {
-      xi.resize((size_t)count);
-      yi.resize((size_t)count);
-      for (long long w = 0; w < count; ++w) seq.at(base + w, xi[(size_t)w], yi[(size_t)w]);
-      opt.count = count;
-      rc = mine_b200_pairs(ctx, ds->values, ds->p, ds->n, xi.data(), yi.data(), count, &par, &opt,
-                           &out);
+    if (dr) {  // statistics and text on the device
+      mine_stats_out out{};
+      out.mic = dr->st[0];
+      out.mas = dr->st[1];
+      out.mev = dr->st[2];
+      out.mcn = dr->st[3];
+      out.pearson_r = dr->st[4];
+      out.nonlinearity = dr->st[5];
+      mine_b200_opts opt{};
+      opt.device_io = 1;
+      opt.stream = dr->s;
+      opt.reuse_vars = base > 0;
+      mb200::PairSpace ps;
+      int rc;
+      if (seq.mode == 0) {
+        opt.first = base;
+        opt.count = count;
+        rc = mine_b200_pairwise(ctx, dr->vals, ds->p, ds->n, &par, &opt, &out);
+        ps.kind = mb200::kPairwise;
+        ps.p = ds->p;
+        ps.first = base;
+      } else {
+        xi.resize((size_t)count);
+        yi.resize((size_t)count);
+        for (long long w = 0; w < count; ++w) seq.at(base + w, xi[(size_t)w], yi[(size_t)w]);
+        cuda_check(cudaMemcpyAsync(dr->xi, xi.data(), sizeof(int) * count, cudaMemcpyHostToDevice, dr->s),
+                   "cudaMemcpyAsync");
+        cuda_check(cudaMemcpyAsync(dr->yi, yi.data(), sizeof(int) * count, cudaMemcpyHostToDevice, dr->s),
+                   "cudaMemcpyAsync");
+        opt.count = count;
+        rc = mine_b200_pairs(ctx, dr->vals, ds->p, ds->n, dr->xi, dr->yi, count, &par, &opt, &out);
+        ps.kind = mb200::kList;
+        ps.xi = dr->xi;
+        ps.yi = dr->yi;
+      }
+      if (rc != 0) throw std::runtime_error(mine_b200_last_error());
+      ps.count = count;
+      const auto c1 = now();
+      size_t bytes = 0;
+      const double* const stp[6] = {dr->st[0], dr->st[1], dr->st[2], dr->st[3], dr->st[4], dr->st[5]};
+      cuda_check(mb200::launch_format_records(ps, stp, dr->names, dr->noff, count, dr->scr, dr->text,
+                                              dr->cap, &bytes, dr->flag, dr->h_fb, dr->s),
+                 "format_records");
+      if (!*dr->h_fb) {
+        if (bytes > dr->cap) {  // cannot happen with the bound above; grow and redo
+          dr->grow(bytes);
+          cuda_check(mb200::launch_format_records(ps, stp, dr->names, dr->noff, count, dr->scr,
+                                                  dr->text, dr->cap, &bytes, dr->flag, dr->h_fb, dr->s),
+                     "format_records");
+        }
+        cuda_check(cudaMemcpyAsync(dr->h_text, dr->text, bytes, cudaMemcpyDeviceToHost, dr->s),
+                   "cudaMemcpyAsync");
+        cuda_check(cudaStreamSynchronize(dr->s), "cudaStreamSynchronize");
+        const auto c2 = now();
+        if (std::fwrite(dr->h_text, 1, bytes, f) != bytes) throw std::runtime_error(tmp + ": write failed");
+        const auto c3 = now();
+        t_gpu += secs(c0, c1);
+        t_fmt += secs(c1, c2);
+        t_io += secs(c2, c3);
+        continue;
+      }
+      // a value outside the device formatter's range: this block on the host
+      for (int k = 0; k < 6; ++k) {
+        st[k].resize((size_t)count);
+        cuda_check(cudaMemcpy(st[k].data(), dr->st[k], sizeof(double) * count, cudaMemcpyDeviceToHost),
+                   "cudaMemcpy");
+      }
+    } else {  // statistics to host buffers, host formatting
+      for (auto& v : st) v.resize((size_t)count);
+      mine_stats_out out{};
+      out.mic = st[0].data();
+      out.mas = st[1].data();
+      out.mev = st[2].data();
+      out.mcn = st[3].data();
+      out.pearson_r = st[4].data();
+      out.nonlinearity = st[5].data();
+      mine_b200_opts opt{};
+      opt.reuse_vars = base > 0;  // the per-variable stages run once per job
+      int rc;
+      if (seq.mode == 0) {
+        opt.first = base;
+        opt.count = count;
+        rc = mine_b200_pairwise(ctx, ds->values, ds->p, ds->n, &par, &opt, &out);
+      } else {
+        xi.resize((size_t)count);
+        yi.resize((size_t)count);
+        for (long long w = 0; w < count; ++w) seq.at(base + w, xi[(size_t)w], yi[(size_t)w]);
+        opt.count = count;
+        rc = mine_b200_pairs(ctx, ds->values, ds->p, ds->n, xi.data(), yi.data(), count, &par, &opt,
+                             &out);
+      }
+      if (rc != 0) throw std::runtime_error(mine_b200_last_error());
     }
-    if (rc != 0) throw std::runtime_error(mine_b200_last_error());
     const auto c1 = now();
     // format_record (io.cpp:37-47) for this block, `workers` threads
     auto format = [&](unsigned t) {
@@ -439,8 +596,7 @@ long long run_analysis(mine_b200_ctx* ctx, const mine_b200_dataset* dataset,
     t_fmt += secs(c1, c2);
     t_io += secs(c2, c3);
   }
-  if (timing)
-    std::fprintf(stderr, "run_analysis: gpu %.3f s, format %.3f s, write %.3f s\n", t_gpu, t_fmt, t_io);
+  const auto s1 = now();
   if (std::fflush(f) != 0 || std::ferror(f)) throw std::runtime_error(tmp + ": write failed");
   std::fclose(f);
   f = nullptr;
@@ -448,6 +604,10 @@ long long run_analysis(mine_b200_ctx* ctx, const mine_b200_dataset* dataset,
   std::filesystem::rename(tmp, out_path, ec);
   if (ec) throw std::runtime_error(out_path + ": cannot replace output: " + ec.message());
   guard.keep = true;
+  dr.reset();
+  if (timing)
+    std::fprintf(stderr, "run_analysis: setup %.3f s, gpu %.3f s, format %.3f s, write %.3f s, close %.3f s\n",
+                 t_setup, t_gpu, t_fmt, t_io, secs(s1, now()));
   return seq.size;
 }
 

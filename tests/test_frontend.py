@@ -98,6 +98,7 @@ def _c1_dataset():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("formatter", ["device", "host"])
 @pytest.mark.parametrize("task", [
     dict(mode=0),
     dict(mode=0, min_variance=0.9),
@@ -105,7 +106,13 @@ def _c1_dataset():
     dict(mode=1, a=40),
     dict(mode=2, a=12, b=3),
 ])
-def test_results_file_matches_reference(tmp_path, engine, reference, task):
+def test_results_file_matches_reference(tmp_path, monkeypatch, engine, reference, task, formatter):
+    """Records formatted on the GPU (format.cu, default) or by host threads
+    (MINE_B200_HOST_FORMAT): the same bytes as the reference's file."""
+    if formatter == "host":
+        monkeypatch.setenv("MINE_B200_HOST_FORMAT", "1")
+    else:
+        monkeypatch.delenv("MINE_B200_HOST_FORMAT", raising=False)
     names, V = _c1_dataset()
     src = _dataset_csv(tmp_path / "in.csv", names, V)
     ref_out, our_out = str(tmp_path / "ref.csv"), str(tmp_path / "ours.csv")
