@@ -226,8 +226,9 @@ int mine_b200_filter_low_variance(mine_b200_ctx* ctx, const mine_b200_dataset* i
 long long mine_b200_run_analysis(mine_b200_ctx* ctx, const mine_b200_dataset* ds,
                                  const mine_b200_task* task, const char* out_path);
 /* Self-test of the exact "%.6g" record formatter against snprintf on `count`
- * generated values; returns the mismatch count (0 expected). */
-long long mine_b200_check_format(long long count, unsigned long long seed);
+ * generated values: the host formatter (device < 0) or the GPU one; returns
+ * the mismatch count (0 expected), -1 on a CUDA error. */
+long long mine_b200_check_format(long long count, unsigned long long seed, int device);
 
 #ifdef __cplusplus
 }

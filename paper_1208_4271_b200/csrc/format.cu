@@ -176,7 +176,23 @@ __global__ void k_rec_write(RecArgs a, const unsigned long long* off, char* text
   record(a, w, text + off[w], fb);
 }
 
+// test hook: "%.6g" of n values into 24-byte slots (length 0: host fallback)
+__global__ void k_format_values(const double* v, long long n, char* out, int* len) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool fb = false;
+  char buf[24];
+  const int l = fmt6g_dev(v[i], buf, fb);
+  len[i] = fb ? 0 : l;
+  for (int k = 0; k < l; ++k) out[i * 24 + k] = buf[k];
+}
+
 }  // namespace
+
+cudaError_t format_values_device(const double* v, long long n, char* out, int* len, cudaStream_t s) {
+  k_format_values<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v, n, out, len);
+  return cudaGetLastError();
+}
 
 size_t format_scratch_bytes(long long count) {
   size_t tmp = 0;

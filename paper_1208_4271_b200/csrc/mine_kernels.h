@@ -181,6 +181,7 @@ void launch_pearson_pairs(const VarSet& vs, const PairSpace& ps, const double* m
 
 // Results-file records on the device (format.cu, io.cpp:37-47).
 size_t format_scratch_bytes(long long count);
+cudaError_t format_values_device(const double* v, long long n, char* out, int* len, cudaStream_t s);
 cudaError_t launch_format_records(const PairSpace& ps, const double* const stat[6],
                                   const char* names, const long long* name_off, long long count,
                                   void* scratch, char* text, size_t text_cap, size_t* bytes,

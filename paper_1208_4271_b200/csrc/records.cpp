@@ -657,22 +657,25 @@ long long mine_b200_run_analysis(mine_b200_ctx* ctx, const mine_b200_dataset* ds
 // Self-test of the exact "%.6g" (records.cpp fmt6g_fast) against snprintf:
 // `count` values (random magnitudes 1e-18 .. 1e16, values near rounding ties
 // and decade boundaries, small rationals); returns the number of mismatches.
-long long mine_b200_check_format(long long count, unsigned long long seed) {
+namespace {
+// the self-test's value generator: random magnitudes 1e-18 .. 1e16, 6-digit
+// decimals +- a few ulps (rounding ties), decade boundaries, small rationals
+std::vector<double> format_test_values(long long count, unsigned long long seed) {
   unsigned long long st = seed * 6364136223846793005ULL + 1442695040888963407ULL;
   auto next = [&] {
     st = st * 6364136223846793005ULL + 1442695040888963407ULL;
     return st >> 11;  // 53 random bits
   };
-  long long bad = 0;
+  std::vector<double> out((size_t)count);
   for (long long i = 0; i < count; ++i) {
     double v;
     switch (i % 4) {
-      case 0: {  // log-uniform magnitude, random sign
+      case 0: {
         const double u = (double)next() / 9007199254740992.0;
         v = std::pow(10.0, -18.0 + 34.0 * u) * ((next() & 1) ? -1 : 1);
         break;
       }
-      case 1: {  // 6-digit decimals +- a few ulps: the rounding ties
+      case 1: {
         const double d = 100000.0 + (double)(next() % 900000);
         const int x = (int)(next() % 30) - 17;
         v = (d + 0.5) * std::pow(10.0, x - 5);
@@ -680,23 +683,64 @@ long long mine_b200_check_format(long long count, unsigned long long seed) {
           v = std::nextafter(v, k > 0 ? 1e300 : -1e300);
         break;
       }
-      case 2: {  // near decade boundaries (9.999995..)
+      case 2: {
         const int x = (int)(next() % 30) - 17;
         v = std::pow(10.0, x) * (1.0 - 5e-7 * ((double)(next() % 2000) / 1000.0));
         break;
       }
-      default: {  // small rationals, like the statistics (k/m, log2 of integers)
+      default: {
         const double num = (double)(next() % 100000), den = (double)(1 + next() % 100000);
         v = (next() & 1) ? num / den : std::log2(1.0 + (double)(next() % 100000));
         break;
       }
     }
-    char a[40], b[40];
-    std::snprintf(b, sizeof b, "%.6g", v);
-    std::string s;
-    append_value(s, v);
-    std::snprintf(a, sizeof a, "%s", s.c_str());
-    if (std::strcmp(a, b) != 0) ++bad;
+    out[(size_t)i] = v;
+  }
+  return out;
+}
+}  // namespace
+
+// Self-test of the exact "%.6g" record formatter (host: records.cpp
+// fmt6g_fast; device >= 0: format.cu on that GPU) against snprintf on
+// `count` generated values; returns the mismatch count (0 expected), -1 on a
+// CUDA error.  Values the device formatter leaves to the host are skipped.
+long long mine_b200_check_format(long long count, unsigned long long seed, int device) {
+  const std::vector<double> vals = format_test_values(count, seed);
+  std::vector<char> dev_text;
+  std::vector<int> dev_len;
+  if (device >= 0) {
+    double* dv = nullptr;
+    char* dt = nullptr;
+    int* dl = nullptr;
+    if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(&dv, sizeof(double) * count) != cudaSuccess ||
+        cudaMalloc(&dt, 24 * (size_t)count) != cudaSuccess || cudaMalloc(&dl, sizeof(int) * count) != cudaSuccess)
+      return -1;
+    cudaMemcpy(dv, vals.data(), sizeof(double) * count, cudaMemcpyHostToDevice);
+    mb200::format_values_device(dv, count, dt, dl, nullptr);
+    dev_text.resize(24 * (size_t)count);
+    dev_len.resize((size_t)count);
+    cudaMemcpy(dev_text.data(), dt, dev_text.size(), cudaMemcpyDeviceToHost);
+    cudaMemcpy(dev_len.data(), dl, sizeof(int) * count, cudaMemcpyDeviceToHost);
+    const bool ok = cudaGetLastError() == cudaSuccess;
+    cudaFree(dv);
+    cudaFree(dt);
+    cudaFree(dl);
+    if (!ok) return -1;
+  }
+  long long bad = 0;
+  for (long long i = 0; i < count; ++i) {
+    const double v = vals[(size_t)i];
+    char want[40];
+    std::snprintf(want, sizeof want, "%.6g", v);
+    std::string got;
+    if (device >= 0) {
+      const int l = dev_len[(size_t)i];
+      if (l == 0) continue;  // outside the device range: the host formats it
+      got.assign(&dev_text[(size_t)i * 24], (size_t)l);
+    } else {
+      append_value(got, v);
+    }
+    if (got != want) ++bad;
   }
   return bad;
 }

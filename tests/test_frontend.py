@@ -75,9 +75,21 @@ def test_record_number_format_matches_printf():
     from paper_1208_4271_b200.engine import load_library
     L = load_library()
     L.mine_b200_check_format.restype = ctypes.c_longlong
-    L.mine_b200_check_format.argtypes = [ctypes.c_longlong, ctypes.c_ulonglong]
+    L.mine_b200_check_format.argtypes = [ctypes.c_longlong, ctypes.c_ulonglong, ctypes.c_int]
     for seed in (1, 2, 3):
-        assert L.mine_b200_check_format(1_000_000, seed) == 0
+        assert L.mine_b200_check_format(1_000_000, seed, -1) == 0
+
+
+@pytest.mark.gpu
+def test_record_number_format_on_gpu_matches_printf(engine):
+    """The device formatter (format.cu) against snprintf, 4 M values."""
+    import ctypes
+    from paper_1208_4271_b200.engine import load_library
+    L = load_library()
+    L.mine_b200_check_format.restype = ctypes.c_longlong
+    L.mine_b200_check_format.argtypes = [ctypes.c_longlong, ctypes.c_ulonglong, ctypes.c_int]
+    for seed in (4, 5):
+        assert L.mine_b200_check_format(2_000_000, seed, 0) == 0
 
 
 # --- GPU: variance filter and the results file ------------------------------
