@@ -390,7 +390,7 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 // F lives in a per-CTA HBM slot (L2-resident for typical sizes); each outer
 // s-chunk's rows are staged into shared memory with coalesced loads, and the
 // current t-tile's rows are kept in shared memory while its inner part runs.
-__global__ void __launch_bounds__(kDpThreads, 512 / kDpThreads) k_dp(VarSet vs, Tables tb, PairSpace ps,
+__global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, PairSpace ps,
                                                       long long base, long long nsub, YParams yp,
                                                       GenScratch gs, double* __restrict__ ocells,
                                                       SubDebug dbg, int has_dbg, int orient_only) {
