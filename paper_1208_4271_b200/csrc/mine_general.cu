@@ -89,7 +89,7 @@ __device__ void write_cells(const Tables& tb, double* ocells, long long pl, int 
 }
 
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kPfThreads) k_part_f2(VarSet vs, Tables tb, PairSpace ps,
+__global__ void __launch_bounds__(kPfThreads, 8) k_part_f2(VarSet vs, Tables tb, PairSpace ps,
                                                         long long base, YParams yp, GenScratch gs,
                                                         double* __restrict__ ocells, SubDebug dbg,
                                                         int has_dbg, int orient_only,
