@@ -187,8 +187,15 @@ struct mine_b200_ctx {
   std::mutex mu;
   TableSet tables;
   DevBuf vals, perm, runid, runstart, nruns, q, yhat, hq, lw, rsmask;
-  DevBuf ocells, fscratch, stats, flag, idx, counters, memo, memo_vals, memo_val, rec, gscr,
-      gqueue, glists, dx, sxx, micscr;
+  DevBuf ocells, stats, flag, idx, counters, memo, memo_vals, memo_val, rec, dx, sxx, micscr;
+  // general tier: the row targets y are independent, so they run on
+  // kYLanes streams at once, each lane with its own scratch set
+  static constexpr int kYLanes = 8;
+  struct YLane {
+    cudaStream_t s = nullptr;
+    cudaEvent_t done = nullptr;
+    DevBuf gscr, gqueue, glists, fscratch;
+  } ylane[kYLanes];
   int memo_n = -1, memo_nval = 0;
   // per-variable state of the previous call (opts.reuse_vars)
   struct Prep {
@@ -235,7 +242,7 @@ cudaEvent_t ctx_event(mine_b200_ctx* ctx, size_t i) {
 
 // Scratch of the general tier for `nsub` subproblems at one row target (the
 // layout depends on y; one buffer is reused across y and chunks).
-GenScratch gen_scratch(mine_b200_ctx* ctx, int n, const YParams& yp, long long nsub) {
+GenScratch gen_scratch(mine_b200_ctx::YLane& ln, int n, const YParams& yp, long long nsub) {
   GenScratch g;
   g.kc = gen_kc(n, yp);
   g.cum_stride = (size_t)yp.y * (g.kc + 1);
@@ -244,18 +251,18 @@ GenScratch gen_scratch(mine_b200_ctx* ctx, int n, const YParams& yp, long long n
   const size_t descb = a16(sizeof(int) * 4 * nsub);
   const size_t cbb = a16(sizeof(int) * (size_t)(g.kc + 1) * nsub);
   const size_t cumb = a16(sizeof(int) * g.cum_stride * nsub);
-  char* base = static_cast<char*>(ctx->gscr.ensure(f2b + descb + cbb + cumb));
+  char* base = static_cast<char*>(ln.gscr.ensure(f2b + descb + cbb + cumb));
   g.f2 = reinterpret_cast<double*>(base);
   g.desc = reinterpret_cast<int*>(base + f2b);
   g.cb = reinterpret_cast<int*>(base + f2b + descb);
   g.cum = reinterpret_cast<int*>(base + f2b + descb + cbb);
-  g.queue = static_cast<unsigned long long*>(ctx->gqueue.ensure(4 * sizeof(unsigned long long)));
+  g.queue = static_cast<unsigned long long*>(ln.gqueue.ensure(4 * sizeof(unsigned long long)));
   g.nsub = nsub;
-  g.lists = static_cast<long long*>(ctx->glists.ensure(2 * sizeof(long long) * (size_t)nsub));
+  g.lists = static_cast<long long*>(ln.glists.ensure(2 * sizeof(long long) * (size_t)nsub));
   g.small_ok = gen_warp_smem_per_warp(yp) <= 24 * 1024;
   if (yp.x_max >= 3)
     g.fslots = static_cast<double*>(
-        ctx->fscratch.ensure(gen_fslot_bytes(n, yp) * (size_t)gen_dp_grid(n, yp)));
+        ln.fscratch.ensure(gen_fslot_bytes(n, yp) * (size_t)gen_dp_grid(n, yp)));
   return g;
 }
 
@@ -458,11 +465,11 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
                       std::to_string(n) + " y=" + std::to_string(yp.y));
       sub_max = std::max(sub_max, gen_scratch_per_sub(n, yp));
     }
-    per_pair += 2 * sub_max;
+    per_pair += 2 * sub_max * std::min<size_t>(mine_b200_ctx::kYLanes, yps.size());
   }
   const long long chunk = small ? (dio ? count : std::min<long long>(count, 1LL << 20))
                                : std::max<long long>(1, std::min<long long>(
-                                     count, (long long)((1024ULL << 20) / per_pair)));
+                                     count, (long long)((4096ULL << 20) / per_pair)));
   const long long nchunks = (count + chunk - 1) / chunk;
   const int nslots = dio ? 1 : 2;  // double-buffered staging for host io
   double* stage = nullptr;
@@ -519,16 +526,34 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
       launch_tiny_pairs(vs, tb, pc, par->c, par->est, so, cells_dst, dcnt, s);
       ++ctx->launches;
     } else {
-      for (const auto& yp : yps) {
-        const GenScratch gs = gen_scratch(ctx, n, yp, 2 * cn);
-        CK(cudaMemsetAsync(gs.queue, 0, 4 * sizeof(unsigned long long), s));
-        launch_part_f2(vs, tb, pc, 0, cn, yp, gs, ocells, nullptr, -1, dcnt, s);
+      // row targets round-robin over the y lanes (y = 2, the heaviest, first);
+      // each lane joins the main stream before the reduction
+      const int nl = (int)std::min<size_t>(mine_b200_ctx::kYLanes, yps.size());
+      CK(cudaEventRecord(ctx_event(ctx, 4), s));
+      for (int j = 0; j < nl; ++j) {
+        auto& ln = ctx->ylane[j];
+        if (!ln.s) {
+          CK(cudaStreamCreateWithFlags(&ln.s, cudaStreamNonBlocking));
+          CK(cudaEventCreateWithFlags(&ln.done, cudaEventDisableTiming));
+        }
+        CK(cudaStreamWaitEvent(ln.s, ctx_event(ctx, 4), 0));
+      }
+      for (size_t i = 0; i < yps.size(); ++i) {
+        const YParams& yp = yps[i];
+        auto& ln = ctx->ylane[i % nl];
+        const GenScratch gs = gen_scratch(ln, n, yp, 2 * cn);
+        CK(cudaMemsetAsync(gs.queue, 0, 4 * sizeof(unsigned long long), ln.s));
+        launch_part_f2(vs, tb, pc, 0, cn, yp, gs, ocells, nullptr, -1, dcnt, ln.s);
         ++ctx->launches;
         if (yp.x_max >= 3) {
-          launch_dp_warp(vs, tb, pc, 0, cn, yp, gs, ocells, nullptr, -1, s);
-          launch_dp(vs, tb, pc, 0, cn, yp, gs, ocells, nullptr, -1, s);
+          launch_dp_warp(vs, tb, pc, 0, cn, yp, gs, ocells, nullptr, -1, ln.s);
+          launch_dp(vs, tb, pc, 0, cn, yp, gs, ocells, nullptr, -1, ln.s);
           ctx->launches += gs.small_ok ? 2 : 1;
         }
+      }
+      for (int j = 0; j < nl; ++j) {
+        CK(cudaEventRecord(ctx->ylane[j].done, ctx->ylane[j].s));
+        CK(cudaStreamWaitEvent(s, ctx->ylane[j].done, 0));
       }
       launch_reduce(tb, cn, ocells, par->est, so, 0, s);
       ++ctx->launches;
@@ -645,6 +670,10 @@ void mine_b200_destroy(mine_b200_ctx* ctx) {
   for (auto e : ctx->events) cudaEventDestroy(e);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->copy) cudaStreamDestroy(ctx->copy);
+  for (auto& ln : ctx->ylane) {
+    if (ln.s) cudaStreamDestroy(ln.s);
+    if (ln.done) cudaEventDestroy(ln.done);
+  }
   delete ctx;
 }
 
@@ -770,7 +799,7 @@ int mine_b200_debug_subproblem(mine_b200_ctx* ctx, int n, const double* col_var,
     dbg.q_x = ib + 3;
     dbg.bounds = ib + 3 + n;
     double* oc = static_cast<double*>(ctx->ocells.ensure(sizeof(double) * 2 * tb.ncell));
-    const GenScratch gs = gen_scratch(ctx, n, yp, 1);
+    const GenScratch gs = gen_scratch(ctx->ylane[0], n, yp, 1);
     CK(cudaMemsetAsync(gs.queue, 0, 4 * sizeof(unsigned long long), s));
     launch_part_f2(vs, tb, ps, 0, 1, yp, gs, oc, &dbg, 0, nullptr, s);
     launch_dp_warp(vs, tb, ps, 0, 1, yp, gs, oc, &dbg, 0, s);
