@@ -739,8 +739,9 @@ __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, 
     f2k = c.val[r];
   } else {
     const double* W2 = c.tab + c.L.w2;
-    const double* R1 = c.tab + c.L.r1;
-    const int* w2r = c.ints + c.L.w2r;
+    // R1[t] = t / n and the W2 row of t are recomputed (FP64 / integer ALU)
+    // instead of gathered: the shared-memory pipe is this kernel's limiter
+    const double dn = (double)n, rn = __drcp_rn(dn);
     const int* sb = c.ints + c.L.sb;
     // Q' = Q + 32768 is staged (unsigned halves); the bias comes off the base
     const uint32_t k2_s = (uint32_t)__cvta_generic_to_shared(K2R) - 32768u;
@@ -792,7 +793,9 @@ __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, 
       const int t = __ffs(ts) - 1;  // t < n <= 31
       const int b0t = __popc(m0 & ((1u << t) - 1u));
       const double f2 = c.val[level(t, b0t, offk[t], nst)];
-      best3 = dmax(best3, __dsub_rn(__dmul_rn(R1[t], f2), W2[w2r[t] + c0 - b0t]));
+      const double r1 = int_quot((double)t, dn, rn);                // == R1[t]
+      const int w2row = t * (n + 1) - ((t * (t - 1)) >> 1);          // == w2_index(n, t, 0)
+      best3 = dmax(best3, __dsub_rn(__dmul_rn(r1, f2), W2[w2row + c0 - b0t]));
       stage(nst, t, b0t);
     }
     f2k = c.val[level(n, c0, offk[n], nst)];
