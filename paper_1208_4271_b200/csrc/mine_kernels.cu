@@ -419,14 +419,12 @@ __host__ __device__ inline MemoLayout memo_layout(int n) {
   // doubles
   L.w2 = 0;
   L.e2 = L.w2 + n * (n + 1) - n * (n - 1) / 2;
-  L.r1 = L.e2 + n + 1;
-  L.pln = L.r1 + n + 1;
+  L.pln = L.e2 + n + 1;
   L.ib = (L.pln + n + 2) & ~1;  // int region starts here (in doubles, 16-byte aligned)
   // ints, relative to the int region
   L.offk = 0;                    // (n + 2)
   // per position t (n + 2 consecutive words each: any gather is conflict-free)
-  L.w2r = L.offk + n + 2;        // first W2 entry of row t
-  L.sb = L.w2r + n + 2;          // staging base word of t (memo_y2)
+  L.sb = L.offk + n + 2;         // staging base word of t (memo_y2)
   L.std3 = L.sb + n + 2;         // 2: standard 3-row totals (C0, C1)
   L.hb = L.std3 + 2;             // uint16 region, relative to the int region
   // uint16 dense candidate ranks, relative to the uint16 region
@@ -474,7 +472,6 @@ __global__ void k_build_memo(Tables tb, double* memo, double* vals, int n) {
   for (int cs = threadIdx.x; cs <= n + 1; cs += blockDim.x) {
     const int g1 = cs * (cs + 1) / 2 - 1;
     const int g2 = cs * (cs + 1) * (2 * cs + 1) / 6 - 1;
-    ints[L.w2r + cs] = cs < n ? w2_index(n, cs, 0) : 0;
     // (P, Q') = (2 g1, 2 (2 g1 - g2) + 32768) as unsigned 16-bit halves; the
     // a0-dependent part is added in memo_y2 (one IMAD)
     ints[L.sb + cs] = cs <= n ? ((2 * g1) << 16) + 2 * (2 * g1 - g2) + 32768 : 0;
@@ -521,7 +518,7 @@ __global__ void k_build_memo(Tables tb, double* memo, double* vals, int n) {
   }
   // T3F[cs][a0][a1] (c_t = n): the whole 3-row F(k,2) candidate for the
   // standard totals -- E2[cs] - (-(((((p a0 + p a1) + p a2) + p b0) + p b1) + p b2)),
-  // the reference's sequence; W2[cs][u0] (c_t = n), E2, R1, PLn
+  // the reference's sequence; W2[cs][u0] (c_t = n), E2, PLn
   for (int cs = threadIdx.x; cs < n; cs += blockDim.x) {
     double acc2 = PL(n, cs);
     acc2 = __dadd_rn(acc2, PL(n, n - cs));
@@ -552,7 +549,6 @@ __global__ void k_build_memo(Tables tb, double* memo, double* vals, int n) {
     double acc2 = PL(n, i);
     acc2 = __dadd_rn(acc2, PL(n, n - i));
     memo[L.e2 + i] = -acc2;
-    memo[L.r1 + i] = __ddiv_rn((double)i, (double)n);
     memo[L.pln + i] = PL(n, i);
   }
 }

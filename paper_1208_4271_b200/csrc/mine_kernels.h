@@ -33,9 +33,9 @@ struct VarSet {
 
 // Memo-tier table layout (offsets in doubles), see mine_kernels.cu.
 struct MemoLayout {
-  // doubles: w2, e2, r1, pln; ints from ib (in doubles): offk, w2r, sb, std3;
+  // doubles: w2, e2, pln; ints from ib (in doubles): offk, sb, std3;
   // uint16 candidate ranks from hb (in ints): k2r, t3r; total in doubles
-  int n, k2cnt, t3cnt, w2, e2, r1, pln, ib, offk, w2r, sb, std3, hb, k2r, t3r, total;
+  int n, k2cnt, t3cnt, w2, e2, pln, ib, offk, sb, std3, hb, k2r, t3r, total;
 };
 
 // Host-built constant tables (glibc libm, the reference's own arithmetic).
