@@ -351,6 +351,14 @@ struct DeviceRecords {
   size_t cap = 0;
 
   DeviceRecords(mine_b200_ctx* ctx, const mine_b200_dataset* ds, long long block) {
+    try {
+      init(ctx, ds, block);
+    } catch (...) {
+      release();
+      throw;
+    }
+  }
+  void init(mine_b200_ctx* ctx, const mine_b200_dataset* ds, long long block) {
     dev = mb200::ctx_device(ctx);
     cuda_check(cudaSetDevice(dev), "cudaSetDevice");
     cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -390,9 +398,13 @@ struct DeviceRecords {
     cuda_check(cudaMallocHost(&h_text, bytes), "cudaMallocHost");
     cap = bytes;
   }
-  ~DeviceRecords() {
+  ~DeviceRecords() { release(); }
+  void release() {
     cudaSetDevice(dev);
-    for (auto p : st) cudaFree(p);
+    for (auto& p : st) {
+      cudaFree(p);
+      p = nullptr;
+    }
     cudaFree(vals);
     cudaFree(names);
     cudaFree(noff);
@@ -404,6 +416,8 @@ struct DeviceRecords {
     cudaFree(text);
     cudaFreeHost(h_text);
     if (s) cudaStreamDestroy(s);
+    vals = nullptr, names = nullptr, noff = nullptr, xi = yi = flag = h_fb = nullptr;
+    scr = nullptr, text = h_text = nullptr, s = nullptr;
   }
 };
 
