@@ -28,8 +28,8 @@ namespace mb200 {
 
 namespace {
 
-constexpr int kPfThreads = 256;
-constexpr int kPfWarps = kPfThreads / 32;
+// k_part_f2 runs 256 threads per subproblem when the F(t,2) level is heavy
+// (x_max >= 3: every t), 128 when only F(k,2) is needed
 #ifndef KDP_THREADS
 #define KDP_THREADS 256
 #endif
@@ -89,7 +89,8 @@ __device__ void write_cells(const Tables& tb, double* ocells, long long pl, int 
 }
 
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kPfThreads, 8) k_part_f2(VarSet vs, Tables tb, PairSpace ps,
+template <int kPfThreads>
+__global__ void __launch_bounds__(kPfThreads, 2048 / kPfThreads) k_part_f2(VarSet vs, Tables tb, PairSpace ps,
                                                         long long base, YParams yp, GenScratch gs,
                                                         double* __restrict__ ocells, SubDebug dbg,
                                                         int has_dbg, int orient_only,
@@ -202,7 +203,7 @@ __global__ void __launch_bounds__(kPfThreads, 8) k_part_f2(VarSet vs, Tables tb,
   __syncthreads();
   for (int t = tid; t < n; t += kPfThreads) atomicAdd(&cum[(lab[t] - 1) * kk + cl[t] + 1], 1);
   __syncthreads();
-  for (int r = warp; r < rows; r += kPfWarps) {
+  for (int r = warp; r < rows; r += (kPfThreads / 32)) {
     int carry = 0;
     for (int j0 = 1; j0 <= k; j0 += 32) {
       const int j = j0 + lane;
@@ -264,7 +265,7 @@ __global__ void __launch_bounds__(kPfThreads, 8) k_part_f2(VarSet vs, Tables tb,
   double* gf2 = gs.f2 + (size_t)sub * (kc + 1);
   if (k >= 2) {
     const int t_lo = l_max >= 3 ? 2 : k;
-    for (int t = t_lo + warp; t <= k; t += kPfWarps) {
+    for (int t = t_lo + warp; t <= k; t += (kPfThreads / 32)) {
       const int ct = cb[t];
       const double* plt = tb.pl + tri(ct);
       double best = kLowest;
@@ -741,7 +742,11 @@ void launch_part_f2(const VarSet& vs, const Tables& tb, const PairSpace& ps, lon
   const unsigned blocks = (unsigned)(npairs * (orient_only >= 0 ? 1 : 2));
   SubDebug d{};
   if (dbg) d = *dbg;
-  k_part_f2<<<blocks, kPfThreads, gen_pf_smem(vs.n, yp), s>>>(vs, tb, ps, base, yp, gs, ocells, d,
+  if (yp.x_max >= 3)
+    k_part_f2<256><<<blocks, 256, gen_pf_smem(vs.n, yp), s>>>(vs, tb, ps, base, yp, gs, ocells, d,
+                                                              dbg ? 1 : 0, orient_only, counters);
+  else
+    k_part_f2<128><<<blocks, 128, gen_pf_smem(vs.n, yp), s>>>(vs, tb, ps, base, yp, gs, ocells, d,
                                                               dbg ? 1 : 0, orient_only, counters);
 }
 
@@ -761,7 +766,8 @@ cudaError_t init_general_attributes(int device) {
   int optin = 0;
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (e != cudaSuccess) return e;
-  const void* fns[] = {reinterpret_cast<const void*>(k_part_f2),
+  const void* fns[] = {reinterpret_cast<const void*>(k_part_f2<256>),
+                       reinterpret_cast<const void*>(k_part_f2<128>),
                        reinterpret_cast<const void*>(k_dp),
                        reinterpret_cast<const void*>(k_dp_warp)};
   for (const void* f : fns) {
