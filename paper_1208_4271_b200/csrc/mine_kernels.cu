@@ -88,8 +88,16 @@ __global__ void k_sort_vars(VarSet vs) {
 // The row map depends only on the row variable, so it is computed
 // once per variable instead of twice per pair.  H(Q) is accumulated with the
 // reference's sequential p*log(p) over rows (mutual_info.cpp:33).
+// One warp per (variable, y).  The greedy scan of equipartition_runs closes
+// the current row before run j iff |in_row + run_j - desired| >=
+// |in_row - desired|, with in_row = rs[j] - rs[row start] growing in j: the
+// test is false ... false, true ... true (also in FP64: exact integers,
+// monotone rounding), so the warp tests 32 runs per step and takes the first
+// true one (ballot) -- the same rows as the sequential scan.  Each closed row
+// is labelled by the whole warp; H(Q) adds the row sizes in row order.
 __global__ void k_equipartition(VarSet vs, Tables tb) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long idx = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (idx >= (long long)vs.V * vs.ny) return;
   const int var = (int)(idx / vs.ny), yi = (int)(idx % vs.ny), y = yi + 2, n = vs.n;
   const int* rs = vs.runstart + (size_t)var * (n + 1);
@@ -98,22 +106,37 @@ __global__ void k_equipartition(VarSet vs, Tables tb) {
   uint16_t* q = vs.q + ((size_t)var * vs.ny + yi) * n;
   const double* pln = tb.pl + tri(n);
   double desired = (double)n / (double)y;
-  int curr = 1, in_row = 0;
+  int curr = 1, r0 = 0, j = 1;  // current row starts at run r0; next run to test j
   double acc = 0.0;
-  for (int r = 0; r < runs; ++r) {
-    const int i = rs[r], j = rs[r + 1], run = j - i;
-    if (in_row != 0 && fabs((double)(in_row + run) - desired) >= fabs((double)in_row - desired)) {
-      acc = __dadd_rn(acc, pln[in_row]);
-      ++curr;
-      in_row = 0;
-      desired = (double)(n - i) / (double)(y - curr + 1);
+  auto label = [&](int r_end) {  // runs [r0, r_end) get label curr
+    for (int t = rs[r0] + lane; t < rs[r_end]; t += 32) q[perm[t]] = (uint16_t)curr;
+  };
+  while (j < runs) {
+    const int jj = j + lane;
+    bool close = false;
+    if (jj < runs) {
+      const int in_row = rs[jj] - rs[r0], run = rs[jj + 1] - rs[jj];
+      close = fabs((double)(in_row + run) - desired) >= fabs((double)in_row - desired);
     }
-    for (int t = i; t < j; ++t) q[perm[t]] = (uint16_t)curr;
-    in_row += run;
+    const unsigned m = __ballot_sync(0xffffffffu, close);
+    if (!m) {
+      j += 32;
+      continue;
+    }
+    const int jc = j + __ffs(m) - 1;  // the next row starts at run jc
+    label(jc);
+    acc = __dadd_rn(acc, pln[rs[jc] - rs[r0]]);
+    ++curr;
+    desired = (double)(n - rs[jc]) / (double)(y - curr + 1);
+    r0 = jc;
+    j = jc + 1;
   }
-  acc = __dadd_rn(acc, pln[in_row]);
-  vs.yhat[idx] = curr;
-  vs.hq[idx] = -acc;
+  label(runs);
+  acc = __dadd_rn(acc, pln[n - rs[r0]]);
+  if (lane == 0) {
+    vs.yhat[idx] = curr;
+    vs.hq[idx] = -acc;
+  }
 }
 
 // Tiny-tier packing: per sample the labels of y=2 and y=3 in one byte, and the
@@ -1049,8 +1072,8 @@ void launch_sort_vars(const VarSet& vs, cudaStream_t s) {
 }
 
 void launch_equipartition(const VarSet& vs, const Tables& tb, cudaStream_t s) {
-  const long long total = (long long)vs.V * vs.ny;
-  k_equipartition<<<(unsigned)((total + 127) / 128), 128, 0, s>>>(vs, tb);
+  const long long warps = (long long)vs.V * vs.ny;
+  k_equipartition<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(vs, tb);
 }
 
 void launch_pack_tiny(const VarSet& vs, cudaStream_t s) {
