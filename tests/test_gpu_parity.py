@@ -378,3 +378,28 @@ def test_span_quotients_match_ieee_division_exhaustively():
     assert L.mine_b200_check_quotients(0, 65535, ctypes.byref(bad), ctypes.byref(cnt)) == 0
     assert cnt.value == 65536 * 65537 // 2 - 1
     assert bad.value == 0
+
+
+@pytest.mark.parametrize("n", [37, 95, 233, 517])
+def test_randomized_batches_bit_exact(engine, oracle, n):
+    """Stress: 1000-pair batches of mixed styles (continuous, tied, monotone,
+    constant, heavy ties), random alpha / c / est, through the batch path (all
+    tiers the auto selection picks, the concurrent y lanes, superclumps),
+    bit-exact against the oracle."""
+    rng = np.random.default_rng(1000 + n)
+    vars_, xi, yi = [], [], []
+    for it in range(1000):
+        style = it % 5
+        if style < 4:
+            x, y = random_pair(rng, n, style)
+        else:
+            x = rng.integers(0, 3, n).astype(float)
+            y = rng.poisson(2.0, n).astype(float)
+        vars_ += [x, y]
+        xi.append(2 * it)
+        yi.append(2 * it + 1)
+    V = np.stack(vars_)
+    for alpha, c, est in [(0.6, 15.0, 0), (float(rng.uniform(0.45, 0.75)), float(rng.choice([1.0, 3.0, 7.5])), 1)]:
+        res = engine.pairs(V, xi, yi, Parameters(alpha, c, est))
+        want = oracle.pairs(V, xi, yi, alpha, c, est)
+        assert_bit_equal(stats_matrix(res), want, f"n={n} alpha={alpha} c={c} est={est}")
