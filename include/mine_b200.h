@@ -113,8 +113,8 @@ typedef struct mine_b200_opts {
    *   counters: host array of MINE_B200_NCOUNTERS realised-work totals
    *             (the reference arithmetic's FP64 ops and p*log(p) lookups, DP
    *             candidates, span entries, subproblems; then the 8-byte and
-   *             rank (2-byte) table gathers the executing tier needs), accumulated
-   *             by the kernels;
+   *             rank (2-byte) table gathers the executing tier needs; then the
+   *             partition's point visits), accumulated by the kernels;
    *   ev_begin / ev_end: cudaEvent_t recorded on the stream around the
    *             pair-scoring kernels (the dominant kernels of a call). */
   unsigned long long* counters;
@@ -127,7 +127,7 @@ typedef struct mine_b200_opts {
    * masters against one Y).  A call whose variables differ fails. */
   int reuse_vars;
 } mine_b200_opts;
-#define MINE_B200_NCOUNTERS 7
+#define MINE_B200_NCOUNTERS 8
 
 /* ---- engine API ---------------------------------------------------------- */
 const char* mine_b200_last_error(void);

@@ -95,9 +95,11 @@ __device__ __forceinline__ void pair_vars(const PairSpace& ps, long long w, int&
 // Realised algorithmic work of one exact subproblem (rows R, k clumps): the
 // FP64 operations the reference arithmetic itself requires (mutual_info.cpp:
 // 47-66 with every 0.0 + x start elided), its p*log(p) lookups, DP candidates
-// and span entries.  Used only when counters are requested.
-__device__ inline void subproblem_work(int R, int k, int x_max, unsigned long long* w,
+// and span entries, and the partition's point visits (n per subproblem,
+// SURVEY 8d N_pv).  Used only when counters are requested.
+__device__ inline void subproblem_work(int R, int k, int x_max, int n, unsigned long long* w,
                                 bool gathers_as_reference = true) {
+  w[kCntPoints] += n;
   if (k < 2) return;
   const long long l_max = min(x_max, k), K = k;
   const long long f2 = l_max >= 3 ? K * (K - 1) / 2 : K - 1;  // F(t,2) candidates

@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kPfThreads, 2048 / kPfThreads) k_part_f2(VarSe
   const int l_max = min(x_max, k);
   if (counters && tid == 0) {
     unsigned long long w[kNumCounters] = {};
-    subproblem_work(rows, k, x_max, w);
+    subproblem_work(rows, k, x_max, n, w);
     for (int i = 0; i < kNumCounters; ++i)
       if (w[i]) atomicAdd(counters + i, w[i]);
   }

@@ -249,7 +249,7 @@ __device__ void tiny_subproblem(const TinyCtx& c, const uint32_t* m, int rows, u
   d &= c.valid & ~1u;
   int k;
   const uint32_t bnd = bits_partition(d, rsm, c.valid, n, k_hat, k);
-  if (work) subproblem_work(rows, k, x_max, work);
+  if (work) subproblem_work(rows, k, x_max, n, work);
   if (k < 2) {
     i2 = 0.0;
     i3 = 0.0;
@@ -733,7 +733,7 @@ __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, 
   int k;
   const uint32_t bnd = bits_partition(d, rsm, c.valid, n, k_hat, k);
   if (work) {
-    subproblem_work(2, k, x_max, work, false);
+    subproblem_work(2, k, x_max, n, work, false);
     if (k >= 2) {
       work[kCntRankGathers] += x_max <= 2 ? k - 1 : k * (k - 1) / 2;  // candidate ranks
       if (x_max > 2) work[kCntGathers] += 2 * (k - 2);          // R1, W2 per span term
@@ -833,7 +833,7 @@ __device__ double memo_y3_rows3(const MemoCtx& c, uint32_t m0, uint32_t m1, uint
   const int c0 = __popc(m0), c1 = __popc(m1);
   const bool standard = c0 == c.std3[0] && c1 == c.std3[1];
   if (work) {
-    subproblem_work(3, k, 2, work, false);
+    subproblem_work(3, k, 2, n, work, false);
     if (k >= 2) {
       if (standard)
         work[kCntRankGathers] += k - 1;  // candidate rank (dense [c_s][a0][a1])

@@ -79,7 +79,7 @@ struct StatsOut {
 // Realised-work counters: algorithmic FP64 ops of the
 // reference arithmetic, p*log(p) lookups, DP candidates, span entries,
 // subproblems.
-enum { kCntFp64 = 0, kCntLookups, kCntCand, kCntSpans, kCntSub, kCntGathers, kCntRankGathers, kNumCounters };
+enum { kCntFp64 = 0, kCntLookups, kCntCand, kCntSpans, kCntSub, kCntGathers, kCntRankGathers, kCntPoints, kNumCounters };
 // kCntGathers / kCntRankGathers: 8-byte / narrow (rank) shared-memory table
 // gathers the executing tier actually needs (memo tier: one 2-byte rank per F(t,2)
 // candidate, ...); the other counters describe the reference's own

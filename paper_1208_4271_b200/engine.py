@@ -42,9 +42,9 @@ class MineStatsOut(ctypes.Structure):
     _fields_ = [(k, _dp) for k in STATS] + [("cells", _dp)] + [(k, _dp) for k in EXTRA_STATS]
 
 
-NCOUNTERS = 7
+NCOUNTERS = 8
 COUNTERS = ("fp64_ops", "lookups", "dp_candidates", "span_entries", "subproblems", "gathers",
-            "rank_gathers")
+            "rank_gathers", "point_visits")
 
 
 class MineOpts(ctypes.Structure):
