@@ -1133,9 +1133,7 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
                        cudaStream_t s) {
   if (ps.count <= 0) return;
   const size_t fixed = memo_smem_fixed(vs.n, nval);
-  size_t budget = 226 * 1024 - fixed;
-  if (const char* e = getenv("MINE_B200_MEMO_SMEM_KB"))
-    budget = std::min<size_t>(budget, atoi(e) * 1024 - fixed);
+  const size_t budget = 226 * 1024 - fixed;
   const size_t row = sizeof(int) * (size_t)memo_scr_stride(vs.n);
   int threads = (int)std::min<size_t>(kMemoMaxThreads, budget / row) / 32 * 32;
   threads = std::max(threads, 32);
