@@ -106,7 +106,7 @@ typedef struct mine_b200_opts {
   int device_io;     /* 1: inputs and outputs are device pointers (HBM-resident) */
   int async;         /* 1 (with device_io): enqueue on `stream` and return */
   void* stream;      /* cudaStream_t or NULL for the context's stream */
-  int tier;          /* 0 auto, 1 tiny (n<=32, B<=7), 2 general, 3 memo (n<=25, B<=7) */
+  int tier;          /* 0 auto, 1 tiny (n<=32, B<=7), 2 general, 3 memo (n<=31, B<=7) */
   long long first;   /* first work item (pairwise/cross/list index) */
   long long count;   /* items to score; <= 0 means all from `first` */
   /* Measurement hooks (bench / profiling), all optional:

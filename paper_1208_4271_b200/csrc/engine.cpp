@@ -318,7 +318,7 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   const bool tiny_ok = n <= 32 && B <= 7;
   const bool memo_pre = memo_fits(n, B, 0);
   if (opts.tier == 1 && !tiny_ok) throw Failure("mine_b200: tiny tier needs n <= 32 and B <= 7");
-  if (opts.tier == 3 && !memo_pre) throw Failure("mine_b200: memo tier needs n <= 24 and B <= 7");
+  if (opts.tier == 3 && !memo_pre) throw Failure("mine_b200: memo tier needs n <= 31 and B <= 7");
   bool memo = memo_pre && (opts.tier == 0 || opts.tier == 3);
 
   ctx->tables.build(n, B, s);

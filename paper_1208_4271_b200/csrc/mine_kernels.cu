@@ -9,7 +9,7 @@
 // Pipeline of one call:
 //   K1 k_sort_vars      per variable: stable rank, tie-run structure       (partition.cpp:13-38)
 //   K2 k_equipartition  per (variable, y): greedy row map Q, yhat, H(Q)      (partition.cpp:42-67, A1)
-//   memo tier  k_memo_pairs   n <= 24, B <= 7 (c1): one thread per pair, tabulated F(t,2) candidates
+//   memo tier  k_memo_pairs   n <= 31, B <= 7 (c1): one thread per pair, tabulated F(t,2) candidates
 //   tiny tier  k_tiny_pairs   n <= 32, B <= 7: one thread per pair, all stages in registers
 //   general    mine_general.cu: k_part_f2 + k_dp per y, then k_reduce here
 //              (max-merge + MIC/MAS/MEV/MCN/MIC_e/TIC, statistics.cpp:10-37)
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(128) k_tiny_pairs(VarSet vs, Tables tb, PairSp
 }
 
 // ---------------------------------------------------------------------------
-// Memo tier (n <= 24, B <= 7; the c1 shape).  With two rows every F(t,2)
+// Memo tier (n <= 31, B <= 7; c1 is n = 23).  With two rows every F(t,2)
 // candidate H(P) - H(P,Q) (mutual_info.cpp:51-52) is a function of (c_t, c_s,
 // a0, b0) only (a1 = c_s - a0, b1 = c_t - c_s - b0), and there are only
 // C(n+4,4)-ish such tuples.  k_build_memo evaluates every candidate ONCE with
@@ -431,6 +431,11 @@ __host__ __device__ __forceinline__ int memo_t3_rs(int n) { return memo_t3_as(n)
 __host__ __device__ __forceinline__ int t3_index(int n, int cs, int a0, int a1) {
   return cs * memo_t3_rs(n) + a0 * memo_t3_as(n) + a1;
 }
+// Compact [c_s][a0][a1] (a0 + a1 <= c_s) for n > 26, where the padded table
+// would crowd the scratch rows out of shared memory.
+__host__ __device__ __forceinline__ int t3_index_c(int cs, int a0, int a1) {
+  return cs * (cs + 1) * (cs + 2) / 6 + a0 * (cs + 1) - a0 * (a0 - 1) / 2 + a1;
+}
 
 __host__ __device__ inline MemoLayout memo_layout(int n) {
   MemoLayout L;
@@ -438,7 +443,9 @@ __host__ __device__ inline MemoLayout memo_layout(int n) {
   for (int ct = 2; ct <= n; ++ct) k2 += memo_G(ct, ct);
   L.n = n;
   L.k2cnt = k2;
-  L.t3cnt = n * memo_t3_rs(n);  // dense [c_s][a0][a1], padded (bank spread)
+  L.t3c = n > 26;
+  L.t3cnt = L.t3c ? n * (n + 1) * (n + 2) / 6  // compact
+                  : n * memo_t3_rs(n);         // dense [c_s][a0][a1], padded (bank spread)
   // doubles
   L.w2 = 0;
   L.e2 = L.w2 + n * (n + 1) - n * (n - 1) / 2;
@@ -545,8 +552,8 @@ __global__ void k_build_memo(Tables tb, double* memo, double* vals, int n) {
   for (int cs = threadIdx.x; cs < n; cs += blockDim.x) {
     double acc2 = PL(n, cs);
     acc2 = __dadd_rn(acc2, PL(n, n - cs));
-    for (int a0 = 0; a0 <= n; ++a0)
-      for (int a1 = 0; a1 <= n; ++a1) {
+    for (int a0 = 0; a0 <= (L.t3c ? cs : n); ++a0)
+      for (int a1 = 0; a1 <= (L.t3c ? cs - a0 : n); ++a1) {
         const int b0 = std3[0] - a0, b1 = std3[1] - a1, b2 = (n - cs) - b0 - b1;
         double v = 0.0;  // unreachable tuple
         if (a0 + a1 <= cs && std3[0] >= 0 && b0 >= 0 && b1 >= 0 && b2 >= 0) {
@@ -558,7 +565,7 @@ __global__ void k_build_memo(Tables tb, double* memo, double* vals, int n) {
           acc = __dadd_rn(acc, PL(n, b2));
           v = __dsub_rn(-acc2, -acc);
         }
-        vals[L.k2cnt + t3_index(n, cs, a0, a1)] = v;
+        vals[L.k2cnt + (L.t3c ? t3_index_c(cs, a0, a1) : t3_index(n, cs, a0, a1))] = v;
       }
     const int m = n - cs;
     for (int u0 = 0; u0 <= m; ++u0) {
@@ -824,6 +831,7 @@ __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, 
 }
 
 // y = 3 with three rows (x_max = 2: F(k,2) only, c_t = n).
+template <bool kT3C>
 __device__ double memo_y3_rows3(const MemoCtx& c, uint32_t m0, uint32_t m1, uint32_t rsm,
                                 int k_hat, double hq, unsigned long long* work) {
   const int n = c.n;
@@ -850,7 +858,8 @@ __device__ double memo_y3_rows3(const MemoCtx& c, uint32_t m0, uint32_t m1, uint
     for (uint32_t s = bnd; s; s &= s - 1) {
       const int cs = __ffs(s) - 1;
       const uint32_t pre = (1u << cs) - 1u;  // c_s < n <= 31
-      r = max(r, T3R[t3_index(n, cs, __popc(m0 & pre), __popc(m1 & pre))]);
+      const int a0 = __popc(m0 & pre), a1 = __popc(m1 & pre);
+      r = max(r, T3R[kT3C ? t3_index_c(cs, a0, a1) : t3_index(n, cs, a0, a1)]);
     }
     best = c.val[r];
   } else {
@@ -885,7 +894,8 @@ __host__ __device__ inline int memo_scr_off(const MemoLayout& L, int nval) {
 }
 
 // kCount: the instrumented (untimed) variant with realised-work counters.
-template <bool kCount>
+// kT3C: the compact 3-row table (MemoLayout::t3c), a compile-time choice
+template <bool kCount, bool kT3C>
 __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Tables tb,
                                                                const double* __restrict__ memo,
                                                                const double* __restrict__ memo_val,
@@ -971,7 +981,7 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
       if (has_y3 && yh3 >= 2) {
         double i2, dummy;
         if (yh3 == 3)
-          i2 = memo_y3_rows3(c, m3a, m3b, rsm, kh3, hq3, wk);
+          i2 = memo_y3_rows3<kT3C>(c, m3a, m3b, rsm, kh3, hq3, wk);
         else
           memo_y2(c, m3a, rsm, 2, kh3, hq3, i2, dummy, wk, scr);
         o[orient][orient ? 1 : 2] = norm_cell(i2, lg[2], lg[yh3]);
@@ -1047,8 +1057,10 @@ cudaError_t init_kernel_attributes(int device) {
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (e != cudaSuccess) return e;
   const void* fns[] = {reinterpret_cast<const void*>(k_sort_vars),
-                       reinterpret_cast<const void*>(k_memo_pairs<false>),
-                       reinterpret_cast<const void*>(k_memo_pairs<true>)};
+                       reinterpret_cast<const void*>(k_memo_pairs<false, false>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, false>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, true>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, true>)};
   for (const void* f : fns) {
     cudaFuncAttributes fa{};
     e = cudaFuncGetAttributes(&fa, f);
@@ -1144,12 +1156,21 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
   const long long need = (ps.count + threads - 1) / threads;
   const unsigned blocks = (unsigned)std::min<long long>(sms, need);
   const MemoLayout L = memo_layout(vs.n);
-  if (counters)
-    k_memo_pairs<true><<<blocks, threads, sm, s>>>(vs, tb, memo, memo_val, nval, L, ps, c, est, out,
-                                                   o_cells, counters);
-  else
-    k_memo_pairs<false><<<blocks, threads, sm, s>>>(vs, tb, memo, memo_val, nval, L, ps, c, est,
-                                                    out, o_cells, nullptr);
+#define MEMO_LAUNCH(CNT, T3C)                                                                  \
+  k_memo_pairs<CNT, T3C><<<blocks, threads, sm, s>>>(vs, tb, memo, memo_val, nval, L, ps, c, est, \
+                                                     out, o_cells, CNT ? counters : nullptr)
+  if (counters) {
+    if (L.t3c)
+      MEMO_LAUNCH(true, true);
+    else
+      MEMO_LAUNCH(true, false);
+  } else {
+    if (L.t3c)
+      MEMO_LAUNCH(false, true);
+    else
+      MEMO_LAUNCH(false, false);
+  }
+#undef MEMO_LAUNCH
 }
 
 void launch_reduce(const Tables& tb, long long npairs, const double* ocells, int est, StatsOut out,

@@ -36,6 +36,7 @@ struct MemoLayout {
   // doubles: w2, e2, pln; ints from ib (in doubles): offk, sb, std3;
   // uint16 candidate ranks from hb (in ints): k2r, t3r; total in doubles
   int n, k2cnt, t3cnt, w2, e2, pln, ib, offk, sb, std3, hb, k2r, t3r, total;
+  int t3c;  // 3-row table compact (n > 26) or padded dense
 };
 
 // Host-built constant tables (glibc libm, the reference's own arithmetic).

@@ -66,12 +66,13 @@ def test_debug_subproblem_bit_exact(engine, oracle, seed):
 
 @pytest.mark.parametrize("tier", [0, 1, 2, 3])
 def test_small_shapes_bit_exact(engine, oracle, tier):
-    """n <= 32, B <= 7: the memo tier (auto / 3, n <= 24), the tiny tier (1)
+    """n <= 32, B <= 7: the memo tier (auto / 3, n <= 31: padded 3-row table
+    up to n = 24, compact above), the tiny tier (1)
     and the general tier (2) must all match the oracle bit for bit, including
     ties, monotone and constant variables and superclumping (small c)."""
     rng = np.random.default_rng(7 + tier)
     for it in range(80):
-        n = int(rng.integers(2, 25 if tier == 3 else 33))
+        n = int(rng.integers(2, 32 if tier == 3 else 33))
         alpha = [0.6, 0.5, 0.55, 0.45][it % 4]
         if grid_bound(n, alpha) > 7:
             alpha = 0.5 if grid_bound(n, 0.5) <= 7 else 0.4
