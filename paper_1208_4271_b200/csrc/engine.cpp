@@ -187,7 +187,7 @@ struct mine_b200_ctx {
   std::mutex mu;
   TableSet tables;
   DevBuf vals, perm, runid, runstart, nruns, q, yhat, hq, lw, rsmask;
-  DevBuf ocells, stats, flag, idx, counters, memo, memo_vals, memo_val, rec, dx, sxx, micscr;
+  DevBuf ocells, stats, flag, idx, counters, memo, memo_vals, memo_val, rec, dx, sxx, micscr, sortscr;
   // general tier: the row targets y are independent, so they run on
   // kYLanes streams at once, each lane with its own scratch set
   static constexpr int kYLanes = 8;
@@ -251,7 +251,9 @@ GenScratch gen_scratch(mine_b200_ctx::YLane& ln, int n, const YParams& yp, long 
   const size_t descb = a16(sizeof(int) * 4 * nsub);
   const size_t cbb = a16(sizeof(int) * (size_t)(g.kc + 1) * nsub);
   const size_t cumb = a16(sizeof(int) * g.cum_stride * nsub);
-  char* base = static_cast<char*>(ln.gscr.ensure(f2b + descb + cbb + cumb));
+  const size_t ptsb = a16(gen_pts_bytes(n, yp) * nsub);
+  char* base = static_cast<char*>(ln.gscr.ensure(f2b + descb + cbb + cumb + ptsb));
+  if (ptsb) g.pts = reinterpret_cast<unsigned char*>(base + f2b + descb + cbb + cumb);
   g.f2 = reinterpret_cast<double*>(base);
   g.desc = reinterpret_cast<int*>(base + f2b);
   g.cb = reinterpret_cast<int*>(base + f2b + descb);
@@ -387,7 +389,7 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   vs.yhat = static_cast<int*>(ctx->yhat.ensure(sizeof(int) * (size_t)V * ny));
   vs.hq = static_cast<double*>(ctx->hq.ensure(sizeof(double) * (size_t)V * ny));
   if (!reuse) {
-    launch_sort_vars(vs, s);
+    CK(launch_sort_vars(vs, ctx->sortscr.ensure(sort_scratch_bytes(V, n)), s));
     launch_equipartition(vs, tb, s);
     ctx->launches += 2;
     P.memo = P.tiny = P.centred = false;
@@ -771,7 +773,7 @@ int mine_b200_debug_subproblem(mine_b200_ctx* ctx, int n, const double* col_var,
     vs.q = static_cast<uint16_t*>(ctx->q.ensure(sizeof(uint16_t) * 2 * vs.ny * n));
     vs.yhat = static_cast<int*>(ctx->yhat.ensure(sizeof(int) * 2 * vs.ny));
     vs.hq = static_cast<double*>(ctx->hq.ensure(sizeof(double) * 2 * vs.ny));
-    launch_sort_vars(vs, s);
+    CK(launch_sort_vars(vs, ctx->sortscr.ensure(sort_scratch_bytes(2, n)), s));
     launch_equipartition(vs, tb, s);
     int hidx[2] = {0, 1};
     int* didx = static_cast<int*>(ctx->idx.ensure(sizeof(int) * 2));

@@ -43,10 +43,14 @@ constexpr int kCells = 8;      // accumulators per thread
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
 struct PfLayout {
-  size_t lab, fused, cl, cb, cnt, misc, total;
+  size_t lab, fused, cl, cb, pts, cnt, misc, total;
 };
 
-__host__ __device__ inline PfLayout pf_layout(int n, int y, int kc) {
+// The per-point arrays (labels, fused flags, clump ids, clump bounds: 11n
+// bytes) sit in shared memory up to n ~ 19000 (alpha 0.6).  Above that they go
+// to a per-subproblem slot in HBM (pts bytes each; kPtsGlobal), and only the
+// cumulative table and the scan scratch stay on chip.  total: shared bytes.
+__host__ __device__ inline PfLayout pf_layout(int n, int y, int kc, bool pts_global) {
   PfLayout L;
   size_t o = 0;
   L.lab = o;
@@ -57,6 +61,8 @@ __host__ __device__ inline PfLayout pf_layout(int n, int y, int kc) {
   o += al16(sizeof(int) * n);
   L.cb = o;
   o += al16(sizeof(int) * (n + 1));
+  L.pts = o;
+  if (pts_global) o = 0;
   L.cnt = o;
   o += al16(sizeof(int) * (size_t)y * (kc + 1));
   L.misc = o;
@@ -89,7 +95,7 @@ __device__ void write_cells(const Tables& tb, double* ocells, long long pl, int 
 }
 
 // ---------------------------------------------------------------------------
-template <int kPfThreads>
+template <int kPfThreads, bool kPtsGlobal>
 __global__ void __launch_bounds__(kPfThreads, 2048 / kPfThreads) k_part_f2(VarSet vs, Tables tb, PairSpace ps,
                                                         long long base, YParams yp, GenScratch gs,
                                                         double* __restrict__ ocells, SubDebug dbg,
@@ -105,11 +111,12 @@ __global__ void __launch_bounds__(kPfThreads, 2048 / kPfThreads) k_part_f2(VarSe
   sub_vars(ps, pl, orient, X, Y);
   const int y = yp.y, yi = yp.yi, x_max = yp.x_max, k_hat = yp.k_hat, kc = gs.kc;
 
-  const PfLayout L = pf_layout(n, y, kc);
-  uint16_t* lab = reinterpret_cast<uint16_t*>(smem + L.lab);
-  uint8_t* fused = smem + L.fused;
-  int* cl = reinterpret_cast<int*>(smem + L.cl);
-  int* cb = reinterpret_cast<int*>(smem + L.cb);
+  const PfLayout L = pf_layout(n, y, kc, kPtsGlobal);
+  unsigned char* pts = kPtsGlobal ? gs.pts + (size_t)sub * L.pts : smem;
+  uint16_t* lab = reinterpret_cast<uint16_t*>(pts + L.lab);
+  uint8_t* fused = pts + L.fused;
+  int* cl = reinterpret_cast<int*>(pts + L.cl);
+  int* cb = reinterpret_cast<int*>(pts + L.cb);
   int* cum = reinterpret_cast<int*>(smem + L.cnt);
   int* misc = reinterpret_cast<int*>(smem + L.misc);
   double* dmisc = reinterpret_cast<double*>(smem + L.misc) + 30;  // ints 0..59 are scan / k scratch
@@ -679,13 +686,24 @@ __global__ void k_build_div(double* div, int n) {
 // ---------------------------------------------------------------------------
 int gen_kc(int n, const YParams& yp) { return std::min(n, yp.k_hat); }
 
+bool gen_pts_global(int n, const YParams& yp) {
+  static const bool force = std::getenv("MINE_B200_PF_GLOBAL") != nullptr;
+  return force || pf_layout(n, yp.y, gen_kc(n, yp), false).total > 200 * 1024;
+}
+
+size_t gen_pts_bytes(int n, const YParams& yp) {
+  return gen_pts_global(n, yp) ? pf_layout(n, yp.y, gen_kc(n, yp), true).pts : 0;
+}
+
 size_t gen_scratch_per_sub(int n, const YParams& yp) {
   const size_t kc = (size_t)gen_kc(n, yp);
   return sizeof(int4) + sizeof(int) * (kc + 1) + sizeof(int) * (size_t)yp.y * (kc + 1) +
-         sizeof(double) * (kc + 1);
+         sizeof(double) * (kc + 1) + gen_pts_bytes(n, yp);
 }
 
-size_t gen_pf_smem(int n, const YParams& yp) { return pf_layout(n, yp.y, gen_kc(n, yp)).total; }
+size_t gen_pf_smem(int n, const YParams& yp) {
+  return pf_layout(n, yp.y, gen_kc(n, yp), gen_pts_global(n, yp)).total;
+}
 
 bool gen_dp_f_in_smem(int, const YParams&) { return false; }
 
@@ -742,12 +760,17 @@ void launch_part_f2(const VarSet& vs, const Tables& tb, const PairSpace& ps, lon
   const unsigned blocks = (unsigned)(npairs * (orient_only >= 0 ? 1 : 2));
   SubDebug d{};
   if (dbg) d = *dbg;
-  if (yp.x_max >= 3)
-    k_part_f2<256><<<blocks, 256, gen_pf_smem(vs.n, yp), s>>>(vs, tb, ps, base, yp, gs, ocells, d,
-                                                              dbg ? 1 : 0, orient_only, counters);
+  const size_t sm = gen_pf_smem(vs.n, yp);
+  const int dg = dbg ? 1 : 0;
+  if (gs.pts)
+    k_part_f2<256, true><<<blocks, 256, sm, s>>>(vs, tb, ps, base, yp, gs, ocells, d, dg,
+                                                 orient_only, counters);
+  else if (yp.x_max >= 3)
+    k_part_f2<256, false><<<blocks, 256, sm, s>>>(vs, tb, ps, base, yp, gs, ocells, d, dg,
+                                                  orient_only, counters);
   else
-    k_part_f2<128><<<blocks, 128, gen_pf_smem(vs.n, yp), s>>>(vs, tb, ps, base, yp, gs, ocells, d,
-                                                              dbg ? 1 : 0, orient_only, counters);
+    k_part_f2<128, false><<<blocks, 128, sm, s>>>(vs, tb, ps, base, yp, gs, ocells, d, dg,
+                                                  orient_only, counters);
 }
 
 void launch_dp(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
@@ -766,8 +789,9 @@ cudaError_t init_general_attributes(int device) {
   int optin = 0;
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (e != cudaSuccess) return e;
-  const void* fns[] = {reinterpret_cast<const void*>(k_part_f2<256>),
-                       reinterpret_cast<const void*>(k_part_f2<128>),
+  const void* fns[] = {reinterpret_cast<const void*>(k_part_f2<256, false>),
+                       reinterpret_cast<const void*>(k_part_f2<128, false>),
+                       reinterpret_cast<const void*>(k_part_f2<256, true>),
                        reinterpret_cast<const void*>(k_dp),
                        reinterpret_cast<const void*>(k_dp_warp)};
   for (const void* f : fns) {

@@ -19,6 +19,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cub/device/device_segmented_radix_sort.cuh>
+
 #include "device_common.cuh"
 #include "mine_kernels.h"
 
@@ -76,6 +78,48 @@ __global__ void k_sort_vars(VarSet vs) {
     const int r = rs[i] - 1;
     runid[i] = r;
     if (i == 0 || rs[i - 1] != rs[i]) rstart[r] = i;
+  }
+  if (threadIdx.x == 0) {
+    rstart[runs] = n;
+    vs.nruns[var] = runs;
+  }
+}
+
+// K1 for large n (the 12n-byte working set of k_sort_vars no longer fits on
+// chip, or the O(n^2) ranking costs more than a sort): a stable segmented
+// radix sort of order-preserving 64-bit keys (cub), then the tie-run scan.
+// -0.0 is keyed as +0.0 (C++ ==), NaN as +inf, as in k_sort_vars.
+__device__ __forceinline__ unsigned long long order_key(double x) {
+  if (isnan(x)) x = HUGE_VAL;
+  if (x == 0.0) x = 0.0;
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+__global__ void k_sort_keys(VarSet vs, unsigned long long* keys, int* idx, int* offs) {
+  const long long total = (long long)vs.V * vs.n;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    keys[i] = order_key(vs.vals[i]);
+    idx[i] = (int)(i % vs.n);
+    if (i % vs.n == 0) offs[i / vs.n] = (int)i;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) offs[vs.V] = (int)total;
+}
+
+__global__ void k_sorted_runs(VarSet vs, const unsigned long long* skeys) {
+  __shared__ int tmp[32];
+  const int n = vs.n, var = blockIdx.x;
+  const unsigned long long* k = skeys + (size_t)var * n;
+  int* runid = vs.runid + (size_t)var * n;
+  int* rstart = vs.runstart + (size_t)var * (n + 1);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) runid[i] = i == 0 || k[i] != k[i - 1];
+  __syncthreads();
+  const int runs = block_incl_scan(runid, n, tmp);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int r = runid[i] - 1;  // each thread touches only its own entries
+    runid[i] = r;
+    if (i == 0 || k[i] != k[i - 1]) rstart[r] = i;
   }
   if (threadIdx.x == 0) {
     rstart[runs] = n;
@@ -1077,10 +1121,50 @@ void launch_check_finite(const double* v, long long count, int* flag, cudaStream
   k_check_finite<<<blocks, 256, 0, s>>>(v, count, flag);
 }
 
-void launch_sort_vars(const VarSet& vs, cudaStream_t s) {
-  const int threads = vs.n <= 256 ? 128 : (vs.n <= 2048 ? 256 : 1024);
-  const size_t sm = sizeof(double) * vs.n + sizeof(int) * (vs.n + 64);
-  k_sort_vars<<<vs.V, threads, sm, s>>>(vs);
+static bool radix_sort_vars(int n) {
+  static const char* force = std::getenv("MINE_B200_RADIX_SORT");
+  if (force) return force[0] == '1';
+  return n > kRadixSortN;
+}
+
+static size_t cub_sort_bytes(int V, int n) {
+  size_t tmp = 0;
+  cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, (const unsigned long long*)nullptr,
+                                           (unsigned long long*)nullptr, (const int*)nullptr,
+                                           (int*)nullptr, (long long)V * n, V, (const int*)nullptr,
+                                           (const int*)nullptr);
+  return tmp;
+}
+
+size_t sort_scratch_bytes(int V, int n) {
+  if (!radix_sort_vars(n)) return 0;
+  const size_t items = (size_t)V * n;
+  return 2 * 8 * items + 4 * items + 4 * (size_t)(V + 1) + 3 * 256 + cub_sort_bytes(V, n);
+}
+
+cudaError_t launch_sort_vars(const VarSet& vs, void* scratch, cudaStream_t s) {
+  if (!radix_sort_vars(vs.n)) {
+    const int threads = vs.n <= 256 ? 128 : (vs.n <= 2048 ? 256 : 1024);
+    const size_t sm = sizeof(double) * vs.n + sizeof(int) * (vs.n + 64);
+    k_sort_vars<<<vs.V, threads, sm, s>>>(vs);
+    return cudaGetLastError();
+  }
+  const size_t items = (size_t)vs.V * vs.n;
+  auto a256 = [](size_t x) { return (x + 255) & ~size_t(255); };
+  char* p = static_cast<char*>(scratch);
+  auto* kin = reinterpret_cast<unsigned long long*>(p);
+  auto* kout = reinterpret_cast<unsigned long long*>(p + a256(8 * items));
+  int* idx = reinterpret_cast<int*>(p + 2 * a256(8 * items));
+  int* offs = reinterpret_cast<int*>(p + 2 * a256(8 * items) + a256(4 * items));
+  void* tmp = p + 2 * a256(8 * items) + a256(4 * items) + a256(4 * (size_t)(vs.V + 1));
+  const unsigned blocks = (unsigned)std::min<size_t>(4 * 148, (items + 255) / 256);
+  k_sort_keys<<<blocks, 256, 0, s>>>(vs, kin, idx, offs);
+  size_t tb = cub_sort_bytes(vs.V, vs.n);
+  cudaError_t e = cub::DeviceSegmentedRadixSort::SortPairs(
+      tmp, tb, kin, kout, idx, vs.perm, (long long)items, vs.V, offs, offs + 1, 0, 64, s);
+  if (e != cudaSuccess) return e;
+  k_sorted_runs<<<vs.V, 1024, 0, s>>>(vs, kout);
+  return cudaGetLastError();
 }
 
 void launch_equipartition(const VarSet& vs, const Tables& tb, cudaStream_t s) {

@@ -106,7 +106,11 @@ struct SubDebug {
 // Must run once per device (under a lock) before any launch.
 cudaError_t init_kernel_attributes(int device);
 void launch_check_finite(const double* v, long long count, int* flag, cudaStream_t s);
-void launch_sort_vars(const VarSet& vs, cudaStream_t s);
+// K1: k_sort_vars (on chip, O(n^2) ranking) up to kRadixSortN samples, a
+// segmented radix sort above (scratch: sort_scratch_bytes, 0 below the limit)
+constexpr int kRadixSortN = 16384;
+size_t sort_scratch_bytes(int V, int n);
+cudaError_t launch_sort_vars(const VarSet& vs, void* scratch, cudaStream_t s);
 void launch_equipartition(const VarSet& vs, const Tables& tb, cudaStream_t s);
 void launch_pack_tiny(const VarSet& vs, cudaStream_t s);
 
@@ -146,6 +150,7 @@ struct GenScratch {
   int kc = 0;                 // min(n, k_hat)
   size_t cum_stride = 0;      // y * (kc+1)
   int small_ok = 0;           // the warp path is available at this y
+  unsigned char* pts = nullptr;  // nsub x gen_pts_bytes per-point arrays (large n), or null
 };
 constexpr int kSmallK = 64;   // subproblems with k <= kSmallK take the warp path
 size_t gen_warp_smem_per_warp(const YParams& yp);
@@ -154,6 +159,7 @@ void launch_dp_warp(const VarSet& vs, const Tables& tb, const PairSpace& ps, lon
                     const SubDebug* dbg, int orient_only, cudaStream_t s);
 int gen_kc(int n, const YParams& yp);
 size_t gen_scratch_per_sub(int n, const YParams& yp);
+size_t gen_pts_bytes(int n, const YParams& yp);  // 0: the point arrays fit on chip
 size_t gen_pf_smem(int n, const YParams& yp);
 size_t gen_dp_smem(int n, const YParams& yp);
 bool gen_dp_f_in_smem(int n, const YParams& yp);

@@ -404,3 +404,53 @@ def test_randomized_batches_bit_exact(engine, oracle, n):
         res = engine.pairs(V, xi, yi, Parameters(alpha, c, est))
         want = oracle.pairs(V, xi, yi, alpha, c, est)
         assert_bit_equal(stats_matrix(res), want, f"n={n} alpha={alpha} c={c} est={est}")
+
+
+@pytest.mark.parametrize("n,alpha", [(30000, 0.45), (65535, 0.4)])
+def test_large_n_point_arrays_in_hbm(engine, oracle, n, alpha):
+    """Above n ~ 19000 (alpha 0.6) the partition stage's per-point arrays no
+    longer fit in shared memory and move to an HBM slot per subproblem
+    (k_part_f2<.., kPtsGlobal>).  Bit-exact up to the ABI's n limit, 65535."""
+    rng = np.random.default_rng(n)
+    vars_ = []
+    for style in range(4):
+        vars_ += list(random_pair(rng, n, style))
+    x = rng.uniform(0, 6, n)
+    vars_ += [x, np.sin(x) + rng.normal(0, 0.3, n)]
+    V = np.stack(vars_)
+    xi, yi = list(range(0, 10, 2)), list(range(1, 10, 2))
+    for c, est in [(15.0, 0), (2.0, 1)]:
+        res = engine.pairs(V, xi, yi, Parameters(alpha, c, est))
+        want = oracle.pairs(V, xi, yi, alpha, c, est)
+        assert_bit_equal(stats_matrix(res), want, f"n={n} c={c}")
+
+
+def test_point_arrays_in_hbm_forced(tmp_path):
+    """The HBM variant of the partition stage, forced at small n
+    (MINE_B200_PF_GLOBAL, read once per process) on a mixed 600-pair batch."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys\n"
+        "sys.path[:0] = ['tests', 'oracle', '.']\n"
+        "from conftest import random_pair, bits\n"
+        "import oracle as O\n"
+        "from paper_1208_4271_b200 import Engine, Parameters\n"
+        "rng = np.random.default_rng(5)\n"
+        "vs = []\n"
+        "for it in range(600):\n"
+        "    vs += list(random_pair(rng, 300, it % 4))\n"
+        "V = np.stack(vs); xi = list(range(0, 1200, 2)); yi = list(range(1, 1200, 2))\n"
+        "e = Engine(0)\n"
+        "for a, c, est in [(0.6, 15.0, 0), (0.7, 3.0, 1)]:\n"
+        "    r = e.pairs(V, xi, yi, Parameters(a, c, est))\n"
+        "    got = np.stack([r[k] for k in ['mic', 'mas', 'mev', 'mcn', 'mic_e', 'tic']], axis=1)\n"
+        "    want = O.Oracle().pairs(V, xi, yi, a, c, est)\n"
+        "    assert (bits(got) == bits(want)).all(), (a, c)\n"
+        "print('OK')\n")
+    env = dict(os.environ, MINE_B200_PF_GLOBAL="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and "OK" in out.stdout, out.stderr[-2000:]
