@@ -254,6 +254,7 @@ GenScratch gen_scratch(mine_b200_ctx::YLane& ln, int n, const YParams& yp, long 
   const size_t ptsb = a16(gen_pts_bytes(n, yp) * nsub);
   char* base = static_cast<char*>(ln.gscr.ensure(f2b + descb + cbb + cumb + ptsb));
   if (ptsb) g.pts = reinterpret_cast<unsigned char*>(base + f2b + descb + cbb + cumb);
+  g.tables_global = gen_tables_global(n, yp);
   g.f2 = reinterpret_cast<double*>(base);
   g.desc = reinterpret_cast<int*>(base + f2b);
   g.cb = reinterpret_cast<int*>(base + f2b + descb);

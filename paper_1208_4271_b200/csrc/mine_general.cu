@@ -49,8 +49,12 @@ struct PfLayout {
 // The per-point arrays (labels, fused flags, clump ids, clump bounds: 11n
 // bytes) sit in shared memory up to n ~ 19000 (alpha 0.6).  Above that they go
 // to a per-subproblem slot in HBM (pts bytes each; kPtsGlobal), and only the
-// cumulative table and the scan scratch stay on chip.  total: shared bytes.
-__host__ __device__ inline PfLayout pf_layout(int n, int y, int kc, bool pts_global) {
+// cumulative table and the scan scratch stay on chip.  When even the
+// cumulative table y (kc+1) ints is too big (c B large), it is built in place
+// in the subproblem's GenScratch slot (kCumGlobal, which implies kPtsGlobal).
+// total: shared bytes.
+__host__ __device__ inline PfLayout pf_layout(int n, int y, int kc, bool pts_global,
+                                              bool cum_global = false) {
   PfLayout L;
   size_t o = 0;
   L.lab = o;
@@ -64,7 +68,7 @@ __host__ __device__ inline PfLayout pf_layout(int n, int y, int kc, bool pts_glo
   L.pts = o;
   if (pts_global) o = 0;
   L.cnt = o;
-  o += al16(sizeof(int) * (size_t)y * (kc + 1));
+  if (!cum_global) o += al16(sizeof(int) * (size_t)y * (kc + 1));
   L.misc = o;
   o += al16(sizeof(double) * 40);
   L.total = o;
@@ -95,7 +99,7 @@ __device__ void write_cells(const Tables& tb, double* ocells, long long pl, int 
 }
 
 // ---------------------------------------------------------------------------
-template <int kPfThreads, bool kPtsGlobal>
+template <int kPfThreads, bool kPtsGlobal, bool kCumGlobal>
 __global__ void __launch_bounds__(kPfThreads, 2048 / kPfThreads) k_part_f2(VarSet vs, Tables tb, PairSpace ps,
                                                         long long base, YParams yp, GenScratch gs,
                                                         double* __restrict__ ocells, SubDebug dbg,
@@ -111,13 +115,14 @@ __global__ void __launch_bounds__(kPfThreads, 2048 / kPfThreads) k_part_f2(VarSe
   sub_vars(ps, pl, orient, X, Y);
   const int y = yp.y, yi = yp.yi, x_max = yp.x_max, k_hat = yp.k_hat, kc = gs.kc;
 
-  const PfLayout L = pf_layout(n, y, kc, kPtsGlobal);
+  const PfLayout L = pf_layout(n, y, kc, kPtsGlobal, kCumGlobal);
   unsigned char* pts = kPtsGlobal ? gs.pts + (size_t)sub * L.pts : smem;
   uint16_t* lab = reinterpret_cast<uint16_t*>(pts + L.lab);
   uint8_t* fused = pts + L.fused;
   int* cl = reinterpret_cast<int*>(pts + L.cl);
   int* cb = reinterpret_cast<int*>(pts + L.cb);
-  int* cum = reinterpret_cast<int*>(smem + L.cnt);
+  int* cum = kCumGlobal ? gs.cum + (size_t)sub * gs.cum_stride
+                        : reinterpret_cast<int*>(smem + L.cnt);
   int* misc = reinterpret_cast<int*>(smem + L.misc);
   double* dmisc = reinterpret_cast<double*>(smem + L.misc) + 30;  // ints 0..59 are scan / k scratch
 
@@ -256,7 +261,8 @@ __global__ void __launch_bounds__(kPfThreads, 2048 / kPfThreads) k_part_f2(VarSe
     int* gcb = gs.cb + (size_t)sub * (kc + 1);
     int* gcum = gs.cum + (size_t)sub * gs.cum_stride;
     for (int j = tid; j <= k; j += kPfThreads) gcb[j] = cb[j];
-    for (int i = tid; i < rows * kk; i += kPfThreads) gcum[i] = cum[i];
+    if (!kCumGlobal)
+      for (int i = tid; i < rows * kk; i += kPfThreads) gcum[i] = cum[i];
   } else if (tid == 0) {
     int4 d;
     d.x = k;
@@ -301,6 +307,12 @@ __global__ void __launch_bounds__(kPfThreads, 2048 / kPfThreads) k_part_f2(VarSe
 }
 
 // ---------------------------------------------------------------------------
+constexpr int kFRing = 128;  // F row ring width above 128 levels (power of two >= 65)
+__host__ __device__ inline int fring_width(int LW) { return LW > kFRing ? kFRing : LW; }
+__host__ __device__ inline size_t fslot_doubles(int kc, int LW) {
+  return (size_t)(kc + 1) * fring_width(LW) + (LW > kFRing ? LW : 0);
+}
+
 struct DpLayout {
   size_t cb, cum, A, W, acc, fs, ft, total;
 };
@@ -308,13 +320,15 @@ struct DpLayout {
 constexpr int kFsW = 64;       // staged F row width (levels l0-1 .. l1-1)
 constexpr int kFtW = 65;       // tile F row width (levels l0-1 .. l1)
 
-__host__ __device__ inline DpLayout dp_layout(int y, int kc) {
+// kGlobalTables: cb and cum are read in place from the subproblem's
+// GenScratch slot instead of being staged (for c B too large for the chip).
+__host__ __device__ inline DpLayout dp_layout(int y, int kc, bool global_tables = false) {
   DpLayout L;
   size_t o = 0;
   L.cb = o;
-  o += al16(sizeof(int) * (kc + 1));
+  if (!global_tables) o += al16(sizeof(int) * (kc + 1));
   L.cum = o;
-  o += al16(sizeof(int) * (size_t)y * (kc + 1));
+  if (!global_tables) o += al16(sizeof(int) * (size_t)y * (kc + 1));
   L.A = o;
   o += al16(sizeof(double) * kMaxTile * kMaxTile);
   L.W = o;
@@ -398,6 +412,7 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 // F lives in a per-CTA HBM slot (L2-resident for typical sizes); each outer
 // s-chunk's rows are staged into shared memory with coalesced loads, and the
 // current t-tile's rows are kept in shared memory while its inner part runs.
+template <bool kGlobalTables, bool kRing>
 __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, PairSpace ps,
                                                       long long base, long long nsub, YParams yp,
                                                       GenScratch gs, double* __restrict__ ocells,
@@ -406,7 +421,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
   __shared__ long long s_sub;
   const int tid = threadIdx.x;
   const int y = yp.y, x_max = yp.x_max, kc = gs.kc, LW = x_max - 1;
-  const DpLayout L = dp_layout(y, kc);
+  const DpLayout L = dp_layout(y, kc, kGlobalTables);
   int* cb = reinterpret_cast<int*>(smem + L.cb);
   int* cum = reinterpret_cast<int*>(smem + L.cum);
   double* A = reinterpret_cast<double*>(smem + L.A);
@@ -414,7 +429,13 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
   double* accS = reinterpret_cast<double*>(smem + L.acc);
   double* fs = reinterpret_cast<double*>(smem + L.fs);
   double* ft = reinterpret_cast<double*>(smem + L.ft);
-  double* F = gs.fslots + (size_t)blockIdx.x * (size_t)(kc + 1) * LW;
+  // F(t, l) at column l - 2 of row t; above 128 levels the row is a ring of
+  // 128 columns (a level tile reads l0-1 .. l1-1 and writes l0 .. l1, 65
+  // columns), and F(k, .) -- all of which I_l needs -- is kept in its own row fk
+  // (kRing: x_max > 129 only).
+  const int RW = kRing ? fring_width(LW) : LW, cm = kRing ? kFRing - 1 : 0x7fffffff;
+  double* F = gs.fslots + (size_t)blockIdx.x * fslot_doubles(kc, LW);
+  double* fk = F + (size_t)(kc + 1) * RW;
   const int norient = orient_only >= 0 ? 1 : 2;
 
   for (;;) {
@@ -435,9 +456,15 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
       const int* gcb = gs.cb + (size_t)sub * (kc + 1);
       const int* gcum = gs.cum + (size_t)sub * gs.cum_stride;
       const double* gf2 = gs.f2 + (size_t)sub * (kc + 1);
-      for (int j = tid; j <= k; j += kDpThreads) cb[j] = gcb[j];
-      for (int i = tid; i < rows * kk; i += kDpThreads) cum[i] = gcum[i];
-      for (int t = 2 + tid; t <= k; t += kDpThreads) F[(size_t)t * LW] = gf2[t];
+      if (kGlobalTables) {
+        cb = const_cast<int*>(gcb);
+        cum = const_cast<int*>(gcum);
+      } else {
+        for (int j = tid; j <= k; j += kDpThreads) cb[j] = gcb[j];
+        for (int i = tid; i < rows * kk; i += kDpThreads) cum[i] = gcum[i];
+      }
+      for (int t = 2 + tid; t <= k; t += kDpThreads) F[(size_t)t * RW] = gf2[t];
+      if (kRing && tid == 0) fk[0] = gf2[k];
     }
     __syncthreads();
 
@@ -466,7 +493,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
           span_terms(tb, cb, cum, kk, rows, k, s0, ns, t0, nt, A, W);
           for (int i = tid; i < ns * nl; i += kDpThreads) {  // stage F(s, l0-1 .. l1-1)
             const int sl = i / nl, j = i - sl * nl;
-            fs[sl * kFsW + j] = F[(size_t)(s0 + sl) * LW + (l0 - 3) + j];
+            fs[sl * kFsW + j] = F[(size_t)(s0 + sl) * RW + (((l0 - 3) + j) & cm)];
           }
           __syncthreads();
           if (owner) {
@@ -511,7 +538,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
         // thread; only the warps holding levels take part (named barrier).
         span_terms(tb, cb, cum, kk, rows, k, t0, nt, t0, nt, A, W);
         for (int tl = tid; tl < nt; tl += kDpThreads)  // column 0: level l0 - 1
-          ft[tl * kFtW] = F[(size_t)(t0 + tl) * LW + (l0 - 3)];
+          ft[tl * kFtW] = F[(size_t)(t0 + tl) * RW + ((l0 - 3) & cm)];
         __syncthreads();
         if (tid < inner_threads) {
           const int ll = tid, l = l0 + ll;
@@ -528,7 +555,8 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
                                       Wp[sl * kMaxTile]));
               }
               ft[tl * kFtW + ll + 1] = m;
-              F[(size_t)tt * LW + (l - 2)] = m;
+              F[(size_t)tt * RW + ((l - 2) & cm)] = m;
+              if (kRing && tt == k) fk[l - 2] = m;
             }
             named_sync(1, inner_threads);
           }
@@ -544,7 +572,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
         tb, ocells, pl, orient, y, x_max, rows,
         [&](int l) {
           const int le = l <= l_max ? l : l_max;
-          return dmax(0.0, __dadd_rn(hq, F[(size_t)k * LW + (le - 2)]));
+          return dmax(0.0, __dadd_rn(hq, kRing ? fk[le - 2] : F[(size_t)k * RW + (le - 2)]));
         },
         dbg, has_dbg != 0);
   }
@@ -686,9 +714,15 @@ __global__ void k_build_div(double* div, int n) {
 // ---------------------------------------------------------------------------
 int gen_kc(int n, const YParams& yp) { return std::min(n, yp.k_hat); }
 
+bool gen_tables_global(int n, const YParams& yp) {
+  static const bool force = std::getenv("MINE_B200_DP_GLOBAL") != nullptr;
+  return force || dp_layout(yp.y, gen_kc(n, yp), false).total > 200 * 1024;
+}
+
 bool gen_pts_global(int n, const YParams& yp) {
   static const bool force = std::getenv("MINE_B200_PF_GLOBAL") != nullptr;
-  return force || pf_layout(n, yp.y, gen_kc(n, yp), false).total > 200 * 1024;
+  return force || gen_tables_global(n, yp) ||
+         pf_layout(n, yp.y, gen_kc(n, yp), false).total > 200 * 1024;
 }
 
 size_t gen_pts_bytes(int n, const YParams& yp) {
@@ -702,15 +736,17 @@ size_t gen_scratch_per_sub(int n, const YParams& yp) {
 }
 
 size_t gen_pf_smem(int n, const YParams& yp) {
-  return pf_layout(n, yp.y, gen_kc(n, yp), gen_pts_global(n, yp)).total;
+  return pf_layout(n, yp.y, gen_kc(n, yp), gen_pts_global(n, yp), gen_tables_global(n, yp)).total;
 }
 
 bool gen_dp_f_in_smem(int, const YParams&) { return false; }
 
-size_t gen_dp_smem(int n, const YParams& yp) { return dp_layout(yp.y, gen_kc(n, yp)).total; }
+size_t gen_dp_smem(int n, const YParams& yp) {
+  return dp_layout(yp.y, gen_kc(n, yp), gen_tables_global(n, yp)).total;
+}
 
 size_t gen_fslot_bytes(int n, const YParams& yp) {
-  return sizeof(double) * (size_t)(gen_kc(n, yp) + 1) * (yp.x_max - 1);
+  return sizeof(double) * fslot_doubles(gen_kc(n, yp), yp.x_max - 1);
 }
 
 int gen_dp_grid(int n, const YParams& yp) {
@@ -719,7 +755,9 @@ int gen_dp_grid(int n, const YParams& yp) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t sm = gen_dp_smem(n, yp);
   const int per = (int)std::max<size_t>(1, std::min<size_t>(512 / kDpThreads * 2, (228 * 1024) / (sm + 1024)));
-  return sms * per;
+  // the F slots of one lane stay within 4 GB (very large c B)
+  const long long cap = std::max<long long>(1, (4LL << 30) / (long long)gen_fslot_bytes(n, yp));
+  return (int)std::min<long long>((long long)sms * per, cap);
 }
 
 size_t gen_warp_smem_per_warp(const YParams& yp) { return warp_layout(yp.y, yp.x_max).per_warp; }
@@ -762,15 +800,18 @@ void launch_part_f2(const VarSet& vs, const Tables& tb, const PairSpace& ps, lon
   if (dbg) d = *dbg;
   const size_t sm = gen_pf_smem(vs.n, yp);
   const int dg = dbg ? 1 : 0;
-  if (gs.pts)
-    k_part_f2<256, true><<<blocks, 256, sm, s>>>(vs, tb, ps, base, yp, gs, ocells, d, dg,
-                                                 orient_only, counters);
+  if (gs.tables_global)
+    k_part_f2<256, true, true><<<blocks, 256, sm, s>>>(vs, tb, ps, base, yp, gs, ocells, d, dg,
+                                                       orient_only, counters);
+  else if (gs.pts)
+    k_part_f2<256, true, false><<<blocks, 256, sm, s>>>(vs, tb, ps, base, yp, gs, ocells, d, dg,
+                                                        orient_only, counters);
   else if (yp.x_max >= 3)
-    k_part_f2<256, false><<<blocks, 256, sm, s>>>(vs, tb, ps, base, yp, gs, ocells, d, dg,
-                                                  orient_only, counters);
+    k_part_f2<256, false, false><<<blocks, 256, sm, s>>>(vs, tb, ps, base, yp, gs, ocells, d, dg,
+                                                         orient_only, counters);
   else
-    k_part_f2<128, false><<<blocks, 128, sm, s>>>(vs, tb, ps, base, yp, gs, ocells, d, dg,
-                                                  orient_only, counters);
+    k_part_f2<128, false, false><<<blocks, 128, sm, s>>>(vs, tb, ps, base, yp, gs, ocells, d, dg,
+                                                         orient_only, counters);
 }
 
 void launch_dp(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
@@ -781,18 +822,30 @@ void launch_dp(const VarSet& vs, const Tables& tb, const PairSpace& ps, long lon
   const int grid = (int)std::min<long long>(nsub, gen_dp_grid(vs.n, yp));
   SubDebug d{};
   if (dbg) d = *dbg;
-  k_dp<<<grid, kDpThreads, gen_dp_smem(vs.n, yp), s>>>(vs, tb, ps, base, nsub, yp, gs, ocells, d,
-                                                      dbg ? 1 : 0, orient_only);
+  const size_t sm = gen_dp_smem(vs.n, yp);
+  const int dg = dbg ? 1 : 0;
+  if (gs.tables_global)
+    k_dp<true, true><<<grid, kDpThreads, sm, s>>>(vs, tb, ps, base, nsub, yp, gs, ocells, d, dg,
+                                                  orient_only);
+  else if (yp.x_max - 1 > kFRing)
+    k_dp<false, true><<<grid, kDpThreads, sm, s>>>(vs, tb, ps, base, nsub, yp, gs, ocells, d, dg,
+                                                   orient_only);
+  else
+    k_dp<false, false><<<grid, kDpThreads, sm, s>>>(vs, tb, ps, base, nsub, yp, gs, ocells, d, dg,
+                                                    orient_only);
 }
 
 cudaError_t init_general_attributes(int device) {
   int optin = 0;
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (e != cudaSuccess) return e;
-  const void* fns[] = {reinterpret_cast<const void*>(k_part_f2<256, false>),
-                       reinterpret_cast<const void*>(k_part_f2<128, false>),
-                       reinterpret_cast<const void*>(k_part_f2<256, true>),
-                       reinterpret_cast<const void*>(k_dp),
+  const void* fns[] = {reinterpret_cast<const void*>(k_part_f2<256, false, false>),
+                       reinterpret_cast<const void*>(k_part_f2<128, false, false>),
+                       reinterpret_cast<const void*>(k_part_f2<256, true, false>),
+                       reinterpret_cast<const void*>(k_part_f2<256, true, true>),
+                       reinterpret_cast<const void*>(k_dp<false, false>),
+                       reinterpret_cast<const void*>(k_dp<false, true>),
+                       reinterpret_cast<const void*>(k_dp<true, true>),
                        reinterpret_cast<const void*>(k_dp_warp)};
   for (const void* f : fns) {
     cudaFuncAttributes fa{};

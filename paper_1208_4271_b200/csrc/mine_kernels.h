@@ -151,6 +151,7 @@ struct GenScratch {
   size_t cum_stride = 0;      // y * (kc+1)
   int small_ok = 0;           // the warp path is available at this y
   unsigned char* pts = nullptr;  // nsub x gen_pts_bytes per-point arrays (large n), or null
+  int tables_global = 0;      // cb / cum used in place from this scratch (c B too large)
 };
 constexpr int kSmallK = 64;   // subproblems with k <= kSmallK take the warp path
 size_t gen_warp_smem_per_warp(const YParams& yp);
@@ -160,6 +161,7 @@ void launch_dp_warp(const VarSet& vs, const Tables& tb, const PairSpace& ps, lon
 int gen_kc(int n, const YParams& yp);
 size_t gen_scratch_per_sub(int n, const YParams& yp);
 size_t gen_pts_bytes(int n, const YParams& yp);  // 0: the point arrays fit on chip
+bool gen_tables_global(int n, const YParams& yp);
 size_t gen_pf_smem(int n, const YParams& yp);
 size_t gen_dp_smem(int n, const YParams& yp);
 bool gen_dp_f_in_smem(int n, const YParams& yp);

@@ -425,9 +425,42 @@ def test_large_n_point_arrays_in_hbm(engine, oracle, n, alpha):
         assert_bit_equal(stats_matrix(res), want, f"n={n} c={c}")
 
 
-def test_point_arrays_in_hbm_forced(tmp_path):
-    """The HBM variant of the partition stage, forced at small n
-    (MINE_B200_PF_GLOBAL, read once per process) on a mixed 600-pair batch."""
+def test_many_levels_f_ring(engine, oracle):
+    """x_max > 128 with k > 128: k_dp's F rows become a 128-column ring and
+    F(k, .) its own row (n = 1500, alpha = 0.8: B = 346, x_max = 173 at y = 2)."""
+    n = 1500
+    rng = np.random.default_rng(12)
+    x = rng.uniform(0, 6, n)
+    V = np.stack([x, np.sin(x) + rng.normal(0, 0.2, n), rng.uniform(-1, 1, n),
+                  np.round(x * 20) + rng.integers(0, 2, n)])
+    xi, yi = [0, 0, 3, 2], [1, 3, 1, 0]
+    for c in (15.0, 4.0):
+        res = engine.pairs(V, xi, yi, Parameters(0.8, c, 0), cells=True)
+        want = oracle.pairs(V, xi, yi, 0.8, c, 0)
+        assert_bit_equal(stats_matrix(res), want, f"c={c}")
+
+
+def test_large_c_times_b_tables_in_hbm(engine, oracle):
+    """c B so large that k_dp's clump bounds and cumulative table (y (k^+1)
+    ints) leave shared memory: n = 20000, alpha = 0.8 (B = 2759), c = 15.
+    Tie-heavy variables keep the oracle's DP small."""
+    n = 20000
+    rng = np.random.default_rng(77)
+    x = rng.integers(0, 40, n).astype(float)
+    V = np.stack([x, (x % 7) + rng.integers(0, 3, n), rng.integers(0, 25, n).astype(float),
+                  np.round(np.sin(x / 6.0), 1)])
+    xi, yi = [0, 0, 2], [1, 3, 1]
+    res = engine.pairs(V, xi, yi, Parameters(0.8, 15.0, 0))
+    want = oracle.pairs(V, xi, yi, 0.8, 15.0, 0)
+    assert_bit_equal(stats_matrix(res), want, "alpha=0.8")
+
+
+@pytest.mark.parametrize("force", ["MINE_B200_PF_GLOBAL", "MINE_B200_DP_GLOBAL",
+                                   "MINE_B200_RADIX_SORT"])
+def test_large_n_variants_forced(force):
+    """The large-n variants forced at small n (each switch is read once per
+    process) on a mixed 600-pair batch: partition point arrays in HBM,
+    clump bounds / cumulative table in HBM for k_part_f2 and k_dp, radix K1."""
     import os
     import subprocess
     import sys
@@ -449,7 +482,7 @@ def test_point_arrays_in_hbm_forced(tmp_path):
         "    want = O.Oracle().pairs(V, xi, yi, a, c, est)\n"
         "    assert (bits(got) == bits(want)).all(), (a, c)\n"
         "print('OK')\n")
-    env = dict(os.environ, MINE_B200_PF_GLOBAL="1")
+    env = dict(os.environ, **{force: "1"})
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                          text=True, timeout=600)
