@@ -777,6 +777,11 @@ __device__ __forceinline__ uint32_t cand_addr(uint32_t packed, uint32_t bt, uint
 // (packed int16 pair, odd stride: conflict-free) and the inner loop is one
 // scratch read, one IDP.2A (the whole byte address), one 2-byte rank gather
 // and half a 3-way integer max per candidate.
+// kRegSlots > 0 (n <= kRegSlots + 1): the staged words live in registers
+// instead of the scratch row -- every level loop is unrolled over the staged
+// count, so the per-candidate scratch read (a third of the shared-memory
+// wavefronts) disappears.
+template <int kRegSlots>
 __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, int k_hat,
                         double hq, double& i2, double& i3, unsigned long long* work, int* scr) {
   const int n = c.n;
@@ -807,6 +812,42 @@ __device__ void memo_y2(const MemoCtx& c, uint32_t m0, uint32_t rsm, int x_max, 
       r = max(r, kb[memo_G(n, cs) + a0 * (n - cs + 1) + (c0 - a0)]);
     }
     f2k = c.val[r];
+  } else if constexpr (kRegSlots > 0) {
+    const double* W2 = c.tab + c.L.w2;
+    const double dn = (double)n, rn = __drcp_rn(dn);
+    const int* sb = c.ints + c.L.sb;
+    const uint32_t k2_s = (uint32_t)__cvta_generic_to_shared(K2R) - 32768u;
+    uint32_t st[kRegSlots];
+    uint32_t ts = bnd;
+    {
+      const int t = __ffs(ts) - 1;
+      st[0] = sb[t] + __popc(m0 & ((1u << t) - 1u)) * (131072 - 2 * t);
+    }
+    ts &= ts - 1;
+    f2k = 0.0;
+    // iteration L has L staged split points; the k - 1 <= n - 1 <= kRegSlots
+    // boundaries end the loop (level n) by L = k - 1
+#pragma unroll
+    for (int L = 1; L <= kRegSlots; ++L) {
+      const bool last = ts == 0;
+      const int t = last ? n : __ffs(ts) - 1;
+      const int b0t = last ? c0 : __popc(m0 & ((1u << t) - 1u));
+      const uint32_t kb = k2_s + 2u * (offk[t] + b0t);
+      const uint32_t bt = ((uint32_t)t << 8) | 1u;
+      int r = -1;
+#pragma unroll
+      for (int j = 0; j < L; ++j) r = max(r, lds_u16(cand_addr(st[j], bt, kb)));
+      if (last) {
+        f2k = c.val[r];
+        break;
+      }
+      const double f2 = c.val[r];
+      const double r1 = int_quot((double)t, dn, rn);
+      const int w2row = t * (n + 1) - ((t * (t - 1)) >> 1);
+      best3 = dmax(best3, __dsub_rn(__dmul_rn(r1, f2), W2[w2row + c0 - b0t]));
+      if (L < kRegSlots) st[L] = sb[t] + b0t * (131072 - 2 * t);
+      ts &= ts - 1;
+    }
   } else {
     const double* W2 = c.tab + c.L.w2;
     // R1[t] = t / n and the W2 row of t are recomputed (FP64 / integer ALU)
@@ -930,6 +971,14 @@ constexpr int kMemoMaxThreads = 1024;
 
 __host__ __device__ inline int memo_scr_stride(int n) { return n | 1; }
 
+// register-staged y = 2 levels up to n = kMemoRegSlots + 1 (the compact
+// 3-row table starts above n = 26, so these always use the padded one)
+constexpr int kMemoRegSlots = 23;
+static bool memo_reg_slots(int n) {
+  static const bool off = std::getenv("MINE_B200_MEMO_SCRATCH") != nullptr;
+  return !off && n <= kMemoRegSlots + 1;
+}
+
 // Shared-memory plan: table image | val[] (distinct candidate values) |
 // per-thread scratch rows.
 __host__ __device__ inline int memo_val_off(const MemoLayout& L) { return (L.total + 1) & ~1; }
@@ -939,7 +988,7 @@ __host__ __device__ inline int memo_scr_off(const MemoLayout& L, int nval) {
 
 // kCount: the instrumented (untimed) variant with realised-work counters.
 // kT3C: the compact 3-row table (MemoLayout::t3c), a compile-time choice
-template <bool kCount, bool kT3C>
+template <bool kCount, bool kT3C, int kRegSlots>
 __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Tables tb,
                                                                const double* __restrict__ memo,
                                                                const double* __restrict__ memo_val,
@@ -1018,7 +1067,7 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
       const double hq3 = __hiloint2double(hy.w, hy.z);
       if (yh2 >= 2) {
         double i2, i3;
-        memo_y2(c, m2, rsm, x2, kh2, hq2, i2, i3, wk, scr);
+        memo_y2<kRegSlots>(c, m2, rsm, x2, kh2, hq2, i2, i3, wk, scr);
         o[orient][0] = norm_cell(i2, lg[2], lg[yh2]);
         if (x2 >= 3) o[orient][orient ? 2 : 1] = norm_cell(i3, lg[3], lg[yh2]);
       }
@@ -1027,7 +1076,7 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
         if (yh3 == 3)
           i2 = memo_y3_rows3<kT3C>(c, m3a, m3b, rsm, kh3, hq3, wk);
         else
-          memo_y2(c, m3a, rsm, 2, kh3, hq3, i2, dummy, wk, scr);
+          memo_y2<kRegSlots>(c, m3a, rsm, 2, kh3, hq3, i2, dummy, wk, scr);
         o[orient][orient ? 1 : 2] = norm_cell(i2, lg[2], lg[yh3]);
       }
     }
@@ -1101,10 +1150,12 @@ cudaError_t init_kernel_attributes(int device) {
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (e != cudaSuccess) return e;
   const void* fns[] = {reinterpret_cast<const void*>(k_sort_vars),
-                       reinterpret_cast<const void*>(k_memo_pairs<false, false>),
-                       reinterpret_cast<const void*>(k_memo_pairs<true, false>),
-                       reinterpret_cast<const void*>(k_memo_pairs<false, true>),
-                       reinterpret_cast<const void*>(k_memo_pairs<true, true>)};
+                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 0>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 0>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, true, 0>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, true, 0>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, false, kMemoRegSlots>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, false, kMemoRegSlots>)};
   for (const void* f : fns) {
     cudaFuncAttributes fa{};
     e = cudaFuncGetAttributes(&fa, f);
@@ -1230,8 +1281,9 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
   if (ps.count <= 0) return;
   const size_t fixed = memo_smem_fixed(vs.n, nval);
   const size_t budget = 226 * 1024 - fixed;
-  const size_t row = sizeof(int) * (size_t)memo_scr_stride(vs.n);
-  int threads = (int)std::min<size_t>(kMemoMaxThreads, budget / row) / 32 * 32;
+  const bool regs = memo_reg_slots(vs.n);
+  const size_t row = regs ? 0 : sizeof(int) * (size_t)memo_scr_stride(vs.n);
+  int threads = (int)(row ? std::min<size_t>(kMemoMaxThreads, budget / row) : kMemoMaxThreads) / 32 * 32;
   threads = std::max(threads, 32);
   const size_t sm = fixed + row * threads;
   int dev = 0, sms = 148;
@@ -1240,19 +1292,23 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
   const long long need = (ps.count + threads - 1) / threads;
   const unsigned blocks = (unsigned)std::min<long long>(sms, need);
   const MemoLayout L = memo_layout(vs.n);
-#define MEMO_LAUNCH(CNT, T3C)                                                                  \
-  k_memo_pairs<CNT, T3C><<<blocks, threads, sm, s>>>(vs, tb, memo, memo_val, nval, L, ps, c, est, \
+#define MEMO_LAUNCH(CNT, T3C, RS)                                                              \
+  k_memo_pairs<CNT, T3C, RS><<<blocks, threads, sm, s>>>(vs, tb, memo, memo_val, nval, L, ps, c, est, \
                                                      out, o_cells, CNT ? counters : nullptr)
   if (counters) {
-    if (L.t3c)
-      MEMO_LAUNCH(true, true);
+    if (regs)
+      MEMO_LAUNCH(true, false, kMemoRegSlots);
+    else if (L.t3c)
+      MEMO_LAUNCH(true, true, 0);
     else
-      MEMO_LAUNCH(true, false);
+      MEMO_LAUNCH(true, false, 0);
   } else {
-    if (L.t3c)
-      MEMO_LAUNCH(false, true);
+    if (regs)
+      MEMO_LAUNCH(false, false, kMemoRegSlots);
+    else if (L.t3c)
+      MEMO_LAUNCH(false, true, 0);
     else
-      MEMO_LAUNCH(false, false);
+      MEMO_LAUNCH(false, false, 0);
   }
 #undef MEMO_LAUNCH
 }
