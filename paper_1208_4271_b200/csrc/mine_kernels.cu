@@ -971,12 +971,11 @@ constexpr int kMemoMaxThreads = 1024;
 
 __host__ __device__ inline int memo_scr_stride(int n) { return n | 1; }
 
-// register-staged y = 2 levels up to n = kMemoRegSlots + 1 (the compact
-// 3-row table starts above n = 26, so these always use the padded one)
-constexpr int kMemoRegSlots = 23;
-static bool memo_reg_slots(int n) {
+// register-staged y = 2 levels: 23 slots up to n = 24, 30 up to n = 31
+// (0: the scratch-row variant, kept behind MINE_B200_MEMO_SCRATCH)
+static int memo_reg_slots(int n) {
   static const bool off = std::getenv("MINE_B200_MEMO_SCRATCH") != nullptr;
-  return !off && n <= kMemoRegSlots + 1;
+  return off ? 0 : (n <= 24 ? 23 : 30);
 }
 
 // Shared-memory plan: table image | val[] (distinct candidate values) |
@@ -1154,8 +1153,12 @@ cudaError_t init_kernel_attributes(int device) {
                        reinterpret_cast<const void*>(k_memo_pairs<true, false, 0>),
                        reinterpret_cast<const void*>(k_memo_pairs<false, true, 0>),
                        reinterpret_cast<const void*>(k_memo_pairs<true, true, 0>),
-                       reinterpret_cast<const void*>(k_memo_pairs<false, false, kMemoRegSlots>),
-                       reinterpret_cast<const void*>(k_memo_pairs<true, false, kMemoRegSlots>)};
+                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 23>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 23>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 30>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 30>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, true, 30>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, true, 30>)};
   for (const void* f : fns) {
     cudaFuncAttributes fa{};
     e = cudaFuncGetAttributes(&fa, f);
@@ -1281,7 +1284,7 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
   if (ps.count <= 0) return;
   const size_t fixed = memo_smem_fixed(vs.n, nval);
   const size_t budget = 226 * 1024 - fixed;
-  const bool regs = memo_reg_slots(vs.n);
+  const int regs = memo_reg_slots(vs.n);
   const size_t row = regs ? 0 : sizeof(int) * (size_t)memo_scr_stride(vs.n);
   int threads = (int)(row ? std::min<size_t>(kMemoMaxThreads, budget / row) : kMemoMaxThreads) / 32 * 32;
   threads = std::max(threads, 32);
@@ -1295,20 +1298,21 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
 #define MEMO_LAUNCH(CNT, T3C, RS)                                                              \
   k_memo_pairs<CNT, T3C, RS><<<blocks, threads, sm, s>>>(vs, tb, memo, memo_val, nval, L, ps, c, est, \
                                                      out, o_cells, CNT ? counters : nullptr)
+  // the compact 3-row table starts above n = 26: never with 23 slots
   if (counters) {
-    if (regs)
-      MEMO_LAUNCH(true, false, kMemoRegSlots);
-    else if (L.t3c)
-      MEMO_LAUNCH(true, true, 0);
+    if (regs == 23)
+      MEMO_LAUNCH(true, false, 23);
+    else if (regs)
+      L.t3c ? MEMO_LAUNCH(true, true, 30) : MEMO_LAUNCH(true, false, 30);
     else
-      MEMO_LAUNCH(true, false, 0);
+      L.t3c ? MEMO_LAUNCH(true, true, 0) : MEMO_LAUNCH(true, false, 0);
   } else {
-    if (regs)
-      MEMO_LAUNCH(false, false, kMemoRegSlots);
-    else if (L.t3c)
-      MEMO_LAUNCH(false, true, 0);
+    if (regs == 23)
+      MEMO_LAUNCH(false, false, 23);
+    else if (regs)
+      L.t3c ? MEMO_LAUNCH(false, true, 30) : MEMO_LAUNCH(false, false, 30);
     else
-      MEMO_LAUNCH(false, false, 0);
+      L.t3c ? MEMO_LAUNCH(false, true, 0) : MEMO_LAUNCH(false, false, 0);
   }
 #undef MEMO_LAUNCH
 }
