@@ -790,6 +790,16 @@ void launch_build_div(double* div, int n, cudaStream_t s) {
   k_build_div<<<blocks, 256, 0, s>>>(div, n);
 }
 
+// up to this many samples the F(t,2) level runs on 128 threads too (c2,
+// n = 500: +8%; 64 threads measured slower)
+static int pf_small_n() {
+  static const int v = [] {
+    const char* e = std::getenv("MINE_B200_PF128_N");
+    return e ? std::atoi(e) : 700;
+  }();
+  return v;
+}
+
 void launch_part_f2(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
                     long long npairs, const YParams& yp, const GenScratch& gs, double* ocells,
                     const SubDebug* dbg, int orient_only, unsigned long long* counters,
@@ -806,7 +816,7 @@ void launch_part_f2(const VarSet& vs, const Tables& tb, const PairSpace& ps, lon
   else if (gs.pts)
     k_part_f2<256, true, false><<<blocks, 256, sm, s>>>(vs, tb, ps, base, yp, gs, ocells, d, dg,
                                                         orient_only, counters);
-  else if (yp.x_max >= 3)
+  else if (yp.x_max >= 3 && vs.n > pf_small_n())
     k_part_f2<256, false, false><<<blocks, 256, sm, s>>>(vs, tb, ps, base, yp, gs, ocells, d, dg,
                                                          orient_only, counters);
   else
