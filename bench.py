@@ -374,6 +374,26 @@ def run_config(args):
     line = {"config": args.config, "call": w.call, "pairs": count, "n": w.n, "alpha": w.alpha,
             "c": w.c, "est": w.est, "e2e_pairs_per_s": count / dt, "e2e_s": dt,
             "launches": eng.last_launches}
+    # FP64 roofline of the whole call: the FP64 ops the
+    # reference's op sequence needs for these pairs (entropy sums with the
+    # p*log(p) terms as lookups, span terms, and DMUL + DADD + DSETP per DP
+    # candidate), counted by the kernels, at the measured DADD issue rate
+    eng.count_work = True
+    call()
+    eng.count_work = False
+    work = eng.last_work
+    dadd = probe_peaks(0)[0]
+    if dadd:
+        line["roofline"] = {"bound": "fp64", "achieved": work["fp64_ops"] / dt / 1e12,
+                            "peak": dadd / 1e12, "unit": "TFLOP/s",
+                            "frac": work["fp64_ops"] / dadd / dt,
+                            "work": {k: int(work[k]) for k in ("fp64_ops", "dp_candidates",
+                                                               "span_entries", "point_visits",
+                                                               "subproblems")},
+                            "work_unit": "FP64 ops of the reference's arithmetic (p log p terms "
+                                         "as lookups; DMUL+DADD+DSETP per DP candidate), counted "
+                                         "by the kernels; time = the whole call (e2e_s)",
+                            "peak_source": "measured live: probes.cu k_dadd"}
     if not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as O

@@ -33,6 +33,14 @@ namespace {
 #ifndef KDP_THREADS
 #define KDP_THREADS 256
 #endif
+// KDP_PREFETCH: F rows staged by cp.async under the span terms' gathers
+// (c4 +47%); KDP_SPAN2: span-term gathers of two rows in flight together
+#ifndef KDP_PREFETCH
+#define KDP_PREFETCH 1
+#endif
+#ifndef KDP_SPAN2
+#define KDP_SPAN2 1
+#endif
 #ifndef KDP_TILE
 #define KDP_TILE 32
 #endif
@@ -374,7 +382,24 @@ __device__ __forceinline__ void span_terms(const Tables& tb, const int* cb, cons
       plm[e] = tb.pl + tri(ct - cs[e]);
       acch[e] = 0.0;
     }
-    for (int r = 0; r < rows; ++r) {
+    int r = 0;
+#if KDP_SPAN2
+    // two rows per step: all eight gathers are issued before the adds (each
+    // sum still runs in row order)
+    for (; r + 2 <= rows; r += 2) {
+      const int ctr0 = cum[r * kk + t], ctr1 = cum[(r + 1) * kk + t];
+      double v[2][4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int s = s0 + base + w0 + e * nw;
+        v[0][e] = ok[e] ? __ldg(plm[e] + (ctr0 - cum[r * kk + s])) : 0.0;
+        v[1][e] = ok[e] ? __ldg(plm[e] + (ctr1 - cum[(r + 1) * kk + s])) : 0.0;
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acch[e] = __dadd_rn(__dadd_rn(acch[e], v[0][e]), v[1][e]);
+    }
+#endif
+    for (; r < rows; ++r) {
       const int ctr = cum[r * kk + t];
       double v[4];
 #pragma unroll
@@ -404,6 +429,14 @@ __device__ __forceinline__ void span_terms(const Tables& tb, const int* cb, cons
     }
   }
 }
+
+// 8-byte global -> shared copy that does not occupy registers until the wait
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -490,11 +523,22 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
         // ---- outer part: every s < t0 (independent candidates)
         for (int s0 = max(2, l0 - 1); s0 < t0; s0 += T) {
           const int ns = min(T, t0 - s0);
+#if KDP_PREFETCH
+          // stage F(s, l0-1 .. l1-1) by cp.async, in flight while the span
+          // terms' gathers run; no registers are held across span_terms
+          for (int i = tid; i < ns * nl; i += kDpThreads) {
+            const int sl = i / nl, j = i - sl * nl;
+            cp_async8(fs + sl * kFsW + j, F + (size_t)(s0 + sl) * RW + (((l0 - 3) + j) & cm));
+          }
+          span_terms(tb, cb, cum, kk, rows, k, s0, ns, t0, nt, A, W);
+          cp_async_wait_all();
+#else
           span_terms(tb, cb, cum, kk, rows, k, s0, ns, t0, nt, A, W);
           for (int i = tid; i < ns * nl; i += kDpThreads) {  // stage F(s, l0-1 .. l1-1)
             const int sl = i / nl, j = i - sl * nl;
             fs[sl * kFsW + j] = F[(size_t)(s0 + sl) * RW + (((l0 - 3) + j) & cm)];
           }
+#endif
           __syncthreads();
           if (owner) {
             // s >= l - 1 holds for all 4 levels once s >= my_l + 2; only the

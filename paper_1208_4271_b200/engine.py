@@ -264,6 +264,8 @@ class Engine:
         if not self.ctx:
             raise RuntimeError("mine_b200_create failed: " + self.L.mine_b200_last_error().decode())
         self.device = device
+        self.count_work = False  # batch calls fill last_work (instrumented pass)
+        self._cnt = None
 
     def close(self):
         if getattr(self, "ctx", None):
@@ -300,12 +302,20 @@ class Engine:
             so.cells = res["cells"].ctypes.data_as(_dp)
         return res, so
 
-    @staticmethod
-    def _opts(first=0, count=0, tier=0, reuse_vars=False) -> MineOpts:
+    def _opts(self, first=0, count=0, tier=0, reuse_vars=False) -> MineOpts:
         o = MineOpts()
         o.first, o.count, o.tier = int(first), int(count), int(tier)
         o.reuse_vars = int(bool(reuse_vars))
+        if self.count_work:
+            self._cnt = (ctypes.c_ulonglong * NCOUNTERS)()
+            o.counters = self._cnt
         return o
+
+    @property
+    def last_work(self) -> dict | None:
+        """Realised-work totals of the last batch call made with
+        `count_work = True` (an instrumented, synchronising pass)."""
+        return dict(zip(COUNTERS, list(self._cnt))) if self._cnt is not None else None
 
     # -- batch calls ----------------------------------------------------------
     def pairwise(self, vars_, params: Parameters = Parameters(), first: int = 0, count: int | None = None,
@@ -419,7 +429,8 @@ class Engine:
         so = MineStatsOut()
         for k in ALL_STATS:
             setattr(so, k, ctypes.cast(ctypes.c_void_p(out_ptrs[k]), _dp) if out_ptrs.get(k) else None)
-        o = self._opts(first, count, tier)
+        o = MineOpts()
+        o.first, o.count, o.tier = int(first), int(count), int(tier)
         o.device_io, o.async_, o.stream = 1, int(async_), ctypes.c_void_p(stream)
         cnt = (ctypes.c_ulonglong * NCOUNTERS)()
         if counters:
