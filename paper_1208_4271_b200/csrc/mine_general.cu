@@ -46,7 +46,7 @@ namespace {
 #endif
 constexpr int kDpThreads = KDP_THREADS;
 constexpr int kMaxTile = KDP_TILE;  // t-tile / s-chunk edge
-constexpr int kCells = 8;      // accumulators per thread
+constexpr int kAccStride = 9;  // doubles per thread in the accumulator hand-over (odd: no bank conflicts)
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -290,15 +290,30 @@ __global__ void __launch_bounds__(kPfThreads, 2048 / kPfThreads) k_part_f2(VarSe
       const int ct = cb[t];
       const double* plt = tb.pl + tri(ct);
       double best = kLowest;
-      for (int s = 1 + lane; s < t; s += 32) {
-        const int cs = cb[s];
-        double acc2 = __ldg(plt + cs);
-        acc2 = __dadd_rn(acc2, __ldg(plt + (ct - cs)));
-        double accj = 0.0;
-        for (int r = 0; r < rows; ++r) accj = __dadd_rn(accj, __ldg(plt + cum[r * kk + s]));
-        for (int r = 0; r < rows; ++r)
-          accj = __dadd_rn(accj, __ldg(plt + (cum[r * kk + t] - cum[r * kk + s])));
-        best = dmax(best, __dsub_rn(-acc2, -accj));
+      if (rows == 2) {
+        // two rows (y = 2, the heaviest level): all six gathers of a
+        // candidate are issued before its adds
+        const int ct0 = cum[t], ct1 = cum[kk + t];
+        for (int s = 1 + lane; s < t; s += 32) {
+          const int cs = cb[s], a0 = cum[s], a1 = cum[kk + s];
+          const double p0 = __ldg(plt + cs), p1 = __ldg(plt + (ct - cs));
+          const double j0 = __ldg(plt + a0), j1 = __ldg(plt + a1);
+          const double j2 = __ldg(plt + (ct0 - a0)), j3 = __ldg(plt + (ct1 - a1));
+          const double acc2 = __dadd_rn(p0, p1);
+          const double accj = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(0.0, j0), j1), j2), j3);
+          best = dmax(best, __dsub_rn(-acc2, -accj));
+        }
+      } else {
+        for (int s = 1 + lane; s < t; s += 32) {
+          const int cs = cb[s];
+          double acc2 = __ldg(plt + cs);
+          acc2 = __dadd_rn(acc2, __ldg(plt + (ct - cs)));
+          double accj = 0.0;
+          for (int r = 0; r < rows; ++r) accj = __dadd_rn(accj, __ldg(plt + cum[r * kk + s]));
+          for (int r = 0; r < rows; ++r)
+            accj = __dadd_rn(accj, __ldg(plt + (cum[r * kk + t] - cum[r * kk + s])));
+          best = dmax(best, __dsub_rn(-acc2, -accj));
+        }
       }
       best = warp_max(best);
       if (lane == 0) {
@@ -326,6 +341,13 @@ struct DpLayout {
 };
 
 constexpr int kFsW = 64;       // staged F row width (levels l0-1 .. l1-1)
+// Staged row layout: level offset j = 4 g + i (g: the consumer's level group)
+// sits at 2 g + i for i < 2 and at 32 + 2 g + (i - 2) otherwise, so the
+// 16-byte loads of consecutive groups are contiguous (no bank conflicts).
+__host__ __device__ inline int fs_col(int j) {
+  const int g = j >> 2, i = j & 3;
+  return (i < 2 ? 0 : 30) + 2 * g + i;
+}
 constexpr int kFtW = 65;       // tile F row width (levels l0-1 .. l1)
 
 // kGlobalTables: cb and cum are read in place from the subproblem's
@@ -342,7 +364,7 @@ __host__ __device__ inline DpLayout dp_layout(int y, int kc, bool global_tables 
   L.W = o;
   o += al16(sizeof(double) * kMaxTile * kMaxTile);
   L.acc = o;
-  o += al16(sizeof(double) * kDpThreads * kCells);
+  o += al16(sizeof(double) * kDpThreads * kAccStride);
   L.fs = o;
   o += al16(sizeof(double) * kMaxTile * kFsW);
   L.ft = o;
@@ -528,7 +550,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
           // terms' gathers run; no registers are held across span_terms
           for (int i = tid; i < ns * nl; i += kDpThreads) {
             const int sl = i / nl, j = i - sl * nl;
-            cp_async8(fs + sl * kFsW + j, F + (size_t)(s0 + sl) * RW + (((l0 - 3) + j) & cm));
+            cp_async8(fs + sl * kFsW + fs_col(j), F + (size_t)(s0 + sl) * RW + (((l0 - 3) + j) & cm));
           }
           span_terms(tb, cb, cum, kk, rows, k, s0, ns, t0, nt, A, W);
           cp_async_wait_all();
@@ -536,7 +558,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
           span_terms(tb, cb, cum, kk, rows, k, s0, ns, t0, nt, A, W);
           for (int i = tid; i < ns * nl; i += kDpThreads) {  // stage F(s, l0-1 .. l1-1)
             const int sl = i / nl, j = i - sl * nl;
-            fs[sl * kFsW + j] = F[(size_t)(s0 + sl) * RW + (((l0 - 3) + j) & cm)];
+            fs[sl * kFsW + fs_col(j)] = F[(size_t)(s0 + sl) * RW + (((l0 - 3) + j) & cm)];
           }
 #endif
           __syncthreads();
@@ -544,7 +566,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
             // s >= l - 1 holds for all 4 levels once s >= my_l + 2; only the
             // chunk(s) near the diagonal need the per-level test.  Cells that
             // are not valid accumulate garbage that is never read.
-            const double* fr = fs + 4 * my_g;
+            const double* fr = fs + 2 * my_g;
             int sl = 0;
             for (; sl < ns && s0 + sl < my_l + 2; ++sl) {
               const int s = s0 + sl;
@@ -553,7 +575,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
 #pragma unroll
               for (int i = 0; i < 4; ++i)
                 if (s >= my_l + i - 1) {
-                  const double f = fr[sl * kFsW + i];
+                  const double f = fr[sl * kFsW + (i < 2 ? i : 30 + i)];
                   acc[i] = dmax(acc[i], __dsub_rn(__dmul_rn(a.x, f), w.x));
                   acc[4 + i] = dmax(acc[4 + i], __dsub_rn(__dmul_rn(a.y, f), w.y));
                 }
@@ -563,7 +585,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
               const double2 a = *reinterpret_cast<const double2*>(A + sl * kMaxTile + my_tl);
               const double2 w = *reinterpret_cast<const double2*>(W + sl * kMaxTile + my_tl);
               const double2 f01 = *reinterpret_cast<const double2*>(fr + sl * kFsW);
-              const double2 f23 = *reinterpret_cast<const double2*>(fr + sl * kFsW + 2);
+              const double2 f23 = *reinterpret_cast<const double2*>(fr + sl * kFsW + 32);
               acc[0] = dmax(acc[0], __dsub_rn(__dmul_rn(a.x, f01.x), w.x));
               acc[1] = dmax(acc[1], __dsub_rn(__dmul_rn(a.x, f01.y), w.x));
               acc[2] = dmax(acc[2], __dsub_rn(__dmul_rn(a.x, f23.x), w.x));
@@ -577,7 +599,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
           __syncthreads();
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) accS[tid * 8 + i] = acc[i];
+        for (int i = 0; i < 8; ++i) accS[tid * kAccStride + i] = acc[i];
         // ---- inner part: s inside the tile, one t at a time, a level per
         // thread; only the warps holding levels take part (named barrier).
         span_terms(tb, cb, cum, kk, rows, k, t0, nt, t0, nt, A, W);
@@ -590,7 +612,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
             const int tt = t0 + tl;
             if (ll < nl && tt >= l && !(l == l_max && tt != k)) {
               // owner of cell (tl, ll): thread (tl/2)*ng + ll/4, slot (tl&1)*4 + (ll&3)
-              double m = accS[((tl >> 1) * ng + (ll >> 2)) * 8 + (tl & 1) * 4 + (ll & 3)];
+              double m = accS[((tl >> 1) * ng + (ll >> 2)) * kAccStride + (tl & 1) * 4 + (ll & 3)];
               const double* Ap = A + tl;
               const double* Wp = W + tl;
               for (int s = max(t0, l - 1); s < tt; ++s) {
@@ -693,8 +715,13 @@ __global__ void __launch_bounds__(kWarpThreads) k_dp_warp(VarSet vs, Tables tb, 
         const int cs = cb[s];
         const double* plm = tb.pl + tri(ct - cs);
         double acch = 0.0;
-        for (int r = 0; r < rows; ++r)
-          acch = __dadd_rn(acch, __ldg(plm + (cum[r * kk + t] - cum[r * kk + s])));
+        int r = 0;
+        for (; r + 2 <= rows; r += 2) {  // two gathers in flight, added in row order
+          const double v0 = __ldg(plm + (cum[r * kk + t] - cum[r * kk + s]));
+          const double v1 = __ldg(plm + (cum[(r + 1) * kk + t] - cum[(r + 1) * kk + s]));
+          acch = __dadd_rn(__dadd_rn(acch, v0), v1);
+        }
+        if (r < rows) acch = __dadd_rn(acch, __ldg(plm + (cum[r * kk + t] - cum[r * kk + s])));
         double a, q;
         if (tb.div) {
           const double* dr = tb.div + tri(ct);

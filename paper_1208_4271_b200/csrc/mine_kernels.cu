@@ -978,6 +978,15 @@ static int memo_reg_slots(int n) {
   return off ? 0 : (n <= 24 ? 23 : 30);
 }
 
+// sorted-batch pair order (MINE_B200_MEMO_SORT=0 turns it off)
+static bool memo_sort() {
+  static const bool on = [] {
+    const char* e = std::getenv("MINE_B200_MEMO_SORT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // Shared-memory plan: table image | val[] (distinct candidate values) |
 // per-thread scratch rows.
 __host__ __device__ inline int memo_val_off(const MemoLayout& L) { return (L.total + 1) & ~1; }
@@ -985,9 +994,122 @@ __host__ __device__ inline int memo_scr_off(const MemoLayout& L, int nval) {
   return memo_val_off(L) + ((nval + 1) & ~1);
 }
 
-// kCount: the instrumented (untimed) variant with realised-work counters.
-// kT3C: the compact 3-row table (MemoLayout::t3c), a compile-time choice
+// Row-label mask of Y's y = 2 rows in X's sorted order (bit t: label of the
+// sample at x rank t) -- the same funnel-shift extraction as memo_pair.
+__device__ __forceinline__ uint32_t memo_mask2(const VarSet& vs, int X, int Y, int n) {
+  const uint4* px = vs.rec + (size_t)X * 6;
+  const uint4 u = __ldg(px), v = __ldg(px + 1);
+  const uint32_t ax[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
+  const uint32_t fy = __ldg(reinterpret_cast<const unsigned int*>(vs.rec + (size_t)Y * 6 + 2));
+  uint32_t m2 = 0;
+#pragma unroll
+  for (int t = 0; t < 32; ++t) {
+    if (t < n) {
+      const uint32_t a = __byte_perm(ax[t >> 2], 0, 0x4440 | (t & 3));
+      m2 |= (uint32_t)(((uint64_t)fy << 32) >> a) & (1u << t);
+    }
+  }
+  return m2;
+}
+
+// One pair (both orientations): the cells of B <= 7 and the statistics.
+// swap: run orientation 1 first (the sorted-batch path puts the orientation
+// with more clumps first in every lane); the cells land in the same places.
 template <bool kCount, bool kT3C, int kRegSlots>
+__device__ __forceinline__ void memo_pair(const MemoCtx& c, const VarSet& vs, const Tables& tb,
+                                          const PairSpace& ps, long long wl, bool swap,
+                                          int kh2, int kh3, int est, const StatsOut& out, double* ocells,
+                                          const double* lg, const double* lg2,
+                                          unsigned long long* wk, int* scr) {
+  const int n = c.n, B = tb.B;
+  const int x2 = B / 2;  // 2 or 3
+  const bool has_y3 = B >= 6;
+  int va, vb;
+  pair_vars(ps, ps.first + wl, va, vb);
+  if (swap) {
+    const int t = va;
+    va = vb;
+    vb = t;
+  }
+  double o[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+#pragma unroll
+  for (int orient = 0; orient < 2; ++orient) {
+    // column variable X: shift bytes + run starts; row variable Y: label
+    // masks, H(Q), yhat.  Loaded per orientation to keep registers low.
+    const uint4* px = vs.rec + (size_t)(orient ? vb : va) * 6;
+    const uint4* py = vs.rec + (size_t)(orient ? va : vb) * 6;
+    uint32_t ax[8];
+    {
+      const uint4 u = __ldg(px), v = __ldg(px + 1);
+      ax[0] = u.x, ax[1] = u.y, ax[2] = u.z, ax[3] = u.w;
+      ax[4] = v.x, ax[5] = v.y, ax[6] = v.z, ax[7] = v.w;
+    }
+    const uint4 fy = __ldg(py + 2);
+    // the row-label masks in x-sorted order: bit t = label of sample
+    // perm_X[t]; one 64-bit funnel shift + one LOP3 per mask and position
+    uint32_t m2 = 0, m3a = 0, m3b = 0;
+#pragma unroll
+    for (int t = 0; t < 32; ++t) {
+      if (t < n) {
+        const uint32_t a = __byte_perm(ax[t >> 2], 0, 0x4440 | (t & 3));
+        m2 |= (uint32_t)(((uint64_t)fy.x << 32) >> a) & (1u << t);
+        m3a |= (uint32_t)(((uint64_t)fy.y << 32) >> a) & (1u << t);
+        m3b |= (uint32_t)(((uint64_t)fy.z << 32) >> a) & (1u << t);
+      }
+    }
+    const uint4 sx = __ldg(px + 5), hy = __ldg(py + 4), sy = __ldg(py + 5);
+    const uint32_t rsm = sx.x;
+    const int yh2 = sy.y & 0xff, yh3 = (sy.y >> 8) & 0xff;
+    const double hq2 = __hiloint2double(hy.y, hy.x);
+    const double hq3 = __hiloint2double(hy.w, hy.z);
+    if (yh2 >= 2) {
+      double i2, i3;
+      memo_y2<kRegSlots>(c, m2, rsm, x2, kh2, hq2, i2, i3, wk, scr);
+      o[orient][0] = norm_cell(i2, lg[2], lg[yh2]);
+      if (x2 >= 3) o[orient][orient ? 2 : 1] = norm_cell(i3, lg[3], lg[yh2]);
+    }
+    if (has_y3 && yh3 >= 2) {
+      double i2, dummy;
+      if (yh3 == 3)
+        i2 = memo_y3_rows3<kT3C>(c, m3a, m3b, rsm, kh3, hq3, wk);
+      else
+        memo_y2<kRegSlots>(c, m3a, rsm, 2, kh3, hq3, i2, dummy, wk, scr);
+      o[orient][orient ? 1 : 2] = norm_cell(i2, lg[2], lg[yh3]);
+    }
+  }
+  if (swap) {
+    // the pass ran with X = vb first: its orientation 0 is the pair's
+    // orientation 1, whose (3,2) / (2,3) cells sit transposed
+    double t[2][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      t[0][i] = o[1][i == 0 ? 0 : 3 - i];
+      t[1][i] = o[0][i == 0 ? 0 : 3 - i];
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      o[0][i] = t[0][i];
+      o[1][i] = t[1][i];
+    }
+  }
+  small_stats(o, has_y3 ? 3 : 1, est, lg2, out, wl, ocells);
+}
+
+#ifndef MEMO_BATCH
+#define MEMO_BATCH 8
+#endif
+constexpr int kMemoBatch = MEMO_BATCH * kMemoMaxThreads;  // pairs per sorted batch
+// sort buffers after the tables: 1024 bucket counts, 4096 sorted slots, 4096 keys
+constexpr size_t kMemoSortBytes = sizeof(int) * (1024 + kMemoBatch) + sizeof(uint16_t) * kMemoBatch;
+
+// kCount: the instrumented (untimed) variant with realised-work counters.
+// kT3C: the compact 3-row table (MemoLayout::t3c), a compile-time choice.
+// kSort: pairs are taken in batches of 4096 and processed in the order of
+// their clump counts (max, min over the two y = 2 orientations, by a counting
+// sort in shared memory), the larger orientation first, so the 32 lanes of a
+// warp run loops of nearly the same trip counts (less divergence).  Results
+// are written at the pairs' own indices; the order changes nothing else.
+template <bool kCount, bool kT3C, int kRegSlots, bool kSort>
 __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Tables tb,
                                                                const double* __restrict__ memo,
                                                                const double* __restrict__ memo_val,
@@ -1022,64 +1144,65 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
   c.L = L;
   c.n = n;
   c.valid = prefix(n);
-  const int x2 = B / 2;  // 2 or 3
-  const bool has_y3 = B >= 6;
-  const int kh2 = max(1, (int)floor(cpar * (double)x2));
-  const int kh3 = max(1, (int)floor(cpar * 2.0));
   unsigned long long work[kNumCounters] = {};
   unsigned long long* wk = kCount ? work : nullptr;
+  const int kh2 = max(1, (int)floor(cpar * (double)(B / 2)));
+  const int kh3 = max(1, (int)floor(cpar * 2.0));
 
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long wl = blockIdx.x * (long long)blockDim.x + threadIdx.x; wl < ps.count; wl += stride) {
-    int va, vb;
-    pair_vars(ps, ps.first + wl, va, vb);
-    double o[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
-#pragma unroll
-    for (int orient = 0; orient < 2; ++orient) {
-      // column variable X: shift bytes + run starts; row variable Y: label
-      // masks, H(Q), yhat.  Loaded per orientation to keep registers low.
-      const uint4* px = vs.rec + (size_t)(orient ? vb : va) * 6;
-      const uint4* py = vs.rec + (size_t)(orient ? va : vb) * 6;
-      uint32_t ax[8];
-      {
-        const uint4 u = __ldg(px), v = __ldg(px + 1);
-        ax[0] = u.x, ax[1] = u.y, ax[2] = u.z, ax[3] = u.w;
-        ax[4] = v.x, ax[5] = v.y, ax[6] = v.z, ax[7] = v.w;
+  if constexpr (kSort) {
+    // the sort buffers follow the tables (no scratch rows with kRegSlots)
+    int* hist = reinterpret_cast<int*>(msm + memo_scr_off(L, nval));
+    int* sidx = hist + 1024;
+    uint16_t* skey = reinterpret_cast<uint16_t*>(sidx + kMemoBatch);
+    __shared__ int wsum[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long nbatch = (ps.count + kMemoBatch - 1) / kMemoBatch;
+    for (long long b = blockIdx.x; b < nbatch; b += gridDim.x) {
+      const long long b0 = b * kMemoBatch;
+      const int nb = (int)min((long long)kMemoBatch, ps.count - b0);
+      hist[tid] = 0;
+      __syncthreads();
+#pragma unroll 1
+      for (int e = tid; e < nb; e += kMemoMaxThreads) {
+        int va, vb;
+        pair_vars(ps, ps.first + b0 + e, va, vb);
+        const uint32_t m0 = memo_mask2(vs, va, vb, n), m1 = memo_mask2(vs, vb, va, n);
+        const uint32_t inner = c.valid & ~1u;
+        const int k0 = __popc((m0 ^ (m0 << 1)) & inner), k1 = __popc((m1 ^ (m1 << 1)) & inner);
+        const int key = (max(k0, k1) << 5) | min(k0, k1);  // < 1024 (n <= 32)
+        skey[e] = (uint16_t)(key | (k1 > k0 ? 0x8000 : 0));
+        atomicAdd(&hist[key], 1);
       }
-      const uint4 fy = __ldg(py + 2);
-      // the row-label masks in x-sorted order: bit t = label of sample
-      // perm_X[t]; one 64-bit funnel shift + one LOP3 per mask and position
-      uint32_t m2 = 0, m3a = 0, m3b = 0;
-#pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        if (t < n) {
-          const uint32_t a = __byte_perm(ax[t >> 2], 0, 0x4440 | (t & 3));
-          m2 |= (uint32_t)(((uint64_t)fy.x << 32) >> a) & (1u << t);
-          m3a |= (uint32_t)(((uint64_t)fy.y << 32) >> a) & (1u << t);
-          m3b |= (uint32_t)(((uint64_t)fy.z << 32) >> a) & (1u << t);
-        }
+      __syncthreads();
+      {  // exclusive scan of the bucket counts (one per thread)
+        const int v = hist[tid];
+        const int incl = warp_incl_scan(v);
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        if (warp == 0) wsum[lane] = warp_incl_scan(wsum[lane]);
+        __syncthreads();
+        hist[tid] = incl - v + (warp ? wsum[warp - 1] : 0);
       }
-      const uint4 sx = __ldg(px + 5), hy = __ldg(py + 4), sy = __ldg(py + 5);
-      const uint32_t rsm = sx.x;
-      const int yh2 = sy.y & 0xff, yh3 = (sy.y >> 8) & 0xff;
-      const double hq2 = __hiloint2double(hy.y, hy.x);
-      const double hq3 = __hiloint2double(hy.w, hy.z);
-      if (yh2 >= 2) {
-        double i2, i3;
-        memo_y2<kRegSlots>(c, m2, rsm, x2, kh2, hq2, i2, i3, wk, scr);
-        o[orient][0] = norm_cell(i2, lg[2], lg[yh2]);
-        if (x2 >= 3) o[orient][orient ? 2 : 1] = norm_cell(i3, lg[3], lg[yh2]);
+      __syncthreads();
+      for (int e = tid; e < nb; e += kMemoMaxThreads) {
+        const int kv = skey[e];
+        const int pos = atomicAdd(&hist[kv & 0x3ff], 1);
+        sidx[pos] = e | ((kv >> 15) << 16);
       }
-      if (has_y3 && yh3 >= 2) {
-        double i2, dummy;
-        if (yh3 == 3)
-          i2 = memo_y3_rows3<kT3C>(c, m3a, m3b, rsm, kh3, hq3, wk);
-        else
-          memo_y2<kRegSlots>(c, m3a, rsm, 2, kh3, hq3, i2, dummy, wk, scr);
-        o[orient][orient ? 1 : 2] = norm_cell(i2, lg[2], lg[yh3]);
+      __syncthreads();
+#pragma unroll 1
+      for (int pos = tid; pos < nb; pos += kMemoMaxThreads) {
+        const int v = sidx[pos];
+        memo_pair<kCount, kT3C, kRegSlots>(c, vs, tb, ps, b0 + (v & 0xffff), (v >> 16) != 0, kh2, kh3,
+                                           est, out, ocells, lg, lg2, wk, scr);
       }
+      __syncthreads();
     }
-    small_stats(o, has_y3 ? 3 : 1, est, lg2, out, wl, ocells);
+  } else {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long wl = blockIdx.x * (long long)blockDim.x + threadIdx.x; wl < ps.count; wl += stride)
+      memo_pair<kCount, kT3C, kRegSlots>(c, vs, tb, ps, wl, false, kh2, kh3, est, out, ocells, lg,
+                                         lg2, wk, scr);
   }
   if (kCount) flush_work(work, counters);
 }
@@ -1149,16 +1272,22 @@ cudaError_t init_kernel_attributes(int device) {
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (e != cudaSuccess) return e;
   const void* fns[] = {reinterpret_cast<const void*>(k_sort_vars),
-                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 0>),
-                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 0>),
-                       reinterpret_cast<const void*>(k_memo_pairs<false, true, 0>),
-                       reinterpret_cast<const void*>(k_memo_pairs<true, true, 0>),
-                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 23>),
-                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 23>),
-                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 30>),
-                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 30>),
-                       reinterpret_cast<const void*>(k_memo_pairs<false, true, 30>),
-                       reinterpret_cast<const void*>(k_memo_pairs<true, true, 30>)};
+                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 0, false>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 23, false>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 23, true>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 30, false>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 30, true>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, true, 0, false>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, true, 30, false>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, true, 30, true>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 0, false>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 23, false>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 23, true>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 30, false>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 30, true>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, true, 0, false>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, true, 30, false>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, true, 30, true>)};
   for (const void* f : fns) {
     cudaFuncAttributes fa{};
     e = cudaFuncGetAttributes(&fa, f);
@@ -1295,24 +1424,31 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
   const long long need = (ps.count + threads - 1) / threads;
   const unsigned blocks = (unsigned)std::min<long long>(sms, need);
   const MemoLayout L = memo_layout(vs.n);
-#define MEMO_LAUNCH(CNT, T3C, RS)                                                              \
-  k_memo_pairs<CNT, T3C, RS><<<blocks, threads, sm, s>>>(vs, tb, memo, memo_val, nval, L, ps, c, est, \
-                                                     out, o_cells, CNT ? counters : nullptr)
-  // the compact 3-row table starts above n = 26: never with 23 slots
+#define MEMO_LAUNCH(CNT, T3C, RS, SORT)                                                        \
+  k_memo_pairs<CNT, T3C, RS, SORT><<<blocks, threads, sm + (SORT ? kMemoSortBytes : 0), s>>>(   \
+      vs, tb, memo, memo_val, nval, L, ps, c, est, out, o_cells, CNT ? counters : nullptr)
+  // the compact 3-row table starts above n = 26: never with 23 slots.  The
+  // sorted-batch order needs the register-staged variant (no scratch rows).
+  const bool srt = regs && memo_sort() && threads == kMemoMaxThreads &&
+                   sm + kMemoSortBytes <= 226 * 1024;
   if (counters) {
     if (regs == 23)
-      MEMO_LAUNCH(true, false, 23);
+      srt ? MEMO_LAUNCH(true, false, 23, true) : MEMO_LAUNCH(true, false, 23, false);
+    else if (regs && srt)
+      L.t3c ? MEMO_LAUNCH(true, true, 30, true) : MEMO_LAUNCH(true, false, 30, true);
     else if (regs)
-      L.t3c ? MEMO_LAUNCH(true, true, 30) : MEMO_LAUNCH(true, false, 30);
+      L.t3c ? MEMO_LAUNCH(true, true, 30, false) : MEMO_LAUNCH(true, false, 30, false);
     else
-      L.t3c ? MEMO_LAUNCH(true, true, 0) : MEMO_LAUNCH(true, false, 0);
+      L.t3c ? MEMO_LAUNCH(true, true, 0, false) : MEMO_LAUNCH(true, false, 0, false);
   } else {
     if (regs == 23)
-      MEMO_LAUNCH(false, false, 23);
+      srt ? MEMO_LAUNCH(false, false, 23, true) : MEMO_LAUNCH(false, false, 23, false);
+    else if (regs && srt)
+      L.t3c ? MEMO_LAUNCH(false, true, 30, true) : MEMO_LAUNCH(false, false, 30, true);
     else if (regs)
-      L.t3c ? MEMO_LAUNCH(false, true, 30) : MEMO_LAUNCH(false, false, 30);
+      L.t3c ? MEMO_LAUNCH(false, true, 30, false) : MEMO_LAUNCH(false, false, 30, false);
     else
-      L.t3c ? MEMO_LAUNCH(false, true, 0) : MEMO_LAUNCH(false, false, 0);
+      L.t3c ? MEMO_LAUNCH(false, true, 0, false) : MEMO_LAUNCH(false, false, 0, false);
   }
 #undef MEMO_LAUNCH
 }
