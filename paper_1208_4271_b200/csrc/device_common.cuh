@@ -92,6 +92,19 @@ __device__ __forceinline__ void pair_vars(const PairSpace& ps, long long w, int&
   }
 }
 
+// The work item after (vx, vy) in pair_vars order (pairwise / cross only).
+__device__ __forceinline__ void pair_next(const PairSpace& ps, int& vx, int& vy) {
+  if (ps.kind == kPairwise) {
+    if (++vy == ps.p) {
+      ++vx;
+      vy = vx + 1;
+    }
+  } else if (++vy == ps.px + ps.py) {
+    ++vx;
+    vy = ps.px;
+  }
+}
+
 // Realised algorithmic work of one exact subproblem (rows R, k clumps): the
 // FP64 operations the reference arithmetic itself requires (mutual_info.cpp:
 // 47-66 with every 0.0 + x start elided), its p*log(p) lookups, DP candidates

@@ -1017,15 +1017,13 @@ __device__ __forceinline__ uint32_t memo_mask2(const VarSet& vs, int X, int Y, i
 // with more clumps first in every lane); the cells land in the same places.
 template <bool kCount, bool kT3C, int kRegSlots>
 __device__ __forceinline__ void memo_pair(const MemoCtx& c, const VarSet& vs, const Tables& tb,
-                                          const PairSpace& ps, long long wl, bool swap,
+                                          int va, int vb, long long wl, bool swap,
                                           int kh2, int kh3, int est, const StatsOut& out, double* ocells,
                                           const double* lg, const double* lg2,
                                           unsigned long long* wk, int* scr) {
   const int n = c.n, B = tb.B;
   const int x2 = B / 2;  // 2 or 3
   const bool has_y3 = B >= 6;
-  int va, vb;
-  pair_vars(ps, ps.first + wl, va, vb);
   if (swap) {
     const int t = va;
     va = vb;
@@ -1099,8 +1097,10 @@ __device__ __forceinline__ void memo_pair(const MemoCtx& c, const VarSet& vs, co
 #define MEMO_BATCH 8
 #endif
 constexpr int kMemoBatch = MEMO_BATCH * kMemoMaxThreads;  // pairs per sorted batch
-// sort buffers after the tables: 1024 bucket counts, 4096 sorted slots, 4096 keys
-constexpr size_t kMemoSortBytes = sizeof(int) * (1024 + kMemoBatch) + sizeof(uint16_t) * kMemoBatch;
+// sort buffers after the tables: 1024 bucket counts, the sorted slots, the
+// keys and the pairs' two variables (16 bits each)
+constexpr size_t kMemoSortBytes =
+    sizeof(int) * (1024 + kMemoBatch) + sizeof(uint16_t) * kMemoBatch + sizeof(uint32_t) * kMemoBatch;
 
 // kCount: the instrumented (untimed) variant with realised-work counters.
 // kT3C: the compact 3-row table (MemoLayout::t3c), a compile-time choice.
@@ -1153,7 +1153,8 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
     // the sort buffers follow the tables (no scratch rows with kRegSlots)
     int* hist = reinterpret_cast<int*>(msm + memo_scr_off(L, nval));
     int* sidx = hist + 1024;
-    uint16_t* skey = reinterpret_cast<uint16_t*>(sidx + kMemoBatch);
+    uint32_t* svar = reinterpret_cast<uint32_t*>(sidx + kMemoBatch);
+    uint16_t* skey = reinterpret_cast<uint16_t*>(svar + kMemoBatch);
     __shared__ int wsum[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long nbatch = (ps.count + kMemoBatch - 1) / kMemoBatch;
@@ -1162,15 +1163,22 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
       const int nb = (int)min((long long)kMemoBatch, ps.count - b0);
       hist[tid] = 0;
       __syncthreads();
+      // MEMO_BATCH consecutive pairs per thread: one index decode, then steps
+      int va = 0, vb = 0;
 #pragma unroll 1
-      for (int e = tid; e < nb; e += kMemoMaxThreads) {
-        int va, vb;
-        pair_vars(ps, ps.first + b0 + e, va, vb);
+      for (int i = 0; i < MEMO_BATCH; ++i) {
+        const int e = tid * MEMO_BATCH + i;
+        if (e >= nb) break;
+        if (i == 0 || ps.kind == kList)
+          pair_vars(ps, ps.first + b0 + e, va, vb);
+        else
+          pair_next(ps, va, vb);
         const uint32_t m0 = memo_mask2(vs, va, vb, n), m1 = memo_mask2(vs, vb, va, n);
         const uint32_t inner = c.valid & ~1u;
         const int k0 = __popc((m0 ^ (m0 << 1)) & inner), k1 = __popc((m1 ^ (m1 << 1)) & inner);
         const int key = (max(k0, k1) << 5) | min(k0, k1);  // < 1024 (n <= 32)
         skey[e] = (uint16_t)(key | (k1 > k0 ? 0x8000 : 0));
+        svar[e] = (uint32_t)va | ((uint32_t)vb << 16);  // the sorted path needs V < 65536
         atomicAdd(&hist[key], 1);
       }
       __syncthreads();
@@ -1192,17 +1200,21 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
       __syncthreads();
 #pragma unroll 1
       for (int pos = tid; pos < nb; pos += kMemoMaxThreads) {
-        const int v = sidx[pos];
-        memo_pair<kCount, kT3C, kRegSlots>(c, vs, tb, ps, b0 + (v & 0xffff), (v >> 16) != 0, kh2, kh3,
-                                           est, out, ocells, lg, lg2, wk, scr);
+        const int v = sidx[pos], e = v & 0xffff;
+        const uint32_t pv = svar[e];
+        memo_pair<kCount, kT3C, kRegSlots>(c, vs, tb, (int)(pv & 0xffffu), (int)(pv >> 16), b0 + e,
+                                           (v >> 16) != 0, kh2, kh3, est, out, ocells, lg, lg2, wk, scr);
       }
       __syncthreads();
     }
   } else {
     const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long wl = blockIdx.x * (long long)blockDim.x + threadIdx.x; wl < ps.count; wl += stride)
-      memo_pair<kCount, kT3C, kRegSlots>(c, vs, tb, ps, wl, false, kh2, kh3, est, out, ocells, lg,
-                                         lg2, wk, scr);
+    for (long long wl = blockIdx.x * (long long)blockDim.x + threadIdx.x; wl < ps.count; wl += stride) {
+      int va, vb;
+      pair_vars(ps, ps.first + wl, va, vb);
+      memo_pair<kCount, kT3C, kRegSlots>(c, vs, tb, va, vb, wl, false, kh2, kh3, est, out, ocells,
+                                         lg, lg2, wk, scr);
+    }
   }
   if (kCount) flush_work(work, counters);
 }
@@ -1375,7 +1387,6 @@ size_t memo_values(int n) {
 }
 size_t memo_work_bytes(int n) { return memo_values(n) * (sizeof(double) + 2 * sizeof(int)) + 16; }
 
-static size_t memo_tab_bytes(int n) { return ((memo_doubles(n) + 1) & ~size_t(1)) * sizeof(double); }
 
 static size_t memo_smem_fixed(int n, int nval) {
   return sizeof(double) * (size_t)memo_scr_off(memo_layout(n), nval);
@@ -1429,7 +1440,7 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
       vs, tb, memo, memo_val, nval, L, ps, c, est, out, o_cells, CNT ? counters : nullptr)
   // the compact 3-row table starts above n = 26: never with 23 slots.  The
   // sorted-batch order needs the register-staged variant (no scratch rows).
-  const bool srt = regs && memo_sort() && threads == kMemoMaxThreads &&
+  const bool srt = regs && memo_sort() && threads == kMemoMaxThreads && vs.V < 65536 &&
                    sm + kMemoSortBytes <= 226 * 1024;
   if (counters) {
     if (regs == 23)
