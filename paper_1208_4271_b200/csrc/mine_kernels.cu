@@ -1093,14 +1093,11 @@ __device__ __forceinline__ void memo_pair(const MemoCtx& c, const VarSet& vs, co
   small_stats(o, has_y3 ? 3 : 1, est, lg2, out, wl, ocells);
 }
 
-#ifndef MEMO_BATCH
-#define MEMO_BATCH 8
-#endif
-constexpr int kMemoBatch = MEMO_BATCH * kMemoMaxThreads;  // pairs per sorted batch
-// sort buffers after the tables: 1024 bucket counts, the sorted slots, the
-// keys and the pairs' two variables (16 bits each)
-constexpr size_t kMemoSortBytes =
-    sizeof(int) * (1024 + kMemoBatch) + sizeof(uint16_t) * kMemoBatch + sizeof(uint32_t) * kMemoBatch;
+// sort buffers after the tables: 1024 bucket counts, then per pair of the
+// batch its sorted slot, its two variables (16 bits each) and its key
+__host__ __device__ inline size_t memo_sort_bytes(int batch) {
+  return sizeof(int) * (1024 + (size_t)batch) + (sizeof(uint32_t) + sizeof(uint16_t)) * (size_t)batch;
+}
 
 // kCount: the instrumented (untimed) variant with realised-work counters.
 // kT3C: the compact 3-row table (MemoLayout::t3c), a compile-time choice.
@@ -1109,7 +1106,7 @@ constexpr size_t kMemoSortBytes =
 // sort in shared memory), the larger orientation first, so the 32 lanes of a
 // warp run loops of nearly the same trip counts (less divergence).  Results
 // are written at the pairs' own indices; the order changes nothing else.
-template <bool kCount, bool kT3C, int kRegSlots, bool kSort>
+template <bool kCount, bool kT3C, int kRegSlots, int kSortBatch>
 __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Tables tb,
                                                                const double* __restrict__ memo,
                                                                const double* __restrict__ memo_val,
@@ -1117,6 +1114,8 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
                                                                PairSpace ps, double cpar, int est,
                                                                StatsOut out, double* ocells,
                                                                unsigned long long* counters) {
+  constexpr bool kSort = kSortBatch > 0;
+  constexpr int sbatch = kSortBatch > 0 ? kSortBatch : 1024;
   extern __shared__ __align__(16) double msm[];
   const int n = vs.n, B = tb.B;
   {
@@ -1153,21 +1152,22 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
     // the sort buffers follow the tables (no scratch rows with kRegSlots)
     int* hist = reinterpret_cast<int*>(msm + memo_scr_off(L, nval));
     int* sidx = hist + 1024;
-    uint32_t* svar = reinterpret_cast<uint32_t*>(sidx + kMemoBatch);
-    uint16_t* skey = reinterpret_cast<uint16_t*>(svar + kMemoBatch);
+    uint32_t* svar = reinterpret_cast<uint32_t*>(sidx + sbatch);
+    uint16_t* skey = reinterpret_cast<uint16_t*>(svar + sbatch);
+    const int per = sbatch / kMemoMaxThreads;  // consecutive pairs per thread in the sort pass
     __shared__ int wsum[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const long long nbatch = (ps.count + kMemoBatch - 1) / kMemoBatch;
+    const long long nbatch = (ps.count + sbatch - 1) / sbatch;
     for (long long b = blockIdx.x; b < nbatch; b += gridDim.x) {
-      const long long b0 = b * kMemoBatch;
-      const int nb = (int)min((long long)kMemoBatch, ps.count - b0);
+      const long long b0 = b * sbatch;
+      const int nb = (int)min((long long)sbatch, ps.count - b0);
       hist[tid] = 0;
       __syncthreads();
-      // MEMO_BATCH consecutive pairs per thread: one index decode, then steps
+      // `per` consecutive pairs per thread: one index decode, then steps
       int va = 0, vb = 0;
 #pragma unroll 1
-      for (int i = 0; i < MEMO_BATCH; ++i) {
-        const int e = tid * MEMO_BATCH + i;
+      for (int i = 0; i < per; ++i) {
+        const int e = tid * per + i;
         if (e >= nb) break;
         if (i == 0 || ps.kind == kList)
           pair_vars(ps, ps.first + b0 + e, va, vb);
@@ -1284,22 +1284,28 @@ cudaError_t init_kernel_attributes(int device) {
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (e != cudaSuccess) return e;
   const void* fns[] = {reinterpret_cast<const void*>(k_sort_vars),
-                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 0, false>),
-                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 23, false>),
-                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 23, true>),
-                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 30, false>),
-                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 30, true>),
-                       reinterpret_cast<const void*>(k_memo_pairs<false, true, 0, false>),
-                       reinterpret_cast<const void*>(k_memo_pairs<false, true, 30, false>),
-                       reinterpret_cast<const void*>(k_memo_pairs<false, true, 30, true>),
-                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 0, false>),
-                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 23, false>),
-                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 23, true>),
-                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 30, false>),
-                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 30, true>),
-                       reinterpret_cast<const void*>(k_memo_pairs<true, true, 0, false>),
-                       reinterpret_cast<const void*>(k_memo_pairs<true, true, 30, false>),
-                       reinterpret_cast<const void*>(k_memo_pairs<true, true, 30, true>)};
+                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 0, 0>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 23, 0>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 23, 4096>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 23, 8192>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 30, 0>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 30, 4096>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, false, 30, 8192>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, true, 0, 0>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, true, 30, 0>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, true, 30, 4096>),
+                       reinterpret_cast<const void*>(k_memo_pairs<false, true, 30, 8192>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 0, 0>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 23, 0>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 23, 4096>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 23, 8192>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 30, 0>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 30, 4096>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, false, 30, 8192>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, true, 0, 0>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, true, 30, 0>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, true, 30, 4096>),
+                       reinterpret_cast<const void*>(k_memo_pairs<true, true, 30, 8192>)};
   for (const void* f : fns) {
     cudaFuncAttributes fa{};
     e = cudaFuncGetAttributes(&fa, f);
@@ -1436,31 +1442,35 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
   const unsigned blocks = (unsigned)std::min<long long>(sms, need);
   const MemoLayout L = memo_layout(vs.n);
 #define MEMO_LAUNCH(CNT, T3C, RS, SORT)                                                        \
-  k_memo_pairs<CNT, T3C, RS, SORT><<<blocks, threads, sm + (SORT ? kMemoSortBytes : 0), s>>>(   \
+  k_memo_pairs<CNT, T3C, RS, SORT><<<blocks, threads, sm + (SORT ? memo_sort_bytes(SORT) : 0), s>>>( \
       vs, tb, memo, memo_val, nval, L, ps, c, est, out, o_cells, CNT ? counters : nullptr)
   // the compact 3-row table starts above n = 26: never with 23 slots.  The
-  // sorted-batch order needs the register-staged variant (no scratch rows).
-  const bool srt = regs && memo_sort() && threads == kMemoMaxThreads && vs.V < 65536 &&
-                   sm + kMemoSortBytes <= 226 * 1024;
+  // sorted-batch order needs the register-staged variant (no scratch rows)
+  // and pays off only with the y = 2 level loop (B >= 6: x_max = 3); the
+  // batch is the larger of 8192 / 4096 pairs whose buffers fit.
+  int sbatch = 0;
+  if (regs && memo_sort() && threads == kMemoMaxThreads && vs.V < 65536 && tb.B >= 6)
+    for (int b = 8192; b >= 4096 && !sbatch; b /= 2)
+      if (sm + memo_sort_bytes(b) <= 226 * 1024) sbatch = b;
+#define MEMO_T3(CNT, RS, SORT) \
+  (L.t3c ? MEMO_LAUNCH(CNT, true, RS, SORT) : MEMO_LAUNCH(CNT, false, RS, SORT))
+#define MEMO_ALL(CNT)                                                           \
+  if (regs == 23)                                                               \
+    sbatch == 8192 ? MEMO_LAUNCH(CNT, false, 23, 8192)                          \
+    : sbatch == 4096 ? MEMO_LAUNCH(CNT, false, 23, 4096)                        \
+                     : MEMO_LAUNCH(CNT, false, 23, 0);                          \
+  else if (regs)                                                                \
+    sbatch == 8192 ? MEMO_T3(CNT, 30, 8192)                                     \
+    : sbatch == 4096 ? MEMO_T3(CNT, 30, 4096) : MEMO_T3(CNT, 30, 0);            \
+  else                                                                          \
+    MEMO_T3(CNT, 0, 0);
   if (counters) {
-    if (regs == 23)
-      srt ? MEMO_LAUNCH(true, false, 23, true) : MEMO_LAUNCH(true, false, 23, false);
-    else if (regs && srt)
-      L.t3c ? MEMO_LAUNCH(true, true, 30, true) : MEMO_LAUNCH(true, false, 30, true);
-    else if (regs)
-      L.t3c ? MEMO_LAUNCH(true, true, 30, false) : MEMO_LAUNCH(true, false, 30, false);
-    else
-      L.t3c ? MEMO_LAUNCH(true, true, 0, false) : MEMO_LAUNCH(true, false, 0, false);
+    MEMO_ALL(true)
   } else {
-    if (regs == 23)
-      srt ? MEMO_LAUNCH(false, false, 23, true) : MEMO_LAUNCH(false, false, 23, false);
-    else if (regs && srt)
-      L.t3c ? MEMO_LAUNCH(false, true, 30, true) : MEMO_LAUNCH(false, false, 30, true);
-    else if (regs)
-      L.t3c ? MEMO_LAUNCH(false, true, 30, false) : MEMO_LAUNCH(false, false, 30, false);
-    else
-      L.t3c ? MEMO_LAUNCH(false, true, 0, false) : MEMO_LAUNCH(false, false, 0, false);
+    MEMO_ALL(false)
   }
+#undef MEMO_ALL
+#undef MEMO_T3
 #undef MEMO_LAUNCH
 }
 

@@ -487,3 +487,52 @@ def test_large_n_variants_forced(force):
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0 and "OK" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("n", [16, 23, 28, 31])
+def test_memo_sorted_batches_all_pair_kinds(engine, oracle, n):
+    """The memo tier runs pairs in sorted batches of 8192: cross
+    and list calls and an unaligned pairwise window, several batches each,
+    bit-exact against the oracle."""
+    rng = np.random.default_rng(100 + n)
+    V = rng.standard_normal((160, n))
+    V[::7] = np.round(V[::7] * 2.0)  # some tied variables (sentinel fusing)
+    X, Y = V[:110], V[110:]
+    res = engine.cross(X, Y)
+    xi = np.repeat(np.arange(110), 50)
+    yi = 110 + np.tile(np.arange(50), 110)
+    want = oracle.pairs(V, xi, yi, 0.6, 15.0, 0)
+    assert_bit_equal(stats_matrix(res), want, f"cross n={n}")
+    total = 160 * 159 // 2
+    first, count = 1234, total - 1234 - 17
+    res = engine.pairwise(V, first=first, count=count)
+    want = oracle.pairwise(V, first=first, count=count)
+    assert_bit_equal(stats_matrix(res), want, f"pairwise window n={n}")
+    xi = rng.integers(0, 160, 9000)
+    yi = rng.integers(0, 160, 9000)
+    res = engine.pairs(V, xi, yi)
+    want = oracle.pairs(V, xi, yi, 0.6, 15.0, 0)
+    assert_bit_equal(stats_matrix(res), want, f"list n={n}")
+
+
+def test_memo_sort_off_same_bits(tmp_path):
+    """MINE_B200_MEMO_SORT=0 (one pair per thread in index order) and the
+    default sorted batches give the same bits."""
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "run.py"
+    script.write_text(
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        "from paper_1208_4271_b200 import Engine, datagen\n"
+        "w = datagen.make(1)\n"
+        "r = Engine(0).pairwise(w.X[:400])\n"
+        "np.save(sys.argv[1], np.stack([r[k] for k in ('mic', 'mas', 'mev', 'mcn', 'mic_e', 'tic')]))\n")
+    outs = []
+    for flag in ("0", "1"):
+        out = tmp_path / f"o{flag}.npy"
+        env = dict(os.environ, MINE_B200_MEMO_SORT=flag)
+        subprocess.run([sys.executable, str(script), str(out)], env=env, check=True, timeout=600)
+        outs.append(np.load(out))
+    assert_bit_equal(outs[0], outs[1], "sorted vs index order")
