@@ -338,21 +338,36 @@ __host__ __device__ inline size_t fslot_doubles(int kc, int LW) {
 
 struct DpLayout {
   size_t cb, cum, A, W, acc, fs, ft, total;
+  int fsw, ftw;  // staged / tile F row widths (doubles)
 };
 
-constexpr int kFsW = 64;       // staged F row width (levels l0-1 .. l1-1)
-// Staged row layout: level offset j = 4 g + i (g: the consumer's level group)
-// sits at 2 g + i for i < 2 and at 32 + 2 g + (i - 2) otherwise, so the
-// 16-byte loads of consecutive groups are contiguous (no bank conflicts).
-__host__ __device__ inline int fs_col(int j) {
+// Staged F rows (levels l0-1 .. l1-1) are 4 ngc doubles wide, ngc = the
+// level groups of the widest level tile (nlc = min(64, x_max - 2) levels).
+// Level offset j = 4 g + i (g: the consumer's group) sits at 2 g + i for
+// i < 2 and at 2 ng + 2 g + (i - 2) otherwise (ng: this tile's groups; 32 in
+// the 64-wide rows of the wide variants), so the 16-byte loads of consecutive
+// groups are contiguous (no bank conflicts).
+__host__ __device__ inline int fs_col(int j, int fo) {  // fo: offset of levels 2, 3 (2 ng)
   const int g = j >> 2, i = j & 3;
-  return (i < 2 ? 0 : 30) + 2 * g + i;
+  return (i < 2 ? 0 : fo - 2) + 2 * g + i;
 }
-constexpr int kFtW = 65;       // tile F row width (levels l0-1 .. l1)
+#ifndef KDP_LEAN_XMAX
+#define KDP_LEAN_XMAX 64
+#endif
+constexpr int kLeanXMax = KDP_LEAN_XMAX;
+#ifndef DP_COMPACT
+#define DP_COMPACT 1
+#endif
+__host__ __device__ inline int dp_nlc(int x_max) { return !DP_COMPACT || x_max - 2 >= 64 ? 64 : x_max - 2; }
+__host__ __device__ inline int dp_ngc(int x_max) { return (dp_nlc(x_max) + 3) >> 2; }
 
 // kGlobalTables: cb and cum are read in place from the subproblem's
 // GenScratch slot instead of being staged (for c B too large for the chip).
-__host__ __device__ inline DpLayout dp_layout(int y, int kc, bool global_tables = false) {
+// The staged F rows (fs) and the accumulator hand-over (acc, the owners'
+// cells only) share one region: acc is written after a tile's last chunk and
+// read by its inner part, fs only by the chunks.
+__host__ __device__ inline DpLayout dp_layout(int y, int kc, int x_max, bool global_tables,
+                                              bool lean) {
   DpLayout L;
   size_t o = 0;
   L.cb = o;
@@ -363,12 +378,24 @@ __host__ __device__ inline DpLayout dp_layout(int y, int kc, bool global_tables 
   o += al16(sizeof(double) * kMaxTile * kMaxTile);
   L.W = o;
   o += al16(sizeof(double) * kMaxTile * kMaxTile);
+  // compact widths for the lean variant only (gen_dp_lean); the others use
+  // 64 / 65
+  const int ngc = lean ? dp_ngc(x_max) : 16;
+  L.fsw = 4 * ngc;
+  L.ftw = lean ? dp_nlc(x_max) + 1 : 65;
+  const size_t acc_b = sizeof(double) * (size_t)(kMaxTile / 2) * ngc * kAccStride;
+  const size_t fs_b = sizeof(double) * (size_t)kMaxTile * L.fsw;
   L.acc = o;
-  o += al16(sizeof(double) * kDpThreads * kAccStride);
-  L.fs = o;
-  o += al16(sizeof(double) * kMaxTile * kFsW);
+  if (!lean) {  // wide variants: separate regions, as sized before the lean variant
+    o += al16(sizeof(double) * kDpThreads * kAccStride);
+    L.fs = o;
+    o += al16(fs_b);
+  } else {
+    L.fs = o;
+    o += al16(acc_b > fs_b ? acc_b : fs_b);
+  }
   L.ft = o;
-  o += al16(sizeof(double) * kMaxTile * kFtW);
+  o += al16(sizeof(double) * (size_t)kMaxTile * L.ftw);
   L.total = o;
   return L;
 }
@@ -467,8 +494,14 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 // F lives in a per-CTA HBM slot (L2-resident for typical sizes); each outer
 // s-chunk's rows are staged into shared memory with coalesced loads, and the
 // current t-tile's rows are kept in shared memory while its inner part runs.
-template <bool kGlobalTables, bool kRing>
-__global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, PairSpace ps,
+#ifndef KDP_MIN_BLOCKS
+#define KDP_MIN_BLOCKS 4
+#endif
+// kLean: x_max <= kLeanXMax (one level tile of <= 62 levels): compiled for 64
+// registers so 4 CTAs share an SM; the wider variants keep 80 (3 per SM).
+
+template <bool kGlobalTables, bool kRing, bool kLean>
+__global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : 3) k_dp(VarSet vs, Tables tb, PairSpace ps,
                                                       long long base, long long nsub, YParams yp,
                                                       GenScratch gs, double* __restrict__ ocells,
                                                       SubDebug dbg, int has_dbg, int orient_only) {
@@ -476,7 +509,9 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
   __shared__ long long s_sub;
   const int tid = threadIdx.x;
   const int y = yp.y, x_max = yp.x_max, kc = gs.kc, LW = x_max - 1;
-  const DpLayout L = dp_layout(y, kc, kGlobalTables);
+  const DpLayout L = dp_layout(y, kc, x_max, kGlobalTables, kLean);
+  // row widths: compile-time for the wide variants (x_max > 64: 64 / 65)
+  const int fsw = kLean ? L.fsw : 64, ftw = kLean ? L.ftw : 65;
   int* cb = reinterpret_cast<int*>(smem + L.cb);
   int* cum = reinterpret_cast<int*>(smem + L.cum);
   double* A = reinterpret_cast<double*>(smem + L.A);
@@ -530,6 +565,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
     for (int l0 = 3; l0 <= l_max; l0 += 64) {
       const int l1 = min(l0 + 63, l_max), nl = l1 - l0 + 1;
       const int ng = (nl + 3) >> 2;
+      const int fo = kLean ? 2 * ng : 32;  // staged row offset of levels 2, 3 of a group
       const int T = max(2, min(kMaxTile, 2 * (kDpThreads / ng)));
       const int t_lo = (l0 == l_max) ? k : l0;  // level l_max is needed at t = k only
       const int my_tp = tid / ng, my_g = tid - my_tp * ng;
@@ -550,7 +586,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
           // terms' gathers run; no registers are held across span_terms
           for (int i = tid; i < ns * nl; i += kDpThreads) {
             const int sl = i / nl, j = i - sl * nl;
-            cp_async8(fs + sl * kFsW + fs_col(j), F + (size_t)(s0 + sl) * RW + (((l0 - 3) + j) & cm));
+            cp_async8(fs + sl * fsw + fs_col(j, fo), F + (size_t)(s0 + sl) * RW + (((l0 - 3) + j) & cm));
           }
           span_terms(tb, cb, cum, kk, rows, k, s0, ns, t0, nt, A, W);
           cp_async_wait_all();
@@ -558,7 +594,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
           span_terms(tb, cb, cum, kk, rows, k, s0, ns, t0, nt, A, W);
           for (int i = tid; i < ns * nl; i += kDpThreads) {  // stage F(s, l0-1 .. l1-1)
             const int sl = i / nl, j = i - sl * nl;
-            fs[sl * kFsW + fs_col(j)] = F[(size_t)(s0 + sl) * RW + (((l0 - 3) + j) & cm)];
+            fs[sl * fsw + fs_col(j, fo)] = F[(size_t)(s0 + sl) * RW + (((l0 - 3) + j) & cm)];
           }
 #endif
           __syncthreads();
@@ -575,7 +611,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
 #pragma unroll
               for (int i = 0; i < 4; ++i)
                 if (s >= my_l + i - 1) {
-                  const double f = fr[sl * kFsW + (i < 2 ? i : 30 + i)];
+                  const double f = fr[sl * fsw + (i < 2 ? i : fo - 2 + i)];
                   acc[i] = dmax(acc[i], __dsub_rn(__dmul_rn(a.x, f), w.x));
                   acc[4 + i] = dmax(acc[4 + i], __dsub_rn(__dmul_rn(a.y, f), w.y));
                 }
@@ -584,8 +620,8 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
             for (; sl < ns; ++sl) {
               const double2 a = *reinterpret_cast<const double2*>(A + sl * kMaxTile + my_tl);
               const double2 w = *reinterpret_cast<const double2*>(W + sl * kMaxTile + my_tl);
-              const double2 f01 = *reinterpret_cast<const double2*>(fr + sl * kFsW);
-              const double2 f23 = *reinterpret_cast<const double2*>(fr + sl * kFsW + 32);
+              const double2 f01 = *reinterpret_cast<const double2*>(fr + sl * fsw);
+              const double2 f23 = *reinterpret_cast<const double2*>(fr + sl * fsw + fo);
               acc[0] = dmax(acc[0], __dsub_rn(__dmul_rn(a.x, f01.x), w.x));
               acc[1] = dmax(acc[1], __dsub_rn(__dmul_rn(a.x, f01.y), w.x));
               acc[2] = dmax(acc[2], __dsub_rn(__dmul_rn(a.x, f23.x), w.x));
@@ -599,12 +635,13 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
           __syncthreads();
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) accS[tid * kAccStride + i] = acc[i];
+        for (int i = 0; i < 8; ++i)
+          if (my_tp < kMaxTile / 2) accS[tid * kAccStride + i] = acc[i];
         // ---- inner part: s inside the tile, one t at a time, a level per
         // thread; only the warps holding levels take part (named barrier).
         span_terms(tb, cb, cum, kk, rows, k, t0, nt, t0, nt, A, W);
         for (int tl = tid; tl < nt; tl += kDpThreads)  // column 0: level l0 - 1
-          ft[tl * kFtW] = F[(size_t)(t0 + tl) * RW + ((l0 - 3) & cm)];
+          ft[tl * ftw] = F[(size_t)(t0 + tl) * RW + ((l0 - 3) & cm)];
         __syncthreads();
         if (tid < inner_threads) {
           const int ll = tid, l = l0 + ll;
@@ -617,10 +654,10 @@ __global__ void __launch_bounds__(kDpThreads, 3) k_dp(VarSet vs, Tables tb, Pair
               const double* Wp = W + tl;
               for (int s = max(t0, l - 1); s < tt; ++s) {
                 const int sl = s - t0;
-                m = dmax(m, __dsub_rn(__dmul_rn(Ap[sl * kMaxTile], ft[sl * kFtW + ll]),
+                m = dmax(m, __dsub_rn(__dmul_rn(Ap[sl * kMaxTile], ft[sl * ftw + ll]),
                                       Wp[sl * kMaxTile]));
               }
-              ft[tl * kFtW + ll + 1] = m;
+              ft[tl * ftw + ll + 1] = m;
               F[(size_t)tt * RW + ((l - 2) & cm)] = m;
               if (kRing && tt == k) fk[l - 2] = m;
             }
@@ -787,7 +824,7 @@ int gen_kc(int n, const YParams& yp) { return std::min(n, yp.k_hat); }
 
 bool gen_tables_global(int n, const YParams& yp) {
   static const bool force = std::getenv("MINE_B200_DP_GLOBAL") != nullptr;
-  return force || dp_layout(yp.y, gen_kc(n, yp), false).total > 200 * 1024;
+  return force || dp_layout(yp.y, gen_kc(n, yp), yp.x_max, false, false).total > 200 * 1024;
 }
 
 bool gen_pts_global(int n, const YParams& yp) {
@@ -812,8 +849,15 @@ size_t gen_pf_smem(int n, const YParams& yp) {
 
 bool gen_dp_f_in_smem(int, const YParams&) { return false; }
 
+// The lean k_dp (64 registers) pays off only where its compact layout lets 4
+// CTAs share an SM; alone on an SM the 80-register variant is faster (c4).
+bool gen_dp_lean(int n, const YParams& yp) {
+  if (gen_tables_global(n, yp) || yp.x_max > kLeanXMax) return false;
+  return dp_layout(yp.y, gen_kc(n, yp), yp.x_max, false, true).total + 1024 <= 228 * 1024 / 4;
+}
+
 size_t gen_dp_smem(int n, const YParams& yp) {
-  return dp_layout(yp.y, gen_kc(n, yp), gen_tables_global(n, yp)).total;
+  return dp_layout(yp.y, gen_kc(n, yp), yp.x_max, gen_tables_global(n, yp), gen_dp_lean(n, yp)).total;
 }
 
 size_t gen_fslot_bytes(int n, const YParams& yp) {
@@ -825,7 +869,9 @@ int gen_dp_grid(int n, const YParams& yp) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t sm = gen_dp_smem(n, yp);
-  const int per = (int)std::max<size_t>(1, std::min<size_t>(512 / kDpThreads * 2, (228 * 1024) / (sm + 1024)));
+  // up to 4 CTAs per SM, as shared memory allows (the wide variants are
+  // register-bound at 3 resident; their extra CTAs start as others finish)
+  const int per = (int)std::max<size_t>(1, std::min<size_t>(4, (228 * 1024) / (sm + 1024)));
   // the F slots of one lane stay within 4 GB (very large c B)
   const long long cap = std::max<long long>(1, (4LL << 30) / (long long)gen_fslot_bytes(n, yp));
   return (int)std::min<long long>((long long)sms * per, cap);
@@ -906,14 +952,17 @@ void launch_dp(const VarSet& vs, const Tables& tb, const PairSpace& ps, long lon
   const size_t sm = gen_dp_smem(vs.n, yp);
   const int dg = dbg ? 1 : 0;
   if (gs.tables_global)
-    k_dp<true, true><<<grid, kDpThreads, sm, s>>>(vs, tb, ps, base, nsub, yp, gs, ocells, d, dg,
-                                                  orient_only);
+    k_dp<true, true, false><<<grid, kDpThreads, sm, s>>>(vs, tb, ps, base, nsub, yp, gs, ocells,
+                                                         d, dg, orient_only);
   else if (yp.x_max - 1 > kFRing)
-    k_dp<false, true><<<grid, kDpThreads, sm, s>>>(vs, tb, ps, base, nsub, yp, gs, ocells, d, dg,
-                                                   orient_only);
+    k_dp<false, true, false><<<grid, kDpThreads, sm, s>>>(vs, tb, ps, base, nsub, yp, gs, ocells,
+                                                          d, dg, orient_only);
+  else if (!gen_dp_lean(vs.n, yp))
+    k_dp<false, false, false><<<grid, kDpThreads, sm, s>>>(vs, tb, ps, base, nsub, yp, gs, ocells,
+                                                           d, dg, orient_only);
   else
-    k_dp<false, false><<<grid, kDpThreads, sm, s>>>(vs, tb, ps, base, nsub, yp, gs, ocells, d, dg,
-                                                    orient_only);
+    k_dp<false, false, true><<<grid, kDpThreads, sm, s>>>(vs, tb, ps, base, nsub, yp, gs, ocells,
+                                                          d, dg, orient_only);
 }
 
 cudaError_t init_general_attributes(int device) {
@@ -924,9 +973,10 @@ cudaError_t init_general_attributes(int device) {
                        reinterpret_cast<const void*>(k_part_f2<128, false, false>),
                        reinterpret_cast<const void*>(k_part_f2<256, true, false>),
                        reinterpret_cast<const void*>(k_part_f2<256, true, true>),
-                       reinterpret_cast<const void*>(k_dp<false, false>),
-                       reinterpret_cast<const void*>(k_dp<false, true>),
-                       reinterpret_cast<const void*>(k_dp<true, true>),
+                       reinterpret_cast<const void*>(k_dp<false, false, false>),
+                       reinterpret_cast<const void*>(k_dp<false, false, true>),
+                       reinterpret_cast<const void*>(k_dp<false, true, false>),
+                       reinterpret_cast<const void*>(k_dp<true, true, false>),
                        reinterpret_cast<const void*>(k_dp_warp)};
   for (const void* f : fns) {
     cudaFuncAttributes fa{};
