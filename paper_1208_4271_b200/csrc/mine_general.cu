@@ -566,6 +566,9 @@ __global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : 3) k_dp(V
       const int l1 = min(l0 + 63, l_max), nl = l1 - l0 + 1;
       const int ng = (nl + 3) >> 2;
       const int fo = kLean ? 2 * ng : 32;  // staged row offset of levels 2, 3 of a group
+      // this thread's first staged element and its stride in (row, level)
+      const int st_sl = tid / nl, st_j = tid - st_sl * nl;
+      const int st_dsl = kDpThreads / nl, st_dj = kDpThreads - st_dsl * nl;
       const int T = max(2, min(kMaxTile, 2 * (kDpThreads / ng)));
       const int t_lo = (l0 == l_max) ? k : l0;  // level l_max is needed at t = k only
       const int my_tp = tid / ng, my_g = tid - my_tp * ng;
@@ -584,9 +587,16 @@ __global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : 3) k_dp(V
 #if KDP_PREFETCH
           // stage F(s, l0-1 .. l1-1) by cp.async, in flight while the span
           // terms' gathers run; no registers are held across span_terms
-          for (int i = tid; i < ns * nl; i += kDpThreads) {
-            const int sl = i / nl, j = i - sl * nl;
+          // element i = tid + 256 u of the (row, level) grid, walked without
+          // a division per element
+          for (int sl = st_sl, j = st_j; sl < ns;) {
             cp_async8(fs + sl * fsw + fs_col(j, fo), F + (size_t)(s0 + sl) * RW + (((l0 - 3) + j) & cm));
+            sl += st_dsl;
+            j += st_dj;
+            if (j >= nl) {
+              j -= nl;
+              ++sl;
+            }
           }
           span_terms(tb, cb, cum, kk, rows, k, s0, ns, t0, nt, A, W);
           cp_async_wait_all();
