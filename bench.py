@@ -11,11 +11,19 @@ over the whole pair batch.  `value` is device-resident throughput (inputs in
 HBM, CUDA events on the launching stream, L2 flushed before every step, max
 over ranks); `e2e` is the same metric through the C ABI with pinned HOST
 buffers (H2D of the variables and D2H of MIC+TIC inside the timed region).
-Multi-GPU (torchrun): weak scaling -- the dataset grows to p = round(4381
-sqrt(N)) variables so every GPU keeps ~9.59M pairs, sharded by contiguous
-condensed-index range; no collective touches the data path.
+Multi-GPU (torchrun): strong scaling by default -- the unchanged c1 (all
+9,594,390 pairs) is sharded by contiguous condensed-index range, each rank
+scores its slice and the slices are gathered to rank 0 inside the timed
+region (the only collective; none on the data path).  `--scaling weak` grows
+the dataset to p = round(4381 sqrt(N)) so every GPU keeps ~9.59M pairs.
 `--impl reference` times the reference's own CPU engine (oracle/_ref, built
-from /root/reference/proj/src) with all host threads on a bounded sample.
+from /root/reference/proj/src) with all host threads: whole c1 steps (all
+9.59M pairs each), at most 1 warm-up + 3 timed steps so the arm ends in
+about a minute.
+The default line also carries `secondary`: the other BASELINE configs (c0 all
+256 pairs, c2 a 20k-pair window, c3 a 4k-pair window, c4 32 pairs) with
+device and end-to-end pairs/s, SURVEY 8(d)'s roofline, the reference engine's
+CPU rate on a sample and a bit-exact-on-sample flag.
 """
 from __future__ import annotations
 
@@ -42,23 +50,36 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def workload(n_gpus: int):
+def workload(n_gpus: int, scaling: str = "strong"):
     from paper_1208_4271_b200 import datagen
-    p = BASE_P if n_gpus == 1 else int(round(BASE_P * math.sqrt(n_gpus)))
+    p = BASE_P if (n_gpus == 1 or scaling == "strong") else int(round(BASE_P * math.sqrt(n_gpus)))
     return datagen.config1(p=p), p
 
 
-def config_dict(w, p, n_gpus, total):
+def config_dict(w, p, n_gpus, total, scaling="strong"):
+    weak = n_gpus > 1 and scaling == "weak"
     return {
         "workload": f"c1: all pairs of p={p} variables x n={w.n} samples (BASELINE configs[1]"
-                    f"{'' if n_gpus == 1 else ', weak-scaled p=round(4381*sqrt(N))'}), "
+                    f"{', weak-scaled p=round(4381*sqrt(N))' if weak else ''}), "
                     f"alpha={w.alpha}, c={w.c}, est=MIC_approx",
         "p": p, "n": w.n, "pairs_per_step": total,
         "stats_written": ["mic", "tic"],
         "l2": "flushed (256 MiB write) before every timed step",
         "inputs": "HBM-resident (value); pinned host (e2e)",
-        "parallelism": f"pairs sharded by condensed-index range over {n_gpus} GPU(s), no collective",
+        "parallelism": f"pairs sharded by condensed-index range over {n_gpus} GPU(s); "
+                       + ("slices gathered to rank 0 inside the timed region (NCCL all_gather)"
+                          if n_gpus > 1 else "no collective"),
     }
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -128,6 +149,46 @@ def hbm_line(bytes_per_launch: int, kern_s: float) -> dict:
             "bytes_per_launch": int(bytes_per_launch), "peak_source": src}
 
 
+def probe_general(device: int, table_bytes: float):
+    """Random 8-byte L2 gathers/s from a table of `table_bytes` (the span
+    terms' p*log(p) lookups) and exact DP candidates/s (probes.cu)."""
+    import ctypes
+    from paper_1208_4271_b200 import _build
+    L = ctypes.CDLL(_build.PROBES)
+    D = ctypes.POINTER(ctypes.c_double)
+    L.mine_b200_probe_general.argtypes = [ctypes.c_int, ctypes.c_double, D, D]
+    a, b = ctypes.c_double(0), ctypes.c_double(0)
+    if L.mine_b200_probe_general(device, float(table_bytes), ctypes.byref(a), ctypes.byref(b)) != 0:
+        return None, None
+    return a.value, b.value
+
+
+def roofline_8d(work: dict, t_s: float, out_bytes: int, peaks: dict) -> dict:
+    """T_roof = max(2 C / R_fp64, N_pv / R_lsu, bytes_out / BW)
+    with C = every DP candidate of levels l = 2 .. l_max (F(t,2) included),
+    N_pv = the partition's point visits; fraction = T_roof / t_s."""
+    C = int(work["dp_candidates"]) + int(work.get("f2_candidates", 0))
+    npv = int(work["point_visits"])
+    terms = {"fp64": 2 * C / peaks["fp64_per_s"],
+             "lsu": npv / peaks["lsu_per_s"],
+             "hbm": out_bytes / (peaks["hbm_gbs"] * 1e9)}
+    bound = max(terms, key=terms.get)
+    return {"t_roof_s": terms[bound], "bound": bound, "terms_s": terms, "t_measured_s": t_s,
+            "frac": terms[bound] / t_s, "C": C, "N_pv": npv, "bytes_out": int(out_bytes),
+            "peaks": {"R_fp64 (DADD/s, probes.cu k_dadd)": peaks["fp64_per_s"],
+                      "R_lsu (random 8 B shared gathers/s, probes.cu k_lds)": peaks["lsu_per_s"],
+                      "BW_hbm (GB/s, MEASURED_PEAKS.json)": peaks["hbm_gbs"]}}
+
+
+def measured_peaks(device: int) -> dict:
+    dadd, lds, lds2 = probe_peaks(device)
+    try:
+        hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except Exception:
+        hbm = 6650.0
+    return {"fp64_per_s": dadd, "lsu_per_s": lds, "lsu2_per_s": lds2, "hbm_gbs": hbm}
+
+
 def probe_peaks(device: int):
     import ctypes
     from paper_1208_4271_b200 import _build
@@ -165,31 +226,57 @@ def cpu_reference(w, p, budget_s: float, cores: int):
     pairs = pp * (pp - 1) // 2
     assert len(out) == pairs
     return {"value": pairs / dt, "unit": UNIT, "cores": cores, "kind": kind,
+            "cpu_model": cpu_model(),
             "sample": f"all {pairs} pairs of the first {pp} of the {p} c1 variables "
                       f"(run_analysis, workers={cores}), {dt:.1f} s"}
 
 
 # ---------------------------------------------------------------------------
 def run_reference(args, world, rank):
+    """The reference's own run_analysis (oracle/_ref: the unmodified
+    reference sources) over ALL c1 pairs per step, all host threads.  A step
+    takes ~18 s on 16 cores, so at most 1 warm-up + 3 timed steps run (the
+    JSON says how many; steps_requested keeps the driver's K / W)."""
     if rank != 0:
         return
-    w, p = workload(world)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    w, p = workload(world, args.scaling)
     cores = os.cpu_count() or 1
-    per_step = max(2.0, min(20.0, 150.0 / max(args.steps + args.warmup, 1)))
-    vals = []
-    for i in range(args.warmup + args.steps):
-        r = cpu_reference(w, p, per_step, cores)
-        if i >= args.warmup:
-            vals.append(r["value"])
-    v = statistics.median(vals)
+    try:
+        R = O.Reference()
+        kind = "reference"
+        run = lambda: R.run_analysis(w.X, w.alpha, w.c, workers=cores)  # noqa: E731
+    except FileNotFoundError:
+        Or = O.Oracle()
+        kind = "port"
+        run = lambda: Or.pairwise(w.X, w.alpha, w.c, threads=cores)  # noqa: E731
     total = p * (p - 1) // 2
+    warm, steps = min(args.warmup, 1), max(1, min(args.steps, 3))
+    for _ in range(warm):
+        run()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        out = run()
+        times.append(time.perf_counter() - t0)
+        assert len(out) == total
+    dt = sum(times)
+    v = total * steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / v * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "steps": steps, "warmup": warm,
+        "steps_requested": args.steps, "warmup_requested": args.warmup,
+        "ms_per_step": dt / steps * 1e3,
+        "higher_is_better": True, "scaling": args.scaling if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded c1 generator, numpy PCG64 seed 43)",
-        "config": config_dict(w, p, world, total),
-        "cpu_baseline": {**r, "value": v},
+        "config": config_dict(w, p, world, total, args.scaling),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+                         "cpu_model": cpu_model(),
+                         "sample": f"whole c1 steps: all {total} pairs per step "
+                                   f"(run_analysis, workers={cores}); {warm} warm-up + "
+                                   f"{steps} timed steps, {dt:.1f} s timed"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -205,17 +292,20 @@ def run_ours(args, world, rank, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
-    w, p = workload(world)
+    w, p = workload(world, args.scaling)
     n = w.n
     total = p * (p - 1) // 2
     first = rank * total // world
     count = (rank + 1) * total // world - first
+    slot = (total + world - 1) // world  # equal gather slots (the last ones padded)
     params = Parameters(w.alpha, w.c, 0)
     eng = Engine(local)
 
     dv = torch.from_numpy(w.X).to(dev).contiguous()
-    outs = {k: torch.empty(count, dtype=torch.float64, device=dev) for k in ("mic", "tic")}
+    outs = {k: torch.empty(slot, dtype=torch.float64, device=dev) for k in ("mic", "tic")}
     ptrs = {k: t.data_ptr() for k, t in outs.items()}
+    gathered = ({k: torch.empty(slot * world, dtype=torch.float64, device=dev) for k in outs}
+                if dist else None)
     stream = torch.cuda.Stream(dev)  # a real stream: the engine enqueues on it
     torch.cuda.set_stream(stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -224,6 +314,9 @@ def run_ours(args, world, rank, local):
     def step(kb=None, ke=None):
         eng.pairwise_device(dv.data_ptr(), p, n, params, ptrs, stream=stream.cuda_stream,
                             first=first, count=count, ev_begin=kb or 0, ev_end=ke or 0)
+        if dist:  # the final gather of the condensed slices (strong and weak)
+            for k in outs:
+                dist.all_gather_into_tensor(gathered[k], outs[k])
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -276,10 +369,12 @@ def run_ours(args, world, rank, local):
     if dist:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_value = total * args.steps / float(e2e_s.item())
-    same = bool(np.array_equal(hout["mic"].view(np.int64), outs["mic"].cpu().numpy().view(np.int64)))
+    same = bool(np.array_equal(hout["mic"].view(np.int64),
+                               outs["mic"][:count].cpu().numpy().view(np.int64)))
 
     if rank == 0:
-        dadd, lds, lds2 = probe_peaks(local)
+        peaks = measured_peaks(local)
+        dadd, lds, lds2 = peaks["fp64_per_s"], peaks["lsu_per_s"], peaks["lsu2_per_s"]
         kern_s = statistics.mean(kern_ms) / 1e3
         g8, g2 = work["gathers"], work["rank_gathers"]
         gathers = g8 + g2
@@ -298,17 +393,19 @@ def run_ours(args, world, rank, local):
                 "traffic": traffic,
                 "traffic_source": "profiles/ncu_traffic.json (dram read+write bytes per launch, ncu)",
                 "kernel": "k_memo_pairs (the pair-scoring launch of a step)",
-                "per_launch_work": {k: int(v) * world for k, v in work.items()},
+                "per_launch_work": {k: int(v) for k, v in work.items()},
                 "work_unit": "shared-memory table gathers the memo-tier algorithm needs "
                              "(one 2 B dense candidate rank per F(t,2) candidate, 2 x 8 B per "
                              "level-3 span term, 2 B rank per standard 3-row candidate, 7 x 8 B "
                              "per other 3-row candidate), counted by the kernel; DESIGN.md "
                              "'Roofline'",
-                "gathers_8b": int(g8) * world, "gathers_rank": int(g2) * world,
+                "gathers_8b": int(g8), "gathers_rank": int(g2),
                 "peak_source": "measured live: probes.cu k_lds (random 8 B gathers, 561-entry "
                                "table) and k_lds2 (random 2 B gathers, 16K-entry table), 8 "
                                "streams/thread, all SMs; peak = time-weighted mix of the two",
                 "kernel_ms": statistics.mean(kern_ms),
+                # SURVEY 8(d)'s own T_roof for the same launch (rank 0's slice)
+                "survey_8d": roofline_8d(work, kern_s, 16 * count + 96 * p, peaks),
                 # the HBM roofline for the same launch, for completeness: the
                 # algorithmic bytes are the outputs (MIC + TIC, 16 B per pair)
                 # plus the per-variable records read (96 B per variable)
@@ -322,23 +419,191 @@ def run_ours(args, world, rank, local):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded c1 generator, numpy PCG64 seed 43)",
-            "config": config_dict(w, p, world, total),
+            "config": config_dict(w, p, world, total, args.scaling),
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": int(w.X.nbytes) * world,
                     "d2h_bytes_per_step": int(total * 8 * 2),
                     "matches_value_leg": same},
-            "gpu_launches": int(launches) * args.steps * world,
+            "gpu_launches": int(launches) * args.steps,
             "clocks": clk.summary(),
             "roofline": roof,
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_reference(w, p, args.cpu_seconds, os.cpu_count() or 1)
+        if world == 1 and not args.no_secondary:
+            line["secondary"] = secondary_block(eng, local, peaks, args)
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# Secondary configs: the heavy-DP general tier, observed
+# by the driver in the default line.
+SECONDARY = (  # (config, pair window, CPU-reference sample pairs)
+    (0, 256, 256),
+    (2, 20000, 4000),
+    (3, 4000, 320),
+    (4, 32, 0),   # CPU rate and parity from the committed full-size fixture
+)
+
+
+def _ref_stats_parallel(R, X, Y, xi, yi, alpha, c, threads):
+    """The reference's compute_statistics per pair (statistics.cpp:53-63) on
+    a host thread pool -- run_analysis's own parallelism (analysis.cpp:
+    148-190); ctypes releases the GIL inside each call."""
+    from concurrent.futures import ThreadPoolExecutor
+    out = np.zeros((len(xi), 6))
+
+    def one(i):
+        out[i] = R.statistics(X[xi[i]], Y[yi[i]], alpha, c)
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(one, range(len(xi))))
+    return out
+
+
+def secondary_block(eng, device, peaks, args):
+    import torch
+    from paper_1208_4271_b200 import Parameters, datagen, cell_shapes, grid_bound
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    try:
+        R = O.Reference()
+    except FileNotFoundError:
+        R = None
+    cores = os.cpu_count() or 1
+    dev = torch.device("cuda", device)
+    stream = torch.cuda.current_stream(dev)
+    res = []
+    l2_rate, cand_rate = probe_general(device, 8.0 * 1341 * 1342 / 2)
+    for cfg, window, cpu_pairs in SECONDARY:
+        t_start = time.perf_counter()
+        w = datagen.make(cfg)
+        params = Parameters(w.alpha, w.c, w.est)
+        if w.call == "pairwise":
+            V = w.X
+            total = V.shape[0] * (V.shape[0] - 1) // 2
+            count = min(window, total)
+            xi = yi = None
+        elif w.call == "cross":
+            V = np.ascontiguousarray(np.concatenate([w.X, w.Y]))
+            count = min(window, w.X.shape[0] * w.Y.shape[0])
+            xi = np.arange(count, dtype=np.int32) // w.Y.shape[0]
+            yi = (w.X.shape[0] + np.arange(count) % w.Y.shape[0]).astype(np.int32)
+            if cfg == 4:  # the pairs of the full-size reference fixture
+                g = np.load(os.path.join(ROOT, "tests", "golden", "ref_c4_full.npz"))
+                xi = g["xi"].astype(np.int32)[:window]
+                yi = (w.X.shape[0] + g["yi"]).astype(np.int32)[:window]
+                count = xi.size
+        else:
+            V = w.X
+            xi, yi = w.xi.astype(np.int32), w.yi.astype(np.int32)
+            count = xi.size
+        dV = torch.from_numpy(np.ascontiguousarray(V)).to(dev)
+        douts = {k: torch.empty(count, dtype=torch.float64, device=dev)
+                 for k in ("mic", "mas", "mev", "mcn", "tic")}
+        dptr = {k: t.data_ptr() for k, t in douts.items()}
+        kind = "pairwise" if xi is None else "pairs"
+        dxi = torch.from_numpy(xi).to(dev) if xi is not None else None
+        dyi = torch.from_numpy(yi).to(dev) if yi is not None else None
+
+        def dcall(counters=False, kb=0, ke=0):
+            return eng.device_call(kind, params, dptr, vars_ptr=dV.data_ptr(), p=V.shape[0],
+                                   n=V.shape[1], xi_ptr=dxi.data_ptr() if dxi is not None else 0,
+                                   yi_ptr=dyi.data_ptr() if dyi is not None else 0,
+                                   npairs=count, first=0, count=count if kind == "pairwise" else 0,
+                                   stream=stream.cuda_stream, counters=counters,
+                                   ev_begin=kb, ev_end=ke)
+
+        def hcall():
+            if kind == "pairwise":
+                return eng.pairwise(V, params, first=0, count=count, stats=("mic", "tic"))
+            return eng.pairs(V, xi, yi, params, stats=("mic", "tic"))
+
+        reps = 1 if cfg == 4 else 3
+        dcall()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(reps)]
+        for a, b in ev:
+            a.record(stream)
+            dcall()
+            b.record(stream)
+        torch.cuda.synchronize()
+        dev_s = statistics.median([a.elapsed_time(b) for a, b in ev]) / 1e3
+        hcall()
+        ht = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            hcall()
+            ht.append(time.perf_counter() - t0)
+        e2e_s = statistics.median(ht)
+        work = dcall(counters=True)
+        r8 = roofline_8d(work, dev_s, 40 * count, peaks)
+        entry = {"config": cfg, "call": w.call, "pairs": count, "n": w.n, "alpha": w.alpha,
+                 "c": w.c, "est": w.est, "device_pairs_per_s": count / dev_s, "device_s": dev_s,
+                 "e2e_pairs_per_s": count / e2e_s, "e2e_s": e2e_s, "launches": eng.last_launches,
+                 "survey_8d": r8,
+                 "fp64_ops_frac": work["fp64_ops"] / peaks["fp64_per_s"] / dev_s,
+                 "work": {k: int(v) for k, v in work.items()}}
+        # extended bound: exact DP candidates at the measured candidate rate
+        # (DMUL + DADD + DSETP each) and the span terms' p*log(p) lookups at the
+        # measured random L2 gather rate
+        if l2_rate and cand_rate:
+            C = r8["C"]
+            terms = {"dp_candidates": C / cand_rate,
+                     "span_lookups_l2": int(work["span_lookups"]) / l2_rate}
+            b = max(terms, key=terms.get)
+            entry["extended_roofline"] = {
+                "t_roof_s": terms[b], "bound": b, "terms_s": terms, "frac": terms[b] / dev_s,
+                "peaks": {"candidates_per_s (probes.cu k_dcand)": cand_rate,
+                          "l2_gathers_per_s (probes.cu k_ldg_rand, 7.2 MB table)": l2_rate},
+                "note": "C = every exact DP candidate (levels 2 .. l_max) at the measured "
+                        "candidate rate; span_lookups = the span terms' p*log(p) lookups (rows "
+                        "m = c_t - c_s scattered over the table) at the measured random L2 "
+                        "gather rate"}
+        got = {k: t.cpu().numpy() for k, t in douts.items()}
+        if cfg == 4:
+            g = np.load(os.path.join(ROOT, "tests", "golden", "ref_c4_full.npz"))
+            n_s = count
+            ok = all(np.array_equal(got[k][:n_s].view(np.int64), g["stats"][:n_s, c].view(np.int64))
+                     for c, k in enumerate(("mic", "mas", "mev", "mcn")))
+            secs = g["cpu_seconds"][:n_s]
+            entry["cpu_reference"] = {
+                "value": n_s / float(secs.sum()), "unit": "pairs/s", "cores": 1,
+                "kind": "reference", "cpu_model": "build container (fixture generation)",
+                "sample": f"the {n_s} fixture pairs (tests/golden/ref_c4_full.npz), reference "
+                          f"compute_score, one thread per pair, {secs.sum():.0f} s CPU total; "
+                          "not re-run here (minutes per pair)"}
+            entry["bit_exact_on_sample"] = bool(ok)
+        elif R is not None and cpu_pairs:
+            n_s = min(cpu_pairs, count)
+            if kind == "pairwise":
+                orc = O.Oracle()
+                idx = np.array([orc.pair_at(V.shape[0], t) for t in range(n_s)], dtype=np.int32)
+                sxi, syi = idx[:, 0], idx[:, 1]
+            else:
+                sxi, syi = xi[:n_s], yi[:n_s]
+            t0 = time.perf_counter()
+            ref = _ref_stats_parallel(R, V, V, sxi, syi, w.alpha, w.c, cores)
+            cdt = time.perf_counter() - t0
+            ok = all(np.array_equal(got[k][:n_s].view(np.int64), ref[:, c].view(np.int64))
+                     for c, k in enumerate(("mic", "mas", "mev", "mcn")))
+            entry["cpu_reference"] = {"value": n_s / cdt, "unit": "pairs/s", "cores": cores,
+                                      "kind": "reference", "cpu_model": cpu_model(),
+                                      "sample": f"the first {n_s} pairs of the window, the "
+                                                f"reference's compute_statistics on {cores} "
+                                                f"threads, {cdt:.1f} s"}
+            entry["bit_exact_on_sample"] = bool(ok)
+        entry["wall_s"] = time.perf_counter() - t_start
+        log(f"secondary c{cfg}: {entry['device_pairs_per_s']:.4g} pairs/s, 8d frac "
+            f"{r8['frac']:.3f}, {entry['wall_s']:.1f} s")
+        res.append(entry)
+    return res
 
 
 def run_config(args):
@@ -430,6 +695,11 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="N > 1: strong = the unchanged c1 sharded over N GPUs; weak = p grows "
+                         "to round(4381 sqrt(N))")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the secondary-config block of the default line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -104,7 +104,8 @@ typedef struct mine_b200_ctx mine_b200_ctx;
 /* Options for batch calls (zero-initialise for defaults). */
 typedef struct mine_b200_opts {
   int device_io;     /* 1: inputs and outputs are device pointers (HBM-resident) */
-  int async;         /* 1 (with device_io): enqueue on `stream` and return */
+  int async;         /* 1 (with device_io): enqueue on `stream` and return;
+                        mine_b200_sync() reports the finite-input check */
   void* stream;      /* cudaStream_t or NULL for the context's stream */
   int tier;          /* 0 auto, 1 tiny (n<=32, B<=7), 2 general, 3 memo (n<=31, B<=7) */
   long long first;   /* first work item (pairwise/cross/list index) */
@@ -114,7 +115,9 @@ typedef struct mine_b200_opts {
    *             (the reference arithmetic's FP64 ops and p*log(p) lookups, DP
    *             candidates, span entries, subproblems; then the 8-byte and
    *             rank (2-byte) table gathers the executing tier needs; then the
-   *             partition's point visits), accumulated by the kernels;
+   *             partition's point visits, then the F(t,2) level's candidates
+   *             and the span terms' p*log(p) lookups),
+   *             accumulated by the kernels;
    *   ev_begin / ev_end: cudaEvent_t recorded on the stream around the
    *             pair-scoring kernels (the dominant kernels of a call). */
   unsigned long long* counters;
@@ -127,7 +130,7 @@ typedef struct mine_b200_opts {
    * masters against one Y).  A call whose variables differ fails. */
   int reuse_vars;
 } mine_b200_opts;
-#define MINE_B200_NCOUNTERS 8
+#define MINE_B200_NCOUNTERS 10
 
 /* ---- engine API ---------------------------------------------------------- */
 const char* mine_b200_last_error(void);
@@ -140,6 +143,13 @@ int mine_b200_grid_bound(long long n, double alpha);
 int mine_b200_cell_count(int bound);
 /* Kernel launches issued by the last batch call on this context. */
 long long mine_b200_last_launches(mine_b200_ctx* ctx);
+/* Waits for the context's last call.  After an async device-io call (which
+ * returns before its finite-input check is read) it reports that check:
+ * -1 with "compute_score: inputs must be finite" as the reference throws
+ * (char_matrix.cpp:74-75).  The result is kept until the next call on the
+ * context.  Calls on one context are ordered among themselves whatever
+ * streams they use. */
+int mine_b200_sync(mine_b200_ctx* ctx);
 
 /* All pairs i < j of p variables (vars: p x n, variable-major), results in
  * condensed PairSequence order (analysis.cpp:66-81, run_analysis

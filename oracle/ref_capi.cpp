@@ -87,6 +87,24 @@ int ref_compute_statistics(int n, const double* x, const double* y, double alpha
   });
 }
 
+// One compute_score, then the reference's own reductions (statistics.cpp:10-37)
+// over that matrix: cells in for_each order plus out4 = mic, mas, mev, mcn.
+// Used for the full-size c4 fixtures, where a second compute_score (as
+// compute_statistics would run) doubles minutes of CPU time per pair.
+int ref_score_statistics(int n, const double* x, const double* y, double alpha, double c,
+                         int* bound, double* cells, double* out4) {
+  return guarded([&] {
+    const CharacteristicMatrix m = compute_score(to_arr(x, n), to_arr(y, n), Parameters{alpha, c});
+    *bound = m.bound();
+    long i = 0;
+    m.for_each([&](int, int, double v) { cells[i++] = v; });
+    out4[0] = mic(m);
+    out4[1] = mas(m);
+    out4[2] = mev(m);
+    out4[3] = mcn(m);
+  });
+}
+
 // Cache-free recount path (oracle.cpp:145-164), guarded to n <= 200.
 int ref_reference_statistics(int n, const double* x, const double* y, double alpha, double c,
                              double* out6) {

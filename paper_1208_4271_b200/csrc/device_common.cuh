@@ -129,6 +129,8 @@ __device__ inline void subproblem_work(int R, int k, int x_max, int n, unsigned 
   w[kCntLookups] += f2 * (2 * R + 2) + spans * R;
   if (gathers_as_reference) w[kCntGathers] += f2 * (2 * R + 2) + spans * R;
   w[kCntCand] += cand;
+  w[kCntF2] += f2;
+  w[kCntSpanLookups] += spans * R;
   w[kCntSpans] += spans;
   w[kCntSub] += 1;
 }

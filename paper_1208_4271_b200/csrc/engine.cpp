@@ -208,6 +208,15 @@ struct mine_b200_ctx {
   } prep;
   std::vector<cudaEvent_t> events;
   long long launches = 0;
+  int sms = 148;
+  // Ordering across calls: every call records `last_done` on its stream when
+  // its last kernel / copy is enqueued, and the next call (whatever stream it
+  // uses) waits on it before touching context-owned buffers.  An async
+  // device-io call returns before its finite-input check is read; that
+  // result is reported by mine_b200_sync().
+  cudaEvent_t last_done = nullptr;
+  bool last_recorded = false;
+  bool async_pending = false;
 };
 
 namespace {
@@ -229,6 +238,17 @@ void validate_param(const mine_parameter* par) {  // char_matrix.cpp:11-15
   if (!(par->c > 0.0)) throw Failure("parameters: c must be > 0");
   if (par->est != MINE_EST_MIC_APPROX && par->est != MINE_EST_MIC_E)
     throw Failure("parameters: est must be MINE_EST_MIC_APPROX or MINE_EST_MIC_E");
+}
+
+// Every call waits for the previous call's work on this context (its stream
+// may differ) before reusing the context's device buffers.
+void order_after_last_call(mine_b200_ctx* ctx, cudaStream_t s) {
+  if (ctx->last_recorded) CK(cudaStreamWaitEvent(s, ctx->last_done, 0));
+}
+
+void mark_call_done(mine_b200_ctx* ctx, cudaStream_t s) {
+  CK(cudaEventRecord(ctx->last_done, s));
+  ctx->last_recorded = true;
 }
 
 cudaEvent_t ctx_event(mine_b200_ctx* ctx, size_t i) {
@@ -314,6 +334,8 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
 
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = opts.stream ? static_cast<cudaStream_t>(opts.stream) : ctx->stream;
+  order_after_last_call(ctx, s);
+  ctx->async_pending = false;  // an unsynced async call's check result expires here
   const bool dio = opts.device_io != 0;
   const int B = grid_bound(n, par->alpha);
   const int ny = B / 2 - 1;
@@ -470,7 +492,9 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
     }
     per_pair += 2 * sub_max * std::min<size_t>(mine_b200_ctx::kYLanes, yps.size());
   }
-  const long long chunk = small ? (dio ? count : std::min<long long>(count, 1LL << 20))
+  // host io streams the small tiers in chunks of one 8192-pair sort batch
+  // per SM (the memo kernel deals whole batches), so no SM idles per chunk
+  const long long chunk = small ? (dio ? count : std::min<long long>(count, 8192LL * ctx->sms))
                                : std::max<long long>(1, std::min<long long>(
                                      count, (long long)((4096ULL << 20) / per_pair)));
   const long long nchunks = (count + chunk - 1) / chunk;
@@ -584,7 +608,11 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
     }
   }
   if (opts.ev_end) CK(cudaEventRecord(static_cast<cudaEvent_t>(opts.ev_end), s));
+  if (!dio) CK(cudaStreamWaitEvent(s, ctx_event(ctx, 2 * ((nchunks - 1) % nslots) + 1), 0));
+  CK(cudaEventRecord(ctx->last_done, s));
+  ctx->last_recorded = true;
   if (dio && opts.async && !opts.counters) {
+    ctx->async_pending = true;
     done.commit(P);
     return;
   }
@@ -638,6 +666,21 @@ int mine_b200_grid_bound(long long n, double alpha) { return grid_bound(n, alpha
 int mine_b200_cell_count(int bound) { return cell_count(bound); }
 long long mine_b200_last_launches(mine_b200_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int mine_b200_sync(mine_b200_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) throw Failure("mine_b200: null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->last_recorded) CK(cudaEventSynchronize(ctx->last_done));
+    if (ctx->async_pending) {
+      ctx->async_pending = false;
+      int h_flag = 0;
+      CK(cudaMemcpy(&h_flag, ctx->flag.as<int>(), sizeof(int), cudaMemcpyDeviceToHost));
+      if (h_flag) throw Failure("compute_score: inputs must be finite");
+    }
+  });
+}
+
 mine_b200_ctx* mine_b200_create(int device) {
   mine_b200_ctx* ctx = nullptr;
   const int rc = guarded([&] {
@@ -662,6 +705,8 @@ mine_b200_ctx* mine_b200_create(int device) {
     c->device = device;
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->last_done, cudaEventDisableTiming));
+    c->sms = prop.multiProcessorCount;
     ctx = c.release();
   });
   return rc ? nullptr : ctx;
@@ -673,6 +718,10 @@ void mine_b200_destroy(mine_b200_ctx* ctx) {
   for (auto e : ctx->events) cudaEventDestroy(e);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->copy) cudaStreamDestroy(ctx->copy);
+  if (ctx->last_done) {
+    cudaEventSynchronize(ctx->last_done);
+    cudaEventDestroy(ctx->last_done);
+  }
   for (auto& ln : ctx->ylane) {
     if (ln.s) cudaStreamDestroy(ln.s);
     if (ln.done) cudaEventDestroy(ln.done);
@@ -725,6 +774,7 @@ int mine_b200_variances(mine_b200_ctx* ctx, const double* vars, int p, int n, do
     std::lock_guard<std::mutex> lk(ctx->mu);
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
+    order_after_last_call(ctx, s);
     ctx->prep.valid = false;  // the variable buffers are reused below
     VarSet vs;
     vs.V = p;
@@ -739,6 +789,7 @@ int mine_b200_variances(mine_b200_ctx* ctx, const double* vars, int p, int n, do
     launch_variances(vs, var, s);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(var_out, var, sizeof(double) * (size_t)p, cudaMemcpyDeviceToHost, s));
+    mark_call_done(ctx, s);
     CK(cudaStreamSynchronize(s));
   });
 }
@@ -756,6 +807,10 @@ int mine_b200_debug_subproblem(mine_b200_ctx* ctx, int n, const double* col_var,
     std::lock_guard<std::mutex> lk(ctx->mu);
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
+    order_after_last_call(ctx, s);
+    // the per-variable buffers (vals, perm, runid, q, yhat, hq, ...) are
+    // overwritten below: a following reuse_vars call must not trust them
+    ctx->prep.valid = false;
     const int B = x_max * y_target;  // admits (x_max, y_target) and rows up to y_target
     ctx->tables.build(n, B, s);
     const Tables tb = ctx->tables.view();
@@ -810,6 +865,7 @@ int mine_b200_debug_subproblem(mine_b200_ctx* ctx, int n, const double* col_var,
     CK(cudaGetLastError());
     std::vector<char> h(bytes);
     CK(cudaMemcpyAsync(h.data(), dd, bytes, cudaMemcpyDeviceToHost, s));
+    mark_call_done(ctx, s);
     CK(cudaStreamSynchronize(s));
     const double* hd = reinterpret_cast<const double*>(h.data());
     const int* hi = reinterpret_cast<const int*>(hd + 1 + x_max);

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -1409,8 +1410,10 @@ static size_t memo_smem_fixed(int n, int nval) {
 }
 
 bool memo_fits(int n, int B, int nval) {
-  // tables + val[] + at least 8 warps of scratch rows in 226 KB
-  return n >= 2 && n <= 32 && B <= 7 &&
+  // tables + val[] + at least 8 warps of scratch rows in 226 KB.  n <= 31:
+  // the register-staged y = 2 level loop holds k - 1 <= n - 1 split points in
+  // memo_reg_slots(n) <= 30 registers (memo_y2), so n = 32 is never admitted.
+  return n >= 2 && n <= 31 && B <= 7 &&
          memo_smem_fixed(n, nval) + sizeof(int) * (size_t)memo_scr_stride(n) * 256 <= 226 * 1024;
 }
 
@@ -1448,8 +1451,6 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long need = (ps.count + threads - 1) / threads;
-  const unsigned blocks = (unsigned)std::min<long long>(sms, need);
   const MemoLayout L = memo_layout(vs.n);
 #define MEMO_LAUNCH(CNT, T3C, RS, SORT)                                                        \
   k_memo_pairs<CNT, T3C, RS, SORT><<<blocks, threads, sm + (SORT ? memo_sort_bytes(SORT) : 0), s>>>( \
@@ -1462,6 +1463,14 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
   if (regs && memo_sort() && threads == kMemoMaxThreads && vs.V < 65536 && tb.B >= 6)
     for (int b = 8192; b >= 4096 && !sbatch; b /= 2)
       if (sm + memo_sort_bytes(b) <= 226 * 1024) sbatch = b;
+  // work is dealt per sort batch when sorting (per thread otherwise): no CTA
+  // is launched that would only stage the tables and exit
+  const long long need = sbatch ? (ps.count + sbatch - 1) / sbatch : (ps.count + threads - 1) / threads;
+  const unsigned blocks = (unsigned)std::min<long long>(sms, need);
+  if (regs && regs < vs.n - 1) {  // memo_y2's register slots must hold k - 1 <= n - 1 split points
+    std::fprintf(stderr, "mine_b200: memo register slots %d < n - 1 = %d\n", regs, vs.n - 1);
+    std::abort();
+  }
 #define MEMO_LAUNCH_N(CNT, N)                                                              \
   k_memo_pairs<CNT, false, 23, 8192, N><<<blocks, threads, sm + memo_sort_bytes(8192), s>>>(   \
       vs, tb, memo, memo_val, nval, L, ps, c, est, out, o_cells, CNT ? counters : nullptr)

@@ -80,7 +80,11 @@ struct StatsOut {
 // Realised-work counters: algorithmic FP64 ops of the
 // reference arithmetic, p*log(p) lookups, DP candidates, span entries,
 // subproblems.
-enum { kCntFp64 = 0, kCntLookups, kCntCand, kCntSpans, kCntSub, kCntGathers, kCntRankGathers, kCntPoints, kNumCounters };
+enum { kCntFp64 = 0, kCntLookups, kCntCand, kCntSpans, kCntSub, kCntGathers, kCntRankGathers, kCntPoints, kCntF2, kCntSpanLookups, kNumCounters };
+// kCntSpanLookups: the span terms' p*log(p) lookups (spans x rows), random
+// rows m = c_t - c_s of the table.
+// kCntF2: candidates of the first DP level F(t,2) (mutual_info.cpp:47-56); with
+// kCntCand they make SURVEY 8d's C = sum over l = 2 .. l_max.
 // kCntGathers / kCntRankGathers: 8-byte / narrow (rank) shared-memory table
 // gathers the executing tier actually needs (memo tier: one 2-byte rank per F(t,2)
 // candidate, ...); the other counters describe the reference's own

@@ -85,6 +85,50 @@ __global__ void k_check_quot(int nmax, unsigned long long* out) {
   atomicAdd(out + 1, cnt);
 }
 
+// Random 8-byte gathers from a global table of `entries` doubles (L2-resident
+// up to ~100 MB): the span-term lookups of the general tier's p*log(p) table
+// (rows m = c_t - c_s scattered across the table).  8 independent streams per
+// thread, so each warp keeps 8 gathers in flight.
+__global__ void k_ldg_rand(const double* __restrict__ tab, unsigned entries, double* out, int iters) {
+  uint32_t st[kChains];
+  double acc[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c)
+    st[c] = 2654435761u * (blockIdx.x * blockDim.x + threadIdx.x + 1) + 40503u * c, acc[c] = 0.0;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+      st[c] = st[c] * 1664525u + 1013904223u;
+      acc[c] += __ldg(tab + (st[c] >> 4) % entries);
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) s += acc[c];
+  if (s == 12345.678) out[0] = s;
+}
+
+// The exact DP candidate (mutual_info.cpp:62-63 as the engine issues it:
+// DMUL, DADD, then libstdc++'s max = DSETP + two selects), 8 independent max
+// chains per thread: the FP64 pipe's candidate rate.
+__global__ void k_dcand(double* out, int iters, double a, double w) {
+  double f[kChains], m[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) f[c] = -(threadIdx.x * 1e-3 + c), m[c] = -1e300;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+      const double v = __dsub_rn(__dmul_rn(a, f[c]), w);
+      m[c] = m[c] < v ? v : m[c];
+      f[c] = __dadd_rn(f[c], w);  // keeps the operands live (not counted as a candidate op)
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) s += m[c];
+  if (s == 12345.678) out[0] = s;
+}
+
 template <typename F>
 float time_ms(F&& launch) {
   cudaEvent_t a, b;
@@ -137,5 +181,31 @@ extern "C" int mine_b200_check_quotients(int device, int nmax, unsigned long lon
   cudaFree(d);
   *mismatches = h[0];
   *checked = h[1];
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+// Extra roofline denominators for the general tier: random 8-byte L2 gathers
+// per second from a `table_bytes` table, and exact DP candidates per second
+// (k_dcand counts DMUL + DADD + DSETP per candidate; its keep-alive DADD is
+// issued too, so this is a lower bound on the pipe's candidate rate).
+extern "C" int mine_b200_probe_general(int device, double table_bytes, double* l2_gathers_per_s,
+                                       double* candidates_per_s) {
+  if (cudaSetDevice(device) != cudaSuccess) return -1;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const unsigned entries = (unsigned)(table_bytes / 8);
+  double* tab = nullptr;
+  double* out = nullptr;
+  if (cudaMalloc(&tab, sizeof(double) * (size_t)entries) != cudaSuccess) return -1;
+  if (cudaMalloc(&out, sizeof(double)) != cudaSuccess) return -1;
+  cudaMemset(tab, 0, sizeof(double) * (size_t)entries);
+  const int blocks = sms * 8, threads = 256, iters = 512;
+  float ms = time_ms([&] { k_ldg_rand<<<blocks, threads>>>(tab, entries, out, iters); });
+  *l2_gathers_per_s = (double)blocks * threads * iters * kChains / (ms * 1e-3);
+  const int citers = 2048;
+  ms = time_ms([&] { k_dcand<<<blocks, threads>>>(out, citers, 0.75, 1e-9); });
+  *candidates_per_s = (double)blocks * threads * citers * kChains / (ms * 1e-3);
+  cudaFree(tab);
+  cudaFree(out);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }

@@ -42,9 +42,9 @@ class MineStatsOut(ctypes.Structure):
     _fields_ = [(k, _dp) for k in STATS] + [("cells", _dp)] + [(k, _dp) for k in EXTRA_STATS]
 
 
-NCOUNTERS = 8
+NCOUNTERS = 10
 COUNTERS = ("fp64_ops", "lookups", "dp_candidates", "span_entries", "subproblems", "gathers",
-            "rank_gathers", "point_visits")
+            "rank_gathers", "point_visits", "f2_candidates", "span_lookups")
 
 
 class MineOpts(ctypes.Structure):
@@ -71,6 +71,21 @@ MODES = {"all_pairs": 0, "master_vs_all": 1, "single_pair": 2}
 
 class MineProblem(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int), ("x", _dp), ("y", _dp)]
+
+
+class MineMatrix(ctypes.Structure):
+    """mine_matrix: n variables x m samples, variable-major."""
+    _fields_ = [("data", ctypes.POINTER(ctypes.c_double)), ("n", ctypes.c_int), ("m", ctypes.c_int)]
+
+
+class MinePstats(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_longlong), ("mic", ctypes.POINTER(ctypes.c_double)),
+                ("tic", ctypes.POINTER(ctypes.c_double))]
+
+
+class MineCstats(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_longlong), ("m", ctypes.c_longlong),
+                ("mic", ctypes.POINTER(ctypes.c_double)), ("tic", ctypes.POINTER(ctypes.c_double))]
 
 
 class MineScore(ctypes.Structure):
@@ -100,6 +115,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.mine_b200_cell_count.argtypes = [ctypes.c_int]
     L.mine_b200_last_launches.argtypes = [vp]
     L.mine_b200_last_launches.restype = ctypes.c_longlong
+    L.mine_b200_sync.argtypes = [vp]
     P = ctypes.POINTER
     L.mine_b200_pairwise.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, P(MineParameter),
                                      P(MineOpts), P(MineStatsOut)]
@@ -115,6 +131,14 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.mine_compute_score.restype = P(MineScore)
     L.mine_free_score.argtypes = [P(P(MineScore))]
     L.mine_free_score.restype = None
+    L.mine_compute_pstats.argtypes = [P(MineMatrix), P(MineParameter)]
+    L.mine_compute_pstats.restype = P(MinePstats)
+    L.mine_compute_cstats.argtypes = [P(MineMatrix), P(MineMatrix), P(MineParameter)]
+    L.mine_compute_cstats.restype = P(MineCstats)
+    L.mine_free_pstats.argtypes = [P(P(MinePstats))]
+    L.mine_free_pstats.restype = None
+    L.mine_free_cstats.argtypes = [P(P(MineCstats))]
+    L.mine_free_cstats.restype = None
     for f in ("mine_mic", "mine_mas", "mine_mev", "mine_mcn_general", "mine_mic_e"):
         getattr(L, f).argtypes = [P(MineScore)]
         getattr(L, f).restype = ctypes.c_double
@@ -282,6 +306,11 @@ class Engine:
         if rc != 0:
             raise MineError(self.L.mine_b200_last_error().decode())
 
+    def sync(self) -> None:
+        """Waits for the last call; raises if an async device-io call's
+        inputs were not finite (mine_b200_sync)."""
+        self._check(self.L.mine_b200_sync(self.ctx))
+
     @property
     def last_launches(self) -> int:
         return int(self.L.mine_b200_last_launches(self.ctx))
@@ -301,6 +330,17 @@ class Engine:
             res["cells"] = np.empty((count, 2, nc))
             so.cells = res["cells"].ctypes.data_as(_dp)
         return res, so
+
+    @staticmethod
+    def _count(total: int, first: int, count: int | None) -> int:
+        """Items of [first, first + count) to score; an explicit 0 is an
+        empty range (never passed to the C ABI, where count <= 0 means all)."""
+        if not 0 <= first <= total:
+            raise MineError("expand_pairs: first index out of range")
+        count = total - first if count is None else int(count)
+        if count < 0 or first + count > total:
+            raise MineError("expand_pairs: pair range out of range")
+        return count
 
     def _opts(self, first=0, count=0, tier=0, reuse_vars=False) -> MineOpts:
         o = MineOpts()
@@ -326,8 +366,10 @@ class Engine:
         v = _f64(vars_)
         p, n = v.shape
         total = p * (p - 1) // 2
-        count = total - first if count is None else count
+        count = self._count(total, first, count)
         res, so = self._outputs(count, stats, cells, grid_bound(n, params.alpha))
+        if count == 0:  # the C ABI reads count <= 0 as "all from first"
+            return res
         self._check(self.L.mine_b200_pairwise(self.ctx, _ptr(v), p, n, ctypes.byref(params._c()),
                                               ctypes.byref(self._opts(first, count, tier, reuse_vars)),
                                               ctypes.byref(so)))
@@ -339,8 +381,10 @@ class Engine:
         if X.shape[1] != Y.shape[1]:
             raise MineError("compute_score: input lengths differ")
         total = X.shape[0] * Y.shape[0]
-        count = total - first if count is None else count
+        count = self._count(total, first, count)
         res, so = self._outputs(count, stats, cells, grid_bound(X.shape[1], params.alpha))
+        if count == 0:
+            return res
         self._check(self.L.mine_b200_cross(self.ctx, _ptr(X), X.shape[0], _ptr(Y), Y.shape[0],
                                            X.shape[1], ctypes.byref(params._c()),
                                            ctypes.byref(self._opts(first, count, tier, reuse_vars)),
@@ -352,7 +396,11 @@ class Engine:
         v = _f64(vars_)
         xi = np.ascontiguousarray(xi, dtype=np.int32)
         yi = np.ascontiguousarray(yi, dtype=np.int32)
+        if xi.shape != yi.shape:
+            raise MineError("expand_pairs: index arrays differ in length")
         res, so = self._outputs(xi.size, stats, cells, grid_bound(v.shape[1], params.alpha))
+        if xi.size == 0:
+            return res
         self._check(self.L.mine_b200_pairs(self.ctx, _ptr(v), v.shape[0], v.shape[1], _ptr(xi),
                                            _ptr(yi), xi.size, ctypes.byref(params._c()),
                                            ctypes.byref(self._opts(0, xi.size, tier, reuse_vars)),
@@ -439,6 +487,42 @@ class Engine:
         self._check(self.L.mine_b200_pairwise(self.ctx, ctypes.c_void_p(vars_ptr), p, n,
                                               ctypes.byref(params._c()), ctypes.byref(o),
                                               ctypes.byref(so)))
+        return dict(zip(COUNTERS, list(cnt))) if counters else None
+
+    def device_call(self, kind: str, params: Parameters, out_ptrs: dict, *, vars_ptr: int = 0,
+                    p: int = 0, n: int = 0, y_ptr: int = 0, py: int = 0, xi_ptr: int = 0,
+                    yi_ptr: int = 0, npairs: int = 0, stream: int = 0, first: int = 0,
+                    count: int = 0, counters: bool = False, ev_begin: int = 0, ev_end: int = 0,
+                    reuse_vars: bool = False):
+        """Any batch call with device-resident inputs / outputs (data_ptr()s):
+        kind = "pairwise" (vars p x n), "cross" (X = vars p x n, Y = y_ptr
+        py x n) or "pairs" (vars p x n, device index arrays xi / yi of
+        npairs).  Synchronous; counters=True returns the realised work."""
+        so = MineStatsOut()
+        for k in ALL_STATS:
+            setattr(so, k, ctypes.cast(ctypes.c_void_p(out_ptrs[k]), _dp) if out_ptrs.get(k) else None)
+        o = MineOpts()
+        o.first, o.count, o.tier = int(first), int(count), 0
+        o.device_io, o.async_, o.stream = 1, 0, ctypes.c_void_p(stream or None)
+        o.reuse_vars = int(bool(reuse_vars))
+        cnt = (ctypes.c_ulonglong * NCOUNTERS)()
+        if counters:
+            o.counters = cnt
+        o.ev_begin, o.ev_end = ctypes.c_void_p(ev_begin or None), ctypes.c_void_p(ev_end or None)
+        par = ctypes.byref(params._c())
+        vp = ctypes.c_void_p
+        if kind == "pairwise":
+            rc = self.L.mine_b200_pairwise(self.ctx, vp(vars_ptr), p, n, par, ctypes.byref(o),
+                                           ctypes.byref(so))
+        elif kind == "cross":
+            rc = self.L.mine_b200_cross(self.ctx, vp(vars_ptr), p, vp(y_ptr), py, n, par,
+                                        ctypes.byref(o), ctypes.byref(so))
+        elif kind == "pairs":
+            rc = self.L.mine_b200_pairs(self.ctx, vp(vars_ptr), p, n, vp(xi_ptr), vp(yi_ptr), npairs,
+                                        par, ctypes.byref(o), ctypes.byref(so))
+        else:
+            raise ValueError(kind)
+        self._check(rc)
         return dict(zip(COUNTERS, list(cnt))) if counters else None
 
     def pairwise_host(self, vars_np: np.ndarray, params: Parameters, outs: dict, first: int = 0,
