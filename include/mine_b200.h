@@ -129,6 +129,18 @@ typedef struct mine_b200_opts {
    * e.g. successive windows of one pairwise job, or master_vs_all over many
    * masters against one Y).  A call whose variables differ fails. */
   int reuse_vars;
+  /* Multi-GPU (the GPU analogue of run_analysis's worker pool,
+   * analysis.cpp:148-190).  ndevices > 1 spreads the call's items over the
+   * listed CUDA devices -- an entry may repeat (virtual shards of one GPU) --
+   * with one host thread and one engine context (owned by this context) per
+   * entry.  The threads claim chunks of `shard_chunk` items (0: automatic,
+   * about 16 chunks per entry) from a shared cursor, so expensive and cheap
+   * pairs balance dynamically, and each chunk's results land at its offset of
+   * the caller's buffers.  Host buffers only (device_io = 0; counters and
+   * events are not available).  Results are bit-identical for any list. */
+  int ndevices;
+  const int* devices;
+  long long shard_chunk;
 } mine_b200_opts;
 #define MINE_B200_NCOUNTERS 10
 

@@ -6,7 +6,9 @@
 // Compiled with -ffp-contract=off: the p*log(p) table must round exactly like
 // the reference's `acc += p * std::log(p)` (mutual_info.hpp:24-27).
 #include <algorithm>
+#include <atomic>
 #include <climits>
+#include <exception>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -217,6 +219,10 @@ struct mine_b200_ctx {
   cudaEvent_t last_done = nullptr;
   bool last_recorded = false;
   bool async_pending = false;
+  // multi-device calls (opts.ndevices > 1): one engine context per device
+  // list entry, created on first use and kept (their tables / buffers are
+  // reused by the next sharded call)
+  std::vector<mine_b200_ctx*> shards;
 };
 
 namespace {
@@ -637,6 +643,92 @@ int guarded(F&& f) {
   }
 }
 
+// Multi-device call (opts.ndevices > 1): the GPU analogue of run_analysis's
+// worker pool (analysis.cpp:148-190).  One host thread per device-list entry
+// drives that entry's engine context; threads claim chunks of items from one
+// atomic cursor and score them with run_call (host io), each chunk's results
+// written at its offset of the caller's buffers.  A thread's first chunk
+// prepares its context's per-variable state, later chunks reuse it.  The first
+// failure is rethrown after every thread has joined, like the reference.
+void run_sharded(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
+                 const mine_b200_opts& opts, mine_stats_out* out) {
+  if (opts.device_io) throw Failure("mine_b200: multi-device calls take host buffers (device_io = 0)");
+  if (opts.counters || opts.ev_begin || opts.ev_end || opts.reuse_vars)
+    throw Failure("mine_b200: counters / events / reuse_vars are single-device options");
+  if (!opts.devices) throw Failure("mine_b200: ndevices > 1 needs a device list");
+  validate_param(par);
+  if (call.n < 2) throw Failure("compute_score: need at least 2 samples");
+  if (!out) throw Failure("mine_b200: null output");
+  const long long first = opts.first;
+  if (first < 0 || first > call.total) throw Failure("expand_pairs: first index out of range");
+  const long long count = opts.count > 0 ? opts.count : call.total - first;
+  if (first + count > call.total) throw Failure("expand_pairs: pair range out of range");
+  const int G = opts.ndevices;
+  while ((int)ctx->shards.size() < G) ctx->shards.push_back(nullptr);
+  for (int g = 0; g < G; ++g) {
+    mine_b200_ctx*& sc = ctx->shards[g];
+    if (sc && sc->device != opts.devices[g]) {
+      mine_b200_destroy(sc);
+      sc = nullptr;
+    }
+    if (!sc) {
+      sc = mine_b200_create(opts.devices[g]);
+      if (!sc) throw Failure(g_err);
+    }
+  }
+  ctx->launches = 0;
+  if (count == 0) return;
+  const long long chunk = opts.shard_chunk > 0 ? opts.shard_chunk
+                                               : std::max<long long>(1, (count + 16LL * G - 1) / (16LL * G));
+  const int ncell = cell_count(grid_bound(call.n, par->alpha));
+  std::atomic<long long> cursor{0};
+  std::atomic<long long> launches{0};
+  std::exception_ptr failure;
+  std::mutex failure_mu;
+  auto worker = [&](int g) {
+    try {
+      mine_b200_ctx* sc = ctx->shards[g];
+      std::lock_guard<std::mutex> lk(sc->mu);
+      bool prepared = false;
+      for (;;) {
+        const long long c0 = cursor.fetch_add(chunk);
+        if (c0 >= count) break;
+        const long long cn = std::min(chunk, count - c0);
+        mine_b200_opts o{};
+        o.first = first + c0;
+        o.count = cn;
+        o.tier = opts.tier;
+        o.reuse_vars = prepared;
+        mine_stats_out so = *out;
+        double** f[] = {&so.mic, &so.mas, &so.mev, &so.mcn, &so.mic_e, &so.tic, &so.pearson_r,
+                        &so.nonlinearity};
+        for (double** q : f)
+          if (*q) *q += c0;
+        if (so.cells) so.cells += (size_t)c0 * 2 * ncell;
+        run_call(sc, call, par, &o, &so);
+        launches += sc->launches;
+        prepared = true;
+      }
+    } catch (const std::exception& e) {
+      std::lock_guard<std::mutex> lk(failure_mu);
+      if (!failure) failure = std::make_exception_ptr(Failure(e.what()));
+    }
+  };
+  std::vector<std::thread> th;
+  for (int g = 0; g < G; ++g) th.emplace_back(worker, g);
+  for (auto& t : th) t.join();
+  ctx->launches = launches;
+  if (failure) std::rethrow_exception(failure);
+}
+
+void dispatch(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
+              const mine_b200_opts* opts, mine_stats_out* out) {
+  if (opts && opts->ndevices > 1)
+    run_sharded(ctx, call, par, *opts, out);
+  else
+    run_call(ctx, call, par, opts, out);
+}
+
 mine_b200_ctx* default_ctx() {
   thread_local std::unique_ptr<mine_b200_ctx, void (*)(mine_b200_ctx*)> ctx(nullptr, mine_b200_destroy);
   if (!ctx) {
@@ -714,6 +806,7 @@ mine_b200_ctx* mine_b200_create(int device) {
 
 void mine_b200_destroy(mine_b200_ctx* ctx) {
   if (!ctx) return;
+  for (auto* sc : ctx->shards) mine_b200_destroy(sc);
   cudaSetDevice(ctx->device);
   for (auto e : ctx->events) cudaEventDestroy(e);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -738,7 +831,7 @@ int mine_b200_pairwise(mine_b200_ctx* ctx, const double* vars, int p, int n,
     std::lock_guard<std::mutex> lk(ctx->mu);
     Call call{kPairwise, vars, nullptr, p, 0, n, nullptr, nullptr, (long long)p * (p - 1) / 2};
     if (p < 2) call.total = 0;
-    run_call(ctx, call, param, opts, out);
+    dispatch(ctx, call, param, opts, out);
   });
 }
 
@@ -750,7 +843,7 @@ int mine_b200_cross(mine_b200_ctx* ctx, const double* X, int px, const double* Y
     if (px < 0 || py < 0) throw Failure("mine_b200: negative variable count");
     std::lock_guard<std::mutex> lk(ctx->mu);
     Call call{kCross, X, Y, px, py, n, nullptr, nullptr, (long long)px * py};
-    run_call(ctx, call, param, opts, out);
+    dispatch(ctx, call, param, opts, out);
   });
 }
 
@@ -762,7 +855,7 @@ int mine_b200_pairs(mine_b200_ctx* ctx, const double* vars, int nvars, int n, co
     if (npairs < 0 || nvars < 0) throw Failure("mine_b200: negative size");
     std::lock_guard<std::mutex> lk(ctx->mu);
     Call call{kList, vars, nullptr, nvars, 0, n, xi, yi, npairs};
-    run_call(ctx, call, param, opts, out);
+    dispatch(ctx, call, param, opts, out);
   });
 }
 

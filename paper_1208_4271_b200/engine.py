@@ -51,7 +51,9 @@ class MineOpts(ctypes.Structure):
     _fields_ = [("device_io", ctypes.c_int), ("async_", ctypes.c_int), ("stream", ctypes.c_void_p),
                 ("tier", ctypes.c_int), ("first", ctypes.c_longlong), ("count", ctypes.c_longlong),
                 ("counters", ctypes.POINTER(ctypes.c_ulonglong)), ("ev_begin", ctypes.c_void_p),
-                ("ev_end", ctypes.c_void_p), ("reuse_vars", ctypes.c_int)]
+                ("ev_end", ctypes.c_void_p), ("reuse_vars", ctypes.c_int),
+                ("ndevices", ctypes.c_int), ("devices", ctypes.POINTER(ctypes.c_int)),
+                ("shard_chunk", ctypes.c_longlong)]
 
 
 class MineDataset(ctypes.Structure):
@@ -342,10 +344,14 @@ class Engine:
             raise MineError("expand_pairs: pair range out of range")
         return count
 
-    def _opts(self, first=0, count=0, tier=0, reuse_vars=False) -> MineOpts:
+    def _opts(self, first=0, count=0, tier=0, reuse_vars=False, devices=None,
+              shard_chunk=0) -> MineOpts:
         o = MineOpts()
         o.first, o.count, o.tier = int(first), int(count), int(tier)
         o.reuse_vars = int(bool(reuse_vars))
+        if devices is not None and len(devices) > 0:
+            self._devs = (ctypes.c_int * len(devices))(*[int(d) for d in devices])
+            o.ndevices, o.devices, o.shard_chunk = len(devices), self._devs, int(shard_chunk)
         if self.count_work:
             self._cnt = (ctypes.c_ulonglong * NCOUNTERS)()
             o.counters = self._cnt
@@ -359,10 +365,13 @@ class Engine:
 
     # -- batch calls ----------------------------------------------------------
     def pairwise(self, vars_, params: Parameters = Parameters(), first: int = 0, count: int | None = None,
-                 stats=STATS, cells: bool = False, tier: int = 0, reuse_vars: bool = False):
+                 stats=STATS, cells: bool = False, tier: int = 0, reuse_vars: bool = False,
+                 devices=None, shard_chunk: int = 0):
         """All pairs i<j in PairSequence order (analysis.cpp:66-81).
         reuse_vars: `vars_` is the same array as in the previous call (e.g. the
-        next window of one job): skip the per-variable stages."""
+        next window of one job): skip the per-variable stages.
+        devices: a list of CUDA devices (repeats allowed) to spread the call
+        over (mine_b200_opts.ndevices / devices / shard_chunk)."""
         v = _f64(vars_)
         p, n = v.shape
         total = p * (p - 1) // 2
@@ -371,12 +380,14 @@ class Engine:
         if count == 0:  # the C ABI reads count <= 0 as "all from first"
             return res
         self._check(self.L.mine_b200_pairwise(self.ctx, _ptr(v), p, n, ctypes.byref(params._c()),
-                                              ctypes.byref(self._opts(first, count, tier, reuse_vars)),
+                                              ctypes.byref(self._opts(first, count, tier, reuse_vars,
+                                                                      devices, shard_chunk)),
                                               ctypes.byref(so)))
         return res
 
     def cross(self, X, Y, params: Parameters = Parameters(), stats=STATS, cells: bool = False,
-              tier: int = 0, first: int = 0, count: int | None = None, reuse_vars: bool = False):
+              tier: int = 0, first: int = 0, count: int | None = None, reuse_vars: bool = False,
+              devices=None, shard_chunk: int = 0):
         X, Y = _f64(X), _f64(Y)
         if X.shape[1] != Y.shape[1]:
             raise MineError("compute_score: input lengths differ")
@@ -387,12 +398,14 @@ class Engine:
             return res
         self._check(self.L.mine_b200_cross(self.ctx, _ptr(X), X.shape[0], _ptr(Y), Y.shape[0],
                                            X.shape[1], ctypes.byref(params._c()),
-                                           ctypes.byref(self._opts(first, count, tier, reuse_vars)),
+                                           ctypes.byref(self._opts(first, count, tier, reuse_vars,
+                                                                   devices, shard_chunk)),
                                            ctypes.byref(so)))
         return res
 
     def pairs(self, vars_, xi, yi, params: Parameters = Parameters(), stats=STATS,
-              cells: bool = False, tier: int = 0, reuse_vars: bool = False):
+              cells: bool = False, tier: int = 0, reuse_vars: bool = False, devices=None,
+              shard_chunk: int = 0):
         v = _f64(vars_)
         xi = np.ascontiguousarray(xi, dtype=np.int32)
         yi = np.ascontiguousarray(yi, dtype=np.int32)
@@ -403,7 +416,8 @@ class Engine:
             return res
         self._check(self.L.mine_b200_pairs(self.ctx, _ptr(v), v.shape[0], v.shape[1], _ptr(xi),
                                            _ptr(yi), xi.size, ctypes.byref(params._c()),
-                                           ctypes.byref(self._opts(0, xi.size, tier, reuse_vars)),
+                                           ctypes.byref(self._opts(0, xi.size, tier, reuse_vars,
+                                                                   devices, shard_chunk)),
                                            ctypes.byref(so)))
         return res
 

@@ -125,3 +125,41 @@ def test_async_calls_are_ordered_and_checked(engine, oracle):
     with pytest.raises(MineError, match="finite"):
         engine.sync()
     engine.sync()  # reported once
+
+
+@pytest.mark.parametrize("devices,chunk", [([0, 0], 0), ([0, 0, 0, 0], 7), ([0, 0, 0], 1000)])
+def test_virtual_shards_bit_identical(engine, devices, chunk):
+    """mine_b200_opts.ndevices / devices: G virtual shards of one GPU (one
+    host thread + engine context each, chunks from a shared cursor) give the
+    single-shard bits for every tier and pair kind -- the multi-GPU contract
+    (SURVEY 8e), checked on one device."""
+    stats = ("mic", "mas", "mev", "mcn", "mic_e", "tic", "pearson_r", "nonlinearity")
+    w1 = datagen.make(1)
+    V1 = np.ascontiguousarray(w1.X[:300])           # memo tier
+    a = engine.pairwise(V1, stats=stats)
+    b = engine.pairwise(V1, stats=stats, devices=devices, shard_chunk=chunk)
+    for k in stats:
+        assert np.array_equal(bits(a[k]), bits(b[k])), k
+    w0 = datagen.make(0, npairs=24)                  # general tier, explicit pairs
+    p0 = Parameters(w0.alpha, w0.c, w0.est)
+    a = engine.pairs(w0.X, w0.xi, w0.yi, p0, stats=stats, cells=True)
+    b = engine.pairs(w0.X, w0.xi, w0.yi, p0, stats=stats, cells=True, devices=devices,
+                     shard_chunk=chunk)
+    for k in stats + ("cells",):
+        assert np.array_equal(bits(a[k]), bits(b[k])), k
+    w3 = datagen.make(3)                             # cross, general tier
+    X, Y = w3.X[:3], w3.X[3:7]
+    a = engine.cross(X, Y, stats=stats)
+    b = engine.cross(X, Y, stats=stats, devices=devices, shard_chunk=chunk, first=2, count=9)
+    for k in stats:
+        assert np.array_equal(bits(a[k][2:11]), bits(b[k])), k
+
+
+def test_virtual_shards_errors(engine):
+    V = np.ascontiguousarray(datagen.make(1).X[:20])
+    with pytest.raises(MineError, match="finite"):
+        bad = V.copy()
+        bad[3, 3] = np.inf
+        engine.pairwise(bad, devices=[0, 0])
+    with pytest.raises(MineError):
+        engine.pairwise(V, devices=[0, 99])
