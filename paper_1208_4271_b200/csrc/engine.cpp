@@ -190,14 +190,19 @@ struct mine_b200_ctx {
   TableSet tables;
   DevBuf vals, perm, runid, runstart, nruns, q, yhat, hq, lw, rsmask;
   DevBuf ocells, stats, flag, idx, counters, memo, memo_vals, memo_val, rec, dx, sxx, micscr, sortscr;
-  // general tier: the row targets y are independent, so they run on
-  // kYLanes streams at once, each lane with its own scratch set
-  static constexpr int kYLanes = 8;
-  struct YLane {
-    cudaStream_t s = nullptr;
-    cudaEvent_t done = nullptr;
-    DevBuf gscr, gqueue, glists, fscratch;
-  } ylane[kYLanes];
+  // general tier: one launch group per chunk of pairs (or per y-group when
+  // the scratch of all y's would not fit): scratch regions, the group's y
+  // table and counters, the DP launches' F slots; the DP launches of
+  // different kernel variants and the warp path run on extra lanes
+  // The y's of a y-group are dealt round-robin to kGenLanes lane groups that
+  // run concurrently (one's partitions overlap another's DP); each has a main
+  // and a side stream and its own buffers.
+  static constexpr int kGenLanes = 8;
+  struct GenLane {
+    cudaStream_t s = nullptr, side = nullptr;
+    cudaEvent_t ev[3] = {};
+    DevBuf scr, ys, cnt, fslots;
+  } glane[kGenLanes];
   int memo_n = -1, memo_nval = 0;
   // per-variable state of the previous call (opts.reuse_vars)
   struct Prep {
@@ -266,33 +271,59 @@ cudaEvent_t ctx_event(mine_b200_ctx* ctx, size_t i) {
   return ctx->events[i];
 }
 
-// Scratch of the general tier for `nsub` subproblems at one row target (the
-// layout depends on y; one buffer is reused across y and chunks).
-GenScratch gen_scratch(mine_b200_ctx::YLane& ln, int n, const YParams& yp, long long nsub) {
-  GenScratch g;
-  g.kc = gen_kc(n, yp);
-  g.cum_stride = (size_t)yp.y * (g.kc + 1);
-  auto a16 = [](size_t x) { return (x + 15) & ~size_t(15); };
-  const size_t f2b = a16(sizeof(double) * (size_t)(g.kc + 1) * nsub);
-  const size_t descb = a16(sizeof(int) * 4 * nsub);
-  const size_t cbb = a16(sizeof(int) * (size_t)(g.kc + 1) * nsub);
-  const size_t cumb = a16(sizeof(int) * g.cum_stride * nsub);
-  const size_t ptsb = a16(gen_pts_bytes(n, yp) * nsub);
-  char* base = static_cast<char*>(ln.gscr.ensure(f2b + descb + cbb + cumb + ptsb));
-  if (ptsb) g.pts = reinterpret_cast<unsigned char*>(base + f2b + descb + cbb + cumb);
-  g.tables_global = gen_tables_global(n, yp);
-  g.f2 = reinterpret_cast<double*>(base);
-  g.desc = reinterpret_cast<int*>(base + f2b);
-  g.cb = reinterpret_cast<int*>(base + f2b + descb);
-  g.cum = reinterpret_cast<int*>(base + f2b + descb + cbb);
-  g.queue = static_cast<unsigned long long*>(ln.gqueue.ensure(4 * sizeof(unsigned long long)));
-  g.nsub = nsub;
-  g.lists = static_cast<long long*>(ln.glists.ensure(2 * sizeof(long long) * (size_t)nsub));
-  g.small_ok = gen_warp_smem_per_warp(yp) <= 24 * 1024;
-  if (yp.x_max >= 3)
-    g.fslots = static_cast<double*>(
-        ln.fscratch.ensure(gen_fslot_bytes(n, yp) * (size_t)gen_dp_grid(n, yp)));
-  return g;
+// Device memory budget of the general tier's per-chunk scratch
+// (MINE_B200_GEN_BUDGET_MB overrides; the F slots come on top).
+size_t gen_budget() {
+  static const size_t b = [] {
+    const char* e = std::getenv("MINE_B200_GEN_BUDGET_MB");
+    return e ? (size_t)std::atoll(e) << 20 : (size_t)8 << 30;
+  }();
+  return b;
+}
+
+static int gen_lanes() {
+  static const int v = [] {
+    const char* e = std::getenv("MINE_B200_GEN_LANES");
+    const int x = e ? std::atoi(e) : 1;  // measured: 1 group is fastest (c0 / c3)
+    return std::max(1, std::min(x, (int)mine_b200_ctx::kGenLanes));
+  }();
+  return v;
+}
+
+// The general tier for the row targets yps[0 .. ny) of pairs [0, npairs) of
+// pc: y's dealt round-robin to the lane groups (ascending y within each), each
+// group a gen_run_group on its own streams, forked from and joined into s.
+int run_gen_group(mine_b200_ctx* ctx, const VarSet& vs, const Tables& tb, const PairSpace& pc,
+                  long long npairs, const YParams* yps, int ny, double* ocells, const SubDebug* dbg,
+                  int orient_only, unsigned long long* dcnt, cudaStream_t s) {
+  const long long nsub = npairs * (orient_only >= 0 ? 1 : 2);
+  const int G = std::min(gen_lanes(), ny);
+  CK(cudaEventRecord(ctx_event(ctx, 4), s));
+  int launches = 0;
+  for (int g = 0; g < G; ++g) {
+    auto& L = ctx->glane[g];
+    if (!L.s) {
+      CK(cudaStreamCreateWithFlags(&L.s, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&L.side, cudaStreamNonBlocking));
+      for (auto& e : L.ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    std::vector<YParams> mine;
+    for (int i = g; i < ny; i += G) mine.push_back(yps[i]);
+    size_t scr = 0;
+    for (const auto& yp : mine) scr += nsub * (gen_scratch_per_sub(vs.n, yp) + 16 * 8);
+    void* scratch = L.scr.ensure(scr);
+    GenY* d_ys = static_cast<GenY*>(L.ys.ensure(sizeof(GenY) * mine.size()));
+    auto* d_cnt = static_cast<unsigned long long*>(L.cnt.ensure(sizeof(unsigned long long) * 4 * mine.size()));
+    double* fslots = static_cast<double*>(
+        L.fslots.ensure(gen_group_fslot_bytes(vs.n, mine.data(), (int)mine.size(), nsub)));
+    CK(cudaStreamWaitEvent(L.s, ctx_event(ctx, 4), 0));
+    launches += gen_run_group(vs, tb, pc, 0, npairs, mine.data(), (int)mine.size(), scratch, d_ys, d_cnt,
+                              fslots, ocells, dbg, orient_only, dcnt, L.s, L.side, L.ev);
+    CK(cudaEventRecord(L.ev[2], L.s));
+    CK(cudaStreamWaitEvent(s, L.ev[2], 0));
+  }
+  CK(cudaGetLastError());
+  return launches;
 }
 
 // The per-variable state a successful call leaves on its context.
@@ -487,22 +518,48 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
     yp.k_hat = std::max(1, static_cast<int>(std::floor(par->c * static_cast<double>(yp.x_max))));
     yps.push_back(yp);
   }
-  size_t per_pair = 16 * (size_t)ncell;  // ocells
+  // General tier plan: every row target of a chunk in one launch group when
+  // its scratch fits the budget with at least two pairs per SM; otherwise
+  // (c4: B = 1000, 499 row targets) the y's are packed into consecutive
+  // groups that each fit, and the chunk is as large as the biggest y allows.
+  const size_t budget = gen_budget();
+  long long gen_chunk = 0;
+  std::vector<std::pair<int, int>> ygroups;  // [first, last) indices into yps
   if (!small) {
-    size_t sub_max = 0;
+    size_t sub_sum = 0, sub_max = 0;
     for (const auto& yp : yps) {
       if (gen_pf_smem(n, yp) > 227 * 1024 || gen_dp_smem(n, yp) > 227 * 1024)
         throw Failure("mine_b200: general tier shared-memory plan exceeds 227 KB for n=" +
                       std::to_string(n) + " y=" + std::to_string(yp.y));
-      sub_max = std::max(sub_max, gen_scratch_per_sub(n, yp));
+      const size_t b = gen_scratch_per_sub(n, yp) + 16 * 8;  // + the regions' alignment
+      sub_sum += b;
+      sub_max = std::max(sub_max, b);
     }
-    per_pair += 2 * sub_max * std::min<size_t>(mine_b200_ctx::kYLanes, yps.size());
+    const size_t cell_b = 16 * (size_t)ncell;
+    gen_chunk = std::max<long long>(1, std::min<long long>(count, (long long)(budget / (cell_b + 2 * sub_sum))));
+    if (gen_chunk < std::min<long long>(count, 2LL * ctx->sms)) {
+      gen_chunk = std::max<long long>(1, std::min<long long>(count, (long long)(budget / (cell_b + 2 * sub_max))));
+      const size_t room = budget - std::min(budget, cell_b * (size_t)gen_chunk);
+      for (int i = 0; i < (int)yps.size();) {
+        int j = i;
+        size_t acc = 0;
+        while (j < (int)yps.size()) {
+          const size_t b = 2 * (size_t)gen_chunk * (gen_scratch_per_sub(n, yps[j]) + 16 * 8);
+          if (j > i && acc + b > room) break;
+          acc += b;
+          ++j;
+        }
+        ygroups.push_back({i, j});
+        i = j;
+      }
+    } else {
+      ygroups.push_back({0, (int)yps.size()});
+    }
   }
   // host io streams the small tiers in chunks of one 8192-pair sort batch
   // per SM (the memo kernel deals whole batches), so no SM idles per chunk
   const long long chunk = small ? (dio ? count : std::min<long long>(count, 8192LL * ctx->sms))
-                               : std::max<long long>(1, std::min<long long>(
-                                     count, (long long)((4096ULL << 20) / per_pair)));
+                               : gen_chunk;
   const long long nchunks = (count + chunk - 1) / chunk;
   const int nslots = dio ? 1 : 2;  // double-buffered staging for host io
   double* stage = nullptr;
@@ -559,35 +616,11 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
       launch_tiny_pairs(vs, tb, pc, par->c, par->est, so, cells_dst, dcnt, s);
       ++ctx->launches;
     } else {
-      // row targets round-robin over the y lanes (y = 2, the heaviest, first);
-      // each lane joins the main stream before the reduction
-      const int nl = (int)std::min<size_t>(mine_b200_ctx::kYLanes, yps.size());
-      CK(cudaEventRecord(ctx_event(ctx, 4), s));
-      for (int j = 0; j < nl; ++j) {
-        auto& ln = ctx->ylane[j];
-        if (!ln.s) {
-          CK(cudaStreamCreateWithFlags(&ln.s, cudaStreamNonBlocking));
-          CK(cudaEventCreateWithFlags(&ln.done, cudaEventDisableTiming));
-        }
-        CK(cudaStreamWaitEvent(ln.s, ctx_event(ctx, 4), 0));
-      }
-      for (size_t i = 0; i < yps.size(); ++i) {
-        const YParams& yp = yps[i];
-        auto& ln = ctx->ylane[i % nl];
-        const GenScratch gs = gen_scratch(ln, n, yp, 2 * cn);
-        CK(cudaMemsetAsync(gs.queue, 0, 4 * sizeof(unsigned long long), ln.s));
-        launch_part_f2(vs, tb, pc, 0, cn, yp, gs, ocells, nullptr, -1, dcnt, ln.s);
-        ++ctx->launches;
-        if (yp.x_max >= 3) {
-          launch_dp_warp(vs, tb, pc, 0, cn, yp, gs, ocells, nullptr, -1, ln.s);
-          launch_dp(vs, tb, pc, 0, cn, yp, gs, ocells, nullptr, -1, ln.s);
-          ctx->launches += gs.small_ok ? 2 : 1;
-        }
-      }
-      for (int j = 0; j < nl; ++j) {
-        CK(cudaEventRecord(ctx->ylane[j].done, ctx->ylane[j].s));
-        CK(cudaStreamWaitEvent(s, ctx->ylane[j].done, 0));
-      }
+      // one launch group per y-group (usually all y's): partitions of every
+      // (y, subproblem), then the DP kernels pulling subproblems y by y
+      for (const auto& gr : ygroups)
+        ctx->launches += run_gen_group(ctx, vs, tb, pc, cn, yps.data() + gr.first,
+                                       gr.second - gr.first, ocells, nullptr, -1, dcnt, s);
       launch_reduce(tb, cn, ocells, par->est, so, 0, s);
       ++ctx->launches;
       if (cells_dst)
@@ -815,9 +848,11 @@ void mine_b200_destroy(mine_b200_ctx* ctx) {
     cudaEventSynchronize(ctx->last_done);
     cudaEventDestroy(ctx->last_done);
   }
-  for (auto& ln : ctx->ylane) {
-    if (ln.s) cudaStreamDestroy(ln.s);
-    if (ln.done) cudaEventDestroy(ln.done);
+  for (auto& L : ctx->glane) {
+    if (L.s) cudaStreamDestroy(L.s);
+    if (L.side) cudaStreamDestroy(L.side);
+    for (auto e : L.ev)
+      if (e) cudaEventDestroy(e);
   }
   delete ctx;
 }
@@ -950,12 +985,7 @@ int mine_b200_debug_subproblem(mine_b200_ctx* ctx, int n, const double* col_var,
     dbg.q_x = ib + 3;
     dbg.bounds = ib + 3 + n;
     double* oc = static_cast<double*>(ctx->ocells.ensure(sizeof(double) * 2 * tb.ncell));
-    const GenScratch gs = gen_scratch(ctx->ylane[0], n, yp, 1);
-    CK(cudaMemsetAsync(gs.queue, 0, 4 * sizeof(unsigned long long), s));
-    launch_part_f2(vs, tb, ps, 0, 1, yp, gs, oc, &dbg, 0, nullptr, s);
-    launch_dp_warp(vs, tb, ps, 0, 1, yp, gs, oc, &dbg, 0, s);
-    launch_dp(vs, tb, ps, 0, 1, yp, gs, oc, &dbg, 0, s);
-    CK(cudaGetLastError());
+    run_gen_group(ctx, vs, tb, ps, 1, &yp, 1, oc, &dbg, 0, nullptr, s);
     std::vector<char> h(bytes);
     CK(cudaMemcpyAsync(h.data(), dd, bytes, cudaMemcpyDeviceToHost, s));
     mark_call_done(ctx, s);

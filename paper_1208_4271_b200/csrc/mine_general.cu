@@ -20,6 +20,8 @@
 // Compiled with -fmad=false; every FP64 op rounds like the reference's.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
+#include <vector>
 
 #include "device_common.cuh"
 #include "mine_kernels.h"
@@ -83,6 +85,22 @@ __host__ __device__ inline PfLayout pf_layout(int n, int y, int kc, bool pts_glo
   return L;
 }
 
+// The device view of row target Y's scratch.
+__device__ __forceinline__ GenScratch scratch_of(const GenY& Y, long long nsub) {
+  GenScratch g;
+  g.desc = Y.desc;
+  g.cb = Y.cb;
+  g.cum = Y.cum;
+  g.f2 = Y.f2;
+  g.nsub = nsub;
+  g.kc = Y.kc;
+  g.cum_stride = Y.cum_stride;
+  g.small_ok = Y.small_ok;
+  g.pts = Y.pts;
+  g.tables_global = Y.tables_global;
+  return g;
+}
+
 __device__ __forceinline__ void sub_vars(const PairSpace& ps, long long pl, int orient, int& X,
                                          int& Y) {
   int va, vb;
@@ -107,18 +125,23 @@ __device__ void write_cells(const Tables& tb, double* ocells, long long pl, int 
 }
 
 // ---------------------------------------------------------------------------
+// Grid: nsub x (the group's y's gi0 .. gi0 + gridDim.x / nsub - 1), y-major.
 template <int kPfThreads, bool kPtsGlobal, bool kCumGlobal>
 __global__ void __launch_bounds__(kPfThreads, 2048 / kPfThreads) k_part_f2(VarSet vs, Tables tb, PairSpace ps,
-                                                        long long base, YParams yp, GenScratch gs,
+                                                        long long base, GenGroup grp, int gi0,
                                                         double* __restrict__ ocells, SubDebug dbg,
                                                         int has_dbg, int orient_only,
                                                         unsigned long long* counters) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = vs.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int norient = orient_only >= 0 ? 1 : 2;
-  const long long pl = base + blockIdx.x / norient;
-  const int orient = orient_only >= 0 ? orient_only : (int)(blockIdx.x % 2);
-  const long long sub = (long long)blockIdx.x;  // index inside this launch's scratch
+  const int gi = gi0 + (int)(blockIdx.x / grp.nsub);
+  const long long sub = (long long)(blockIdx.x % grp.nsub);  // index inside this y's scratch
+  const GenY& GY = grp.ys[gi];
+  const YParams yp = GY.yp;
+  const GenScratch gs = scratch_of(GY, grp.nsub);
+  const long long pl = base + sub / norient;
+  const int orient = orient_only >= 0 ? orient_only : (int)(sub % 2);
   int X, Y;
   sub_vars(ps, pl, orient, X, Y);
   const int y = yp.y, yi = yp.yi, x_max = yp.x_max, k_hat = yp.k_hat, kc = gs.kc;
@@ -262,9 +285,9 @@ __global__ void __launch_bounds__(kPfThreads, 2048 / kPfThreads) k_part_f2(VarSe
       d.w = l_max;
       reinterpret_cast<int4*>(gs.desc)[sub] = d;
       if (gs.small_ok && k <= kSmallK)
-        gs.lists[atomicAdd(gs.queue + 2, 1ull)] = sub;
+        GY.small_list[atomicAdd(grp.cnt + gi, 1ull)] = sub;
       else
-        gs.lists[gs.nsub + (long long)atomicAdd(gs.queue + 3, 1ull)] = sub;
+        GY.big_list[atomicAdd(grp.cnt + grp.ny + gi, 1ull)] = sub;
     }
     int* gcb = gs.cb + (size_t)sub * (kc + 1);
     int* gcum = gs.cum + (size_t)sub * gs.cum_stride;
@@ -332,8 +355,10 @@ __global__ void __launch_bounds__(kPfThreads, 2048 / kPfThreads) k_part_f2(VarSe
 // ---------------------------------------------------------------------------
 constexpr int kFRing = 128;  // F row ring width above 128 levels (power of two >= 65)
 __host__ __device__ inline int fring_width(int LW) { return LW > kFRing ? kFRing : LW; }
+// Rows 0 .. kc of F, then the row fk of F(k, .) that the ring variants keep
+// (always reserved: the global-table variant runs the ring code at any width).
 __host__ __device__ inline size_t fslot_doubles(int kc, int LW) {
-  return (size_t)(kc + 1) * fring_width(LW) + (LW > kFRing ? LW : 0);
+  return (size_t)(kc + 1) * fring_width(LW) + LW;
 }
 
 struct DpLayout {
@@ -500,43 +525,63 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 // kLean: x_max <= kLeanXMax (one level tile of <= 62 levels): compiled for 64
 // registers so 4 CTAs share an SM; the wider variants keep 80 (3 per SM).
 
+// Persistent: each CTA pulls subproblems from the big lists of the y's
+// gi0 .. gi0 + gcount - 1 in ascending y (the heaviest first).  The layout is
+// set up per item (the launch's shared memory is the maximum over its y's);
+// F lives in this CTA's HBM slot of fslot_stride doubles.
 template <bool kGlobalTables, bool kRing, bool kLean>
 __global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : 3) k_dp(VarSet vs, Tables tb, PairSpace ps,
-                                                      long long base, long long nsub, YParams yp,
-                                                      GenScratch gs, double* __restrict__ ocells,
+                                                      long long base, GenGroup grp, int gi0,
+                                                      int gcount, double* __restrict__ fslots,
+                                                      unsigned long long fslot_stride,
+                                                      double* __restrict__ ocells,
                                                       SubDebug dbg, int has_dbg, int orient_only) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ long long s_sub;
+  __shared__ int s_gi;
   const int tid = threadIdx.x;
-  const int y = yp.y, x_max = yp.x_max, kc = gs.kc, LW = x_max - 1;
-  const DpLayout L = dp_layout(y, kc, x_max, kGlobalTables, kLean);
-  // row widths: compile-time for the wide variants (x_max > 64: 64 / 65)
-  const int fsw = kLean ? L.fsw : 64, ftw = kLean ? L.ftw : 65;
-  int* cb = reinterpret_cast<int*>(smem + L.cb);
-  int* cum = reinterpret_cast<int*>(smem + L.cum);
-  double* A = reinterpret_cast<double*>(smem + L.A);
-  double* W = reinterpret_cast<double*>(smem + L.W);
-  double* accS = reinterpret_cast<double*>(smem + L.acc);
-  double* fs = reinterpret_cast<double*>(smem + L.fs);
-  double* ft = reinterpret_cast<double*>(smem + L.ft);
-  // F(t, l) at column l - 2 of row t; above 128 levels the row is a ring of
-  // 128 columns (a level tile reads l0-1 .. l1-1 and writes l0 .. l1, 65
-  // columns), and F(k, .) -- all of which I_l needs -- is kept in its own row fk
-  // (kRing: x_max > 129 only).
-  const int RW = kRing ? fring_width(LW) : LW, cm = kRing ? kFRing - 1 : 0x7fffffff;
-  double* F = gs.fslots + (size_t)blockIdx.x * fslot_doubles(kc, LW);
-  double* fk = F + (size_t)(kc + 1) * RW;
   const int norient = orient_only >= 0 ? 1 : 2;
+  if (tid == 0) s_gi = gi0;
+  double* const F = fslots + (size_t)blockIdx.x * fslot_stride;
 
   for (;;) {
     __syncthreads();
     if (tid == 0) {
-      const unsigned long long i = atomicAdd(gs.queue, 1ull);
-      s_sub = i < gs.queue[3] ? gs.lists[gs.nsub + i] : -1;
+      long long got = -1;
+      int gi = s_gi;
+      for (; gi < gi0 + gcount; ++gi) {  // ascending y: drain y's list, then move on
+        const unsigned long long i = atomicAdd(grp.cnt + 2 * grp.ny + gi, 1ull);
+        if (i < grp.cnt[grp.ny + gi]) {
+          got = grp.ys[gi].big_list[i];
+          break;
+        }
+      }
+      s_gi = gi;
+      s_sub = got;
     }
     __syncthreads();
     const long long sub = s_sub;
     if (sub < 0) break;
+    const GenY& GY = grp.ys[s_gi];
+    const YParams yp = GY.yp;
+    const GenScratch gs = scratch_of(GY, grp.nsub);
+    const int y = yp.y, x_max = yp.x_max, kc = gs.kc, LW = x_max - 1;
+    const DpLayout L = dp_layout(y, kc, x_max, kGlobalTables, kLean);
+    // row widths: compile-time for the wide variants (x_max > 64: 64 / 65)
+    const int fsw = kLean ? L.fsw : 64, ftw = kLean ? L.ftw : 65;
+    int* cb = reinterpret_cast<int*>(smem + L.cb);
+    int* cum = reinterpret_cast<int*>(smem + L.cum);
+    double* A = reinterpret_cast<double*>(smem + L.A);
+    double* W = reinterpret_cast<double*>(smem + L.W);
+    double* accS = reinterpret_cast<double*>(smem + L.acc);
+    double* fs = reinterpret_cast<double*>(smem + L.fs);
+    double* ft = reinterpret_cast<double*>(smem + L.ft);
+    // F(t, l) at column l - 2 of row t; above 128 levels the row is a ring of
+    // 128 columns (a level tile reads l0-1 .. l1-1 and writes l0 .. l1, 65
+    // columns), and F(k, .) -- all of which I_l needs -- is kept in its own row fk
+    // (kRing: x_max > 129 only).
+    const int RW = kRing ? fring_width(LW) : LW, cm = kRing ? kFRing - 1 : 0x7fffffff;
+    double* fk = F + (size_t)(kc + 1) * RW;
     const int4 d = reinterpret_cast<const int4*>(gs.desc)[sub];
     const int k = d.x, rows = d.y, l_max = d.w, kk = k + 1;
     if (l_max < 3) continue;  // finished by k_part_f2
@@ -719,30 +764,44 @@ __host__ __device__ inline WarpLayout warp_layout(int y, int x_max) {
 
 constexpr int kWarpThreads = 256;
 
+// Persistent warps pulling the small subproblems of the y's gi0 .. gi0 +
+// gcount - 1 in ascending y; each warp owns per_warp bytes of shared memory
+// (the maximum warp_layout over the launch's y's).
 __global__ void __launch_bounds__(kWarpThreads) k_dp_warp(VarSet vs, Tables tb, PairSpace ps,
-                                                          long long base, YParams yp,
-                                                          GenScratch gs,
+                                                          long long base, GenGroup grp, int gi0,
+                                                          int gcount, int per_warp,
                                                           double* __restrict__ ocells,
                                                           SubDebug dbg, int has_dbg,
                                                           int orient_only) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int y = yp.y, x_max = yp.x_max, LW = x_max - 1, kc = gs.kc;
-  const WarpLayout L = warp_layout(y, x_max);
-  unsigned char* wb = smem + (size_t)wib * L.per_warp;
-  double* F = reinterpret_cast<double*>(wb + L.F);
-  double* A = reinterpret_cast<double*>(wb + L.A);
-  double* W = reinterpret_cast<double*>(wb + L.W);
-  int* cb = reinterpret_cast<int*>(wb + L.cb);
-  int* cum = reinterpret_cast<int*>(wb + L.cum);
+  unsigned char* wb = smem + (size_t)wib * per_warp;
   const int norient = orient_only >= 0 ? 1 : 2;
-  const unsigned long long nsmall = gs.queue[2];
+  int gi = gi0;
   for (;;) {
-    unsigned long long i = 0;
-    if (lane == 0) i = atomicAdd(gs.queue + 1, 1ull);
-    i = __shfl_sync(0xffffffffu, i, 0);
-    if (i >= nsmall) break;
-    const long long sub = gs.lists[i];
+    long long got = -1;
+    if (lane == 0) {
+      for (; gi < gi0 + gcount; ++gi) {
+        const unsigned long long i = atomicAdd(grp.cnt + 3 * grp.ny + gi, 1ull);
+        if (i < grp.cnt[gi]) {
+          got = grp.ys[gi].small_list[i];
+          break;
+        }
+      }
+    }
+    gi = __shfl_sync(0xffffffffu, gi, 0);
+    const long long sub = __shfl_sync(0xffffffffu, got, 0);
+    if (sub < 0) break;
+    const GenY& GY = grp.ys[gi];
+    const YParams yp = GY.yp;
+    const GenScratch gs = scratch_of(GY, grp.nsub);
+    const int y = yp.y, x_max = yp.x_max, LW = x_max - 1, kc = gs.kc;
+    const WarpLayout L = warp_layout(y, x_max);
+    double* F = reinterpret_cast<double*>(wb + L.F);
+    double* A = reinterpret_cast<double*>(wb + L.A);
+    double* W = reinterpret_cast<double*>(wb + L.W);
+    int* cb = reinterpret_cast<int*>(wb + L.cb);
+    int* cum = reinterpret_cast<int*>(wb + L.cum);
     const int4 d = reinterpret_cast<const int4*>(gs.desc)[sub];
     const int k = d.x, rows = d.y, l_max = d.w, kk = k + 1;
     {
@@ -850,14 +909,12 @@ size_t gen_pts_bytes(int n, const YParams& yp) {
 size_t gen_scratch_per_sub(int n, const YParams& yp) {
   const size_t kc = (size_t)gen_kc(n, yp);
   return sizeof(int4) + sizeof(int) * (kc + 1) + sizeof(int) * (size_t)yp.y * (kc + 1) +
-         sizeof(double) * (kc + 1) + gen_pts_bytes(n, yp);
+         sizeof(double) * (kc + 1) + gen_pts_bytes(n, yp) + 2 * sizeof(long long);
 }
 
 size_t gen_pf_smem(int n, const YParams& yp) {
   return pf_layout(n, yp.y, gen_kc(n, yp), gen_pts_global(n, yp), gen_tables_global(n, yp)).total;
 }
-
-bool gen_dp_f_in_smem(int, const YParams&) { return false; }
 
 // The lean k_dp (64 registers) pays off only where its compact layout lets 4
 // CTAs share an SM; alone on an SM the 80-register variant is faster (c4).
@@ -874,48 +931,15 @@ size_t gen_fslot_bytes(int n, const YParams& yp) {
   return sizeof(double) * fslot_doubles(gen_kc(n, yp), yp.x_max - 1);
 }
 
-int gen_dp_grid(int n, const YParams& yp) {
+static int sm_count() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t sm = gen_dp_smem(n, yp);
-  // up to 4 CTAs per SM, as shared memory allows (the wide variants are
-  // register-bound at 3 resident; their extra CTAs start as others finish)
-  const int per = (int)std::max<size_t>(1, std::min<size_t>(4, (228 * 1024) / (sm + 1024)));
-  // the F slots of one lane stay within 4 GB (very large c B)
-  const long long cap = std::max<long long>(1, (4LL << 30) / (long long)gen_fslot_bytes(n, yp));
-  return (int)std::min<long long>((long long)sms * per, cap);
+  return sms;
 }
 
-size_t gen_warp_smem_per_warp(const YParams& yp) { return warp_layout(yp.y, yp.x_max).per_warp; }
-
-void launch_dp_warp(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
-                    long long npairs, const YParams& yp, const GenScratch& gs, double* ocells,
-                    const SubDebug* dbg, int orient_only, cudaStream_t s) {
-  if (npairs <= 0 || yp.x_max < 3 || !gs.small_ok) return;
-  const size_t per_warp = gen_warp_smem_per_warp(yp);
-  const int warps = kWarpThreads / 32;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t sm = per_warp * warps;
-  const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / (sm + 1024)));
-  const long long nsub = npairs * (orient_only >= 0 ? 1 : 2);
-  const int grid = (int)std::max<long long>(1, std::min<long long>((nsub + warps - 1) / warps,
-                                                                    (long long)sms * per_sm));
-  SubDebug d{};
-  if (dbg) d = *dbg;
-  k_dp_warp<<<grid, kWarpThreads, sm, s>>>(vs, tb, ps, base, yp, gs, ocells, d, dbg ? 1 : 0,
-                                           orient_only);
-}
-
-size_t div_table_doubles(int n) { return (size_t)(n + 1) * (n + 2) / 2; }
-
-void launch_build_div(double* div, int n, cudaStream_t s) {
-  const size_t total = div_table_doubles(n);
-  const unsigned blocks = (unsigned)std::min<size_t>(4096, (total + 255) / 256);
-  k_build_div<<<blocks, 256, 0, s>>>(div, n);
-}
+static size_t warp_per_warp(const YParams& yp) { return warp_layout(yp.y, yp.x_max).per_warp; }
+static bool warp_ok(const YParams& yp) { return yp.x_max >= 3 && warp_per_warp(yp) <= 24 * 1024; }
 
 // up to this many samples the F(t,2) level runs on 128 threads too (c2,
 // n = 500: +8%; 64 threads measured slower)
@@ -927,52 +951,182 @@ static int pf_small_n() {
   return v;
 }
 
-void launch_part_f2(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
-                    long long npairs, const YParams& yp, const GenScratch& gs, double* ocells,
-                    const SubDebug* dbg, int orient_only, unsigned long long* counters,
-                    cudaStream_t s) {
-  if (npairs <= 0) return;
-  const unsigned blocks = (unsigned)(npairs * (orient_only >= 0 ? 1 : 2));
-  SubDebug d{};
-  if (dbg) d = *dbg;
-  const size_t sm = gen_pf_smem(vs.n, yp);
-  const int dg = dbg ? 1 : 0;
-  if (gs.tables_global)
-    k_part_f2<256, true, true><<<blocks, 256, sm, s>>>(vs, tb, ps, base, yp, gs, ocells, d, dg,
-                                                       orient_only, counters);
-  else if (gs.pts)
-    k_part_f2<256, true, false><<<blocks, 256, sm, s>>>(vs, tb, ps, base, yp, gs, ocells, d, dg,
-                                                        orient_only, counters);
-  else if (yp.x_max >= 3 && vs.n > pf_small_n())
-    k_part_f2<256, false, false><<<blocks, 256, sm, s>>>(vs, tb, ps, base, yp, gs, ocells, d, dg,
-                                                         orient_only, counters);
-  else
-    k_part_f2<128, false, false><<<blocks, 128, sm, s>>>(vs, tb, ps, base, yp, gs, ocells, d, dg,
-                                                         orient_only, counters);
+// k_part_f2 / k_dp template variant of a row target; a launch covers a run of
+// consecutive y's with the same variant.
+enum { kPfGlobalTables = 0, kPfGlobalPts, kPf256, kPf128 };
+static int pf_variant(int n, const YParams& yp) {
+  if (gen_tables_global(n, yp)) return kPfGlobalTables;
+  if (gen_pts_bytes(n, yp)) return kPfGlobalPts;
+  return yp.x_max >= 3 && n > pf_small_n() ? kPf256 : kPf128;
+}
+enum { kDpNone = -1, kDpGlobalTables = 0, kDpRing, kDpWide, kDpLean };
+static int dp_variant(int n, const YParams& yp) {
+  if (yp.x_max < 3) return kDpNone;
+  if (gen_tables_global(n, yp)) return kDpGlobalTables;
+  if (yp.x_max - 1 > kFRing) return kDpRing;
+  return gen_dp_lean(n, yp) ? kDpLean : kDpWide;
 }
 
-void launch_dp(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
-               long long npairs, const YParams& yp, const GenScratch& gs, double* ocells,
-               const SubDebug* dbg, int orient_only, cudaStream_t s) {
-  if (npairs <= 0 || yp.x_max < 3) return;
+// The k_dp launches of a group: runs of consecutive y's with one variant.
+struct DpRun {
+  int gi0, count, variant, grid;
+  size_t smem, fslot_doubles;
+};
+static std::vector<DpRun> dp_runs(int n, const YParams* yps, int ny, long long nsub) {
+  std::vector<DpRun> runs;
+  const int sms = sm_count();
+  for (int gi = 0; gi < ny;) {
+    const int v = dp_variant(n, yps[gi]);
+    int gj = gi + 1;
+    while (gj < ny && dp_variant(n, yps[gj]) == v) ++gj;
+    if (v != kDpNone) {
+      DpRun r{gi, gj - gi, v, 0, 0, 0};
+      for (int g = gi; g < gj; ++g) {
+        r.smem = std::max(r.smem, gen_dp_smem(n, yps[g]));
+        r.fslot_doubles = std::max(r.fslot_doubles, gen_fslot_bytes(n, yps[g]) / sizeof(double));
+      }
+      // up to 4 CTAs per SM, as shared memory allows (the wide variants are
+      // register-bound at 3 resident; their extra CTAs start as others finish)
+      const int per = (int)std::max<size_t>(1, std::min<size_t>(4, (228 * 1024) / (r.smem + 1024)));
+      // the F slots of one run stay within 4 GB (very large c B)
+      const long long cap = std::max<long long>(1, (4LL << 30) / (long long)(8 * r.fslot_doubles));
+      r.grid = (int)std::min<long long>(std::min<long long>((long long)sms * per, cap),
+                                        nsub * (gj - gi));
+      runs.push_back(r);
+    }
+    gi = gj;
+  }
+  return runs;
+}
+
+size_t gen_group_fslot_bytes(int n, const YParams* yps, int ny, long long nsub) {
+  size_t b = 0;
+  for (const DpRun& r : dp_runs(n, yps, ny, nsub)) b += al16(8 * r.fslot_doubles * (size_t)r.grid);
+  return b;
+}
+
+int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
+                  long long npairs, const YParams* yps, int ny, void* scratch, GenY* d_ys,
+                  unsigned long long* d_cnt, double* fslots, double* ocells, const SubDebug* dbg,
+                  int orient_only, unsigned long long* counters, cudaStream_t s0, cudaStream_t side,
+                  cudaEvent_t* ev) {
+  if (npairs <= 0 || ny <= 0) return 0;
+  const int n = vs.n;
   const long long nsub = npairs * (orient_only >= 0 ? 1 : 2);
-  const int grid = (int)std::min<long long>(nsub, gen_dp_grid(vs.n, yp));
+  // ---- per-y scratch regions, carved from one buffer
+  std::vector<GenY> hy(ny);
+  char* p = static_cast<char*>(scratch);
+  auto carve = [&](size_t bytes) {
+    char* q = p;
+    p += al16(bytes);
+    return q;
+  };
+  for (int gi = 0; gi < ny; ++gi) {
+    GenY& Y = hy[gi];
+    std::memset(&Y, 0, sizeof(Y));
+    Y.yp = yps[gi];
+    Y.kc = gen_kc(n, Y.yp);
+    Y.small_ok = warp_ok(Y.yp);
+    Y.tables_global = gen_tables_global(n, Y.yp);
+    Y.cum_stride = (unsigned long long)Y.yp.y * (Y.kc + 1);
+    Y.desc = reinterpret_cast<int*>(carve(sizeof(int4) * nsub));
+    Y.cb = reinterpret_cast<int*>(carve(sizeof(int) * (size_t)(Y.kc + 1) * nsub));
+    Y.cum = reinterpret_cast<int*>(carve(sizeof(int) * Y.cum_stride * nsub));
+    Y.f2 = reinterpret_cast<double*>(carve(sizeof(double) * (size_t)(Y.kc + 1) * nsub));
+    const size_t ptsb = gen_pts_bytes(n, Y.yp);
+    Y.pts = ptsb ? reinterpret_cast<unsigned char*>(carve(ptsb * nsub)) : nullptr;
+    Y.small_list = reinterpret_cast<long long*>(carve(sizeof(long long) * nsub));
+    Y.big_list = reinterpret_cast<long long*>(carve(sizeof(long long) * nsub));
+  }
+  cudaMemcpyAsync(d_ys, hy.data(), sizeof(GenY) * ny, cudaMemcpyHostToDevice, s0);
+  cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 4 * ny, s0);
+  GenGroup g;
+  g.ys = d_ys;
+  g.ny = ny;
+  g.nsub = nsub;
+  g.cnt = d_cnt;
   SubDebug d{};
   if (dbg) d = *dbg;
-  const size_t sm = gen_dp_smem(vs.n, yp);
   const int dg = dbg ? 1 : 0;
-  if (gs.tables_global)
-    k_dp<true, true, false><<<grid, kDpThreads, sm, s>>>(vs, tb, ps, base, nsub, yp, gs, ocells,
-                                                         d, dg, orient_only);
-  else if (yp.x_max - 1 > kFRing)
-    k_dp<false, true, false><<<grid, kDpThreads, sm, s>>>(vs, tb, ps, base, nsub, yp, gs, ocells,
-                                                          d, dg, orient_only);
-  else if (!gen_dp_lean(vs.n, yp))
-    k_dp<false, false, false><<<grid, kDpThreads, sm, s>>>(vs, tb, ps, base, nsub, yp, gs, ocells,
-                                                           d, dg, orient_only);
-  else
-    k_dp<false, false, true><<<grid, kDpThreads, sm, s>>>(vs, tb, ps, base, nsub, yp, gs, ocells,
-                                                          d, dg, orient_only);
+  int launches = 0;
+  // ---- partitions + F(t,2): one launch per run of one variant, y-major
+  for (int gi = 0; gi < ny;) {
+    const int v = pf_variant(n, yps[gi]);
+    int gj = gi + 1;
+    while (gj < ny && pf_variant(n, yps[gj]) == v) ++gj;
+    size_t sm = 0;
+    for (int q = gi; q < gj; ++q) sm = std::max(sm, gen_pf_smem(n, yps[q]));
+    const unsigned blocks = (unsigned)(nsub * (gj - gi));
+#define PF_LAUNCH(T, PG, CG) \
+  k_part_f2<T, PG, CG><<<blocks, T, sm, s0>>>(vs, tb, ps, base, g, gi, ocells, d, dg, orient_only, counters)
+    switch (v) {
+      case kPfGlobalTables: PF_LAUNCH(256, true, true); break;
+      case kPfGlobalPts: PF_LAUNCH(256, true, false); break;
+      case kPf256: PF_LAUNCH(256, false, false); break;
+      default: PF_LAUNCH(128, false, false); break;
+    }
+#undef PF_LAUNCH
+    ++launches;
+    gi = gj;
+  }
+  // ---- levels >= 3: the k_dp runs and the warp path, each on its own lane
+  const std::vector<DpRun> runs = dp_runs(n, yps, ny, nsub);
+  int wlo = ny, whi = -1;
+  size_t per_warp = 0;
+  for (int gi = 0; gi < ny; ++gi)
+    if (warp_ok(yps[gi])) {
+      wlo = std::min(wlo, gi);
+      whi = std::max(whi, gi);
+      per_warp = std::max(per_warp, warp_per_warp(yps[gi]));
+    }
+  if (runs.empty() && whi < wlo) return launches;
+  // the warp path on the side lane (its items are disjoint from k_dp's), the
+  // k_dp runs in ascending y on the main lane
+  cudaStream_t sw = s0;
+  if (whi >= wlo && side) {
+    cudaEventRecord(ev[0], s0);
+    cudaStreamWaitEvent(side, ev[0], 0);
+    sw = side;
+  }
+  if (whi >= wlo) {
+    const int warps = kWarpThreads / 32;
+    const size_t sm = per_warp * warps;
+    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / (sm + 1024)));
+    const int grid = (int)std::max<long long>(
+        1, std::min<long long>((nsub * (whi - wlo + 1) + warps - 1) / warps, (long long)sm_count() * per_sm));
+    k_dp_warp<<<grid, kWarpThreads, sm, sw>>>(vs, tb, ps, base, g, wlo, whi - wlo + 1, (int)per_warp,
+                                              ocells, d, dg, orient_only);
+    ++launches;
+  }
+  char* fp = reinterpret_cast<char*>(fslots);
+  for (const DpRun& r : runs) {
+    double* fs = reinterpret_cast<double*>(fp);
+    fp += al16(8 * r.fslot_doubles * (size_t)r.grid);
+#define DP_LAUNCH(GT, RG, LN)                                                                 \
+  k_dp<GT, RG, LN><<<r.grid, kDpThreads, r.smem, s0>>>(vs, tb, ps, base, g, r.gi0, r.count, fs, \
+                                                        r.fslot_doubles, ocells, d, dg, orient_only)
+    switch (r.variant) {
+      case kDpGlobalTables: DP_LAUNCH(true, true, false); break;
+      case kDpRing: DP_LAUNCH(false, true, false); break;
+      case kDpWide: DP_LAUNCH(false, false, false); break;
+      default: DP_LAUNCH(false, false, true); break;
+    }
+#undef DP_LAUNCH
+    ++launches;
+  }
+  if (sw != s0) {
+    cudaEventRecord(ev[1], sw);
+    cudaStreamWaitEvent(s0, ev[1], 0);
+  }
+  return launches;
+}
+
+size_t div_table_doubles(int n) { return (size_t)(n + 1) * (n + 2) / 2; }
+
+void launch_build_div(double* div, int n, cudaStream_t s) {
+  const size_t total = div_table_doubles(n);
+  const unsigned blocks = (unsigned)std::min<size_t>(4096, (total + 255) / 256);
+  k_build_div<<<blocks, 256, 0, s>>>(div, n);
 }
 
 cudaError_t init_general_attributes(int device) {

@@ -140,16 +140,18 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
                        StatsOut out, double* o_cells, unsigned long long* counters,
                        cudaStream_t s);
 
-// General tier (mine_general.cu): k_part_f2 + persistent tiled k_dp per y.
-struct GenScratch {
+// General tier (mine_general.cu).  One launch GROUP covers many row targets
+// y at once: k_part_f2 over every (y, subproblem) of the group (y-major, so
+// the heaviest y = 2 blocks start first), then the persistent DP kernels pull
+// subproblems y by y in ascending y -- a cost-sorted queue, y = 2 carrying
+// ~(B/y)^3 of the work -- from per-y lists the partition kernel filled
+// (k <= kSmallK: k_dp_warp, else k_dp).  A call runs one group per chunk of
+// pairs unless the scratch of all y's would not fit (c4), then several.
+struct GenScratch {  // the device view of one y's scratch (built per item)
   int* desc = nullptr;        // nsub x int4 {k, rows, raw k, l_max}
   int* cb = nullptr;          // nsub x (kc+1) clump boundaries
   int* cum = nullptr;         // nsub x cum_stride cumulative counts, row-major [r][j]
   double* f2 = nullptr;       // nsub x (kc+1) F(t,2)
-  double* fslots = nullptr;   // grid x (kc+1) x (x_max-1) F tables (when not in smem)
-  unsigned long long* queue = nullptr;  // [0] k_dp queue, [1] k_dp_warp queue,
-                                        // [2] small-list length, [3] big-list length
-  long long* lists = nullptr; // [0, nsub): small subproblems, [nsub, 2 nsub): big ones
   long long nsub = 0;
   int kc = 0;                 // min(n, k_hat)
   size_t cum_stride = 0;      // y * (kc+1)
@@ -157,27 +159,49 @@ struct GenScratch {
   unsigned char* pts = nullptr;  // nsub x gen_pts_bytes per-point arrays (large n), or null
   int tables_global = 0;      // cb / cum used in place from this scratch (c B too large)
 };
+// One row target of a group (host-built, copied to the device).
+struct GenY {
+  YParams yp;
+  int kc, small_ok, tables_global, pad;
+  unsigned long long cum_stride;
+  int* desc;
+  int* cb;
+  int* cum;
+  double* f2;
+  unsigned char* pts;
+  long long* small_list;  // [nsub] subproblems with k <= kSmallK (when small_ok)
+  long long* big_list;    // [nsub] the others needing levels >= 3
+};
+struct GenGroup {
+  const GenY* ys = nullptr;      // device [ny]
+  int ny = 0;
+  long long nsub = 0;            // subproblems per y (2 per pair, 1 for one orientation)
+  // [gi]: small count, [ny + gi]: big count, [2 ny + gi]: k_dp ticket,
+  // [3 ny + gi]: k_dp_warp ticket
+  unsigned long long* cnt = nullptr;
+};
 constexpr int kSmallK = 64;   // subproblems with k <= kSmallK take the warp path
-size_t gen_warp_smem_per_warp(const YParams& yp);
-void launch_dp_warp(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
-                    long long npairs, const YParams& yp, const GenScratch& gs, double* ocells,
-                    const SubDebug* dbg, int orient_only, cudaStream_t s);
 int gen_kc(int n, const YParams& yp);
-size_t gen_scratch_per_sub(int n, const YParams& yp);
+size_t gen_scratch_per_sub(int n, const YParams& yp);  // incl. list entries
 size_t gen_pts_bytes(int n, const YParams& yp);  // 0: the point arrays fit on chip
 bool gen_tables_global(int n, const YParams& yp);
 size_t gen_pf_smem(int n, const YParams& yp);
 size_t gen_dp_smem(int n, const YParams& yp);
-bool gen_dp_f_in_smem(int n, const YParams& yp);
 size_t gen_fslot_bytes(int n, const YParams& yp);
-int gen_dp_grid(int n, const YParams& yp);
-void launch_part_f2(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
-                    long long npairs, const YParams& yp, const GenScratch& gs, double* ocells,
-                    const SubDebug* dbg, int orient_only, unsigned long long* counters,
-                    cudaStream_t s);
-void launch_dp(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
-               long long npairs, const YParams& yp, const GenScratch& gs, double* ocells,
-               const SubDebug* dbg, int orient_only, cudaStream_t s);
+// Device memory one group needs besides its scratch: the F slots of its DP
+// launches (k_dp CTAs keep F in an HBM slot each).
+size_t gen_group_fslot_bytes(int n, const YParams* yps, int ny, long long nsub);
+// Runs the whole general tier for `yps` over pairs [base, base + npairs) of
+// ps: writes both orientations' cells of every y into ocells.  scratch:
+// >= nsub * sum gen_scratch_per_sub; d_ys: >= ny GenY; d_cnt: >= 4 ny
+// counters; fslots: gen_group_fslot_bytes.  Everything runs on s0 except the
+// warp path, which runs on `side` (if non-null) forked / joined with ev[0],
+// ev[1].  Returns the launch count.
+int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
+                  long long npairs, const YParams* yps, int ny, void* scratch, GenY* d_ys,
+                  unsigned long long* d_cnt, double* fslots, double* ocells, const SubDebug* dbg,
+                  int orient_only, unsigned long long* counters, cudaStream_t s0, cudaStream_t side,
+                  cudaEvent_t* ev);
 cudaError_t init_general_attributes(int device);
 size_t div_table_doubles(int n);
 void launch_build_div(double* div, int n, cudaStream_t s);

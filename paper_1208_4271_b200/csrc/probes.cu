@@ -115,12 +115,15 @@ __global__ void k_dcand(double* out, int iters, double a, double w) {
   double f[kChains], m[kChains];
 #pragma unroll
   for (int c = 0; c < kChains; ++c) f[c] = -(threadIdx.x * 1e-3 + c), m[c] = -1e300;
+  const long long abits = __double_as_longlong(a);
   for (int i = 0; i < iters; ++i) {
+    // the multiplier changes every iteration by an integer op (ALU pipe), so
+    // nothing is loop-invariant and the FP64 pipe sees only the candidate ops
+    const double ai = __longlong_as_double(abits ^ (long long)(i & 7));
 #pragma unroll
     for (int c = 0; c < kChains; ++c) {
-      const double v = __dsub_rn(__dmul_rn(a, f[c]), w);
+      const double v = __dsub_rn(__dmul_rn(ai, f[c]), w);
       m[c] = m[c] < v ? v : m[c];
-      f[c] = __dadd_rn(f[c], w);  // keeps the operands live (not counted as a candidate op)
     }
   }
   double s = 0;
@@ -186,8 +189,8 @@ extern "C" int mine_b200_check_quotients(int device, int nmax, unsigned long lon
 
 // Extra roofline denominators for the general tier: random 8-byte L2 gathers
 // per second from a `table_bytes` table, and exact DP candidates per second
-// (k_dcand counts DMUL + DADD + DSETP per candidate; its keep-alive DADD is
-// issued too, so this is a lower bound on the pipe's candidate rate).
+// (k_dcand: DMUL + DADD + DSETP + two selects per candidate, as the DP's
+// inner loop issues them).
 extern "C" int mine_b200_probe_general(int device, double table_bytes, double* l2_gathers_per_s,
                                        double* candidates_per_s) {
   if (cudaSetDevice(device) != cudaSuccess) return -1;
