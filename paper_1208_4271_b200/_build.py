@@ -39,7 +39,19 @@ def _run(cmd: list[str]) -> None:
     subprocess.run(cmd, check=True)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+CHECKED_LIB = os.path.join(PKG, "libmine_b200_checked.so")
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """checked=True: the bounds-checked variant (device asserts, -DMB_BOUNDS_CHECK)
+    as libmine_b200_checked.so, objects under build/checked (load it with
+    MINE_B200_LIB); the substitute for compute-sanitizer, closed on the pool."""
+    if checked:
+        return _build_into(os.path.join(BUILD, "checked"), CHECKED_LIB, ["-DMB_BOUNDS_CHECK"], force, verbose)
+    return _build_into(BUILD, LIB, [], force, verbose, probes=True)
+
+
+def _build_into(BUILD: str, LIB: str, defs: list, force: bool, verbose: bool, probes: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     hdrs = [os.path.normpath(os.path.join(CSRC, h)) for h in HEADERS]
     objs = []
@@ -47,7 +59,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         if force or not _newer(o, [s] + hdrs):
-            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
+            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", *defs,
                    "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-c", s, "-o", o]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
@@ -63,7 +75,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if force or not _newer(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lpthread"])
     probe_src = os.path.join(CSRC, "probes.cu")
-    if force or not _newer(PROBES, [probe_src] + [os.path.normpath(os.path.join(CSRC, h)) for h in HEADERS]):
+    if probes and (force or not _newer(PROBES, [probe_src] + [os.path.normpath(os.path.join(CSRC, h)) for h in HEADERS])):
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
               "-cudart", "static", "-o", PROBES, probe_src])
     return LIB
@@ -71,4 +83,4 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 if __name__ == "__main__":
     import sys
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

@@ -8,6 +8,17 @@
 
 #include "mine_kernels.h"
 
+// Bounds-checked build (MB_BOUNDS_CHECK, _build.build(checked=True) ->
+// libmine_b200_checked.so): device asserts on the scratch / slot / layout
+// indexing of the general tier, the substitute for compute-sanitizer (closed
+// on this GPU pool).  A failed check traps the kernel and the call fails.
+#ifdef MB_BOUNDS_CHECK
+#include <cassert>
+#define MB_CHECK(cond) assert(cond)
+#else
+#define MB_CHECK(cond) ((void)0)
+#endif
+
 namespace mb200 {
 
 constexpr double kLowest = -DBL_MAX;  // std::numeric_limits<double>::lowest()

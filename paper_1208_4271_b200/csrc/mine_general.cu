@@ -126,8 +126,11 @@ __device__ void write_cells(const Tables& tb, double* ocells, long long pl, int 
 
 // ---------------------------------------------------------------------------
 // Grid: nsub x (the group's y's gi0 .. gi0 + gridDim.x / nsub - 1), y-major.
+#ifndef PF_MINB_THREADS
+#define PF_MINB_THREADS 2048  // resident threads per SM the register budget is set for
+#endif
 template <int kPfThreads, bool kPtsGlobal, bool kCumGlobal>
-__global__ void __launch_bounds__(kPfThreads, 2048 / kPfThreads) k_part_f2(VarSet vs, Tables tb, PairSpace ps,
+__global__ void __launch_bounds__(kPfThreads, PF_MINB_THREADS / kPfThreads) k_part_f2(VarSet vs, Tables tb, PairSpace ps,
                                                         long long base, GenGroup grp, int gi0,
                                                         double* __restrict__ ocells, SubDebug dbg,
                                                         int has_dbg, int orient_only,
@@ -259,6 +262,8 @@ __global__ void __launch_bounds__(kPfThreads, 2048 / kPfThreads) k_part_f2(VarSe
   __syncthreads();
 
   const int l_max = min(x_max, k);
+  MB_CHECK(k >= 1 && k <= kc && kraw <= n && rows >= 1 && rows <= y && sub < grp.nsub);
+  MB_CHECK(kCumGlobal || L.total <= 227 * 1024);
   if (counters && tid == 0) {
     unsigned long long w[kNumCounters] = {};
     subproblem_work(rows, k, x_max, n, w);
@@ -284,10 +289,15 @@ __global__ void __launch_bounds__(kPfThreads, 2048 / kPfThreads) k_part_f2(VarSe
       d.z = kraw;
       d.w = l_max;
       reinterpret_cast<int4*>(gs.desc)[sub] = d;
-      if (gs.small_ok && k <= kSmallK)
-        GY.small_list[atomicAdd(grp.cnt + gi, 1ull)] = sub;
-      else
-        GY.big_list[atomicAdd(grp.cnt + grp.ny + gi, 1ull)] = sub;
+      if (gs.small_ok && k <= kSmallK) {
+        const unsigned long long q = atomicAdd(grp.cnt + gi, 1ull);
+        MB_CHECK(q < (unsigned long long)grp.nsub);
+        GY.small_list[q] = sub;
+      } else {
+        const unsigned long long q = atomicAdd(grp.cnt + grp.ny + gi, 1ull);
+        MB_CHECK(q < (unsigned long long)grp.nsub);
+        GY.big_list[q] = sub;
+      }
     }
     int* gcb = gs.cb + (size_t)sub * (kc + 1);
     int* gcum = gs.cum + (size_t)sub * gs.cum_stride;
@@ -307,42 +317,61 @@ __global__ void __launch_bounds__(kPfThreads, 2048 / kPfThreads) k_part_f2(VarSe
   // every t is independent; warps over t, lanes over s, all p*log(p) terms
   // from row c_t of the table.
   double* gf2 = gs.f2 + (size_t)sub * (kc + 1);
+  // max over s in [1, t) of one t's candidates, by the lanes hl = 0 .. W-1
+  // of a W-lane segment (W = 32: a warp; W = 16: a half-warp)
+  auto f2_best = [&](int t, int hl, int W) {
+    const int ct = cb[t];
+    const double* plt = tb.pl + tri(ct);
+    double best = kLowest;
+    if (rows == 2) {
+      // two rows (y = 2, the heaviest level): all six gathers of a
+      // candidate are issued before its adds; unsigned offsets from the
+      // row base (one IMAD.WIDE.U32 per address)
+      const unsigned uct = ct, ct0 = cum[t], ct1 = cum[kk + t];
+      for (int s = 1 + hl; s < t; s += W) {
+        const unsigned cs = cb[s], a0 = cum[s], a1 = cum[kk + s];
+        const double p0 = __ldg(plt + cs), p1 = __ldg(plt + (uct - cs));
+        const double j0 = __ldg(plt + a0), j1 = __ldg(plt + a1);
+        const double j2 = __ldg(plt + (ct0 - a0)), j3 = __ldg(plt + (ct1 - a1));
+        const double acc2 = __dadd_rn(p0, p1);
+        const double accj = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(0.0, j0), j1), j2), j3);
+        best = dmax(best, __dsub_rn(-acc2, -accj));
+      }
+    } else {
+      const unsigned uct = ct;
+      for (int s = 1 + hl; s < t; s += W) {
+        const unsigned cs = cb[s];
+        const double acc2 = __dadd_rn(__ldg(plt + cs), __ldg(plt + (uct - cs)));
+        double accj = 0.0;
+        for (int r = 0; r < rows; ++r) accj = __dadd_rn(accj, __ldg(plt + (unsigned)cum[r * kk + s]));
+        for (int r = 0; r < rows; ++r)
+          accj = __dadd_rn(accj, __ldg(plt + ((unsigned)cum[r * kk + t] - (unsigned)cum[r * kk + s])));
+        best = dmax(best, __dsub_rn(-acc2, -accj));
+      }
+    }
+    return best;
+  };
+  auto f2_store = [&](int t, double best) {
+    if (l_max >= 3) gf2[t] = best;
+    if (t == k) dmisc[0] = best;
+  };
   if (k >= 2) {
+    constexpr int nw = kPfThreads / 32;
     const int t_lo = l_max >= 3 ? 2 : k;
-    for (int t = t_lo + warp; t <= k; t += (kPfThreads / 32)) {
-      const int ct = cb[t];
-      const double* plt = tb.pl + tri(ct);
-      double best = kLowest;
-      if (rows == 2) {
-        // two rows (y = 2, the heaviest level): all six gathers of a
-        // candidate are issued before its adds
-        const int ct0 = cum[t], ct1 = cum[kk + t];
-        for (int s = 1 + lane; s < t; s += 32) {
-          const int cs = cb[s], a0 = cum[s], a1 = cum[kk + s];
-          const double p0 = __ldg(plt + cs), p1 = __ldg(plt + (ct - cs));
-          const double j0 = __ldg(plt + a0), j1 = __ldg(plt + a1);
-          const double j2 = __ldg(plt + (ct0 - a0)), j3 = __ldg(plt + (ct1 - a1));
-          const double acc2 = __dadd_rn(p0, p1);
-          const double accj = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(0.0, j0), j1), j2), j3);
-          best = dmax(best, __dsub_rn(-acc2, -accj));
-        }
-      } else {
-        for (int s = 1 + lane; s < t; s += 32) {
-          const int cs = cb[s];
-          double acc2 = __ldg(plt + cs);
-          acc2 = __dadd_rn(acc2, __ldg(plt + (ct - cs)));
-          double accj = 0.0;
-          for (int r = 0; r < rows; ++r) accj = __dadd_rn(accj, __ldg(plt + cum[r * kk + s]));
-          for (int r = 0; r < rows; ++r)
-            accj = __dadd_rn(accj, __ldg(plt + (cum[r * kk + t] - cum[r * kk + s])));
-          best = dmax(best, __dsub_rn(-acc2, -accj));
-        }
-      }
-      best = warp_max(best);
-      if (lane == 0) {
-        if (l_max >= 3) gf2[t] = best;
-        if (t == k) dmisc[0] = best;
-      }
+    // t <= 17 (at most 16 candidates): two t's per warp, a half-warp each --
+    // small-k subproblems (ties, large y) would leave most lanes idle
+    const int t_mid = min(k, 17);
+    for (int t2 = t_lo + 2 * warp; t2 <= t_mid; t2 += 2 * nw) {
+      const int half = lane >> 4, t = t2 + half;
+      const bool ok = t <= t_mid;
+      double best = ok ? f2_best(t, lane & 15, 16) : kLowest;
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) best = dmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+      if (ok && (lane & 15) == 0) f2_store(t, best);
+    }
+    for (int t = max(t_lo, t_mid + 1) + warp; t <= k; t += nw) {
+      const double best = warp_max(f2_best(t, lane, 32));
+      if (lane == 0) f2_store(t, best);
     }
   }
   __syncthreads();
@@ -457,29 +486,30 @@ __device__ __forceinline__ void span_terms(const Tables& tb, const int* cb, cons
       acch[e] = 0.0;
     }
     int r = 0;
+    // unsigned offsets from the row base (one IMAD.WIDE.U32 per address)
 #if KDP_SPAN2
     // two rows per step: all eight gathers are issued before the adds (each
     // sum still runs in row order)
     for (; r + 2 <= rows; r += 2) {
-      const int ctr0 = cum[r * kk + t], ctr1 = cum[(r + 1) * kk + t];
+      const unsigned ctr0 = cum[r * kk + t], ctr1 = cum[(r + 1) * kk + t];
       double v[2][4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int s = s0 + base + w0 + e * nw;
-        v[0][e] = ok[e] ? __ldg(plm[e] + (ctr0 - cum[r * kk + s])) : 0.0;
-        v[1][e] = ok[e] ? __ldg(plm[e] + (ctr1 - cum[(r + 1) * kk + s])) : 0.0;
+        v[0][e] = ok[e] ? __ldg(plm[e] + (ctr0 - (unsigned)cum[r * kk + s])) : 0.0;
+        v[1][e] = ok[e] ? __ldg(plm[e] + (ctr1 - (unsigned)cum[(r + 1) * kk + s])) : 0.0;
       }
 #pragma unroll
       for (int e = 0; e < 4; ++e) acch[e] = __dadd_rn(__dadd_rn(acch[e], v[0][e]), v[1][e]);
     }
 #endif
     for (; r < rows; ++r) {
-      const int ctr = cum[r * kk + t];
+      const unsigned ctr = cum[r * kk + t];
       double v[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int s = s0 + base + w0 + e * nw;
-        v[e] = ok[e] ? __ldg(plm[e] + (ctr - cum[r * kk + s])) : 0.0;
+        v[e] = ok[e] ? __ldg(plm[e] + (ctr - (unsigned)cum[r * kk + s])) : 0.0;
       }
 #pragma unroll
       for (int e = 0; e < 4; ++e) acch[e] = __dadd_rn(acch[e], v[e]);
@@ -585,6 +615,9 @@ __global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : 3) k_dp(V
     const int4 d = reinterpret_cast<const int4*>(gs.desc)[sub];
     const int k = d.x, rows = d.y, l_max = d.w, kk = k + 1;
     if (l_max < 3) continue;  // finished by k_part_f2
+    MB_CHECK(k <= kc && rows <= y && l_max <= x_max && sub < grp.nsub);
+    MB_CHECK((size_t)(kc + 1) * RW + LW <= fslot_stride);  // F rows + the fk row inside this CTA's slot
+    MB_CHECK(L.total <= 227 * 1024);
     const long long pl = base + sub / norient;
     const int orient = orient_only >= 0 ? orient_only : (int)(sub % 2);
     {
@@ -607,6 +640,9 @@ __global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : 3) k_dp(V
     // (t0 + 2p, t0 + 2p + 1) x a group of 4 consecutive levels, so each s
     // costs one 16-byte load for both A, one for both W and two for four F
     // values, feeding 8 independent max chains.  (T/2) * groups <= 256.
+    // (Splitting a chunk's rows over several owner sets when the level tile
+    // is narrow was measured: no gain, and the larger hand-over region cost
+    // L1 capacity -- c3 -13%.)
     for (int l0 = 3; l0 <= l_max; l0 += 64) {
       const int l1 = min(l0 + 63, l_max), nl = l1 - l0 + 1;
       const int ng = (nl + 3) >> 2;
@@ -797,6 +833,7 @@ __global__ void __launch_bounds__(kWarpThreads) k_dp_warp(VarSet vs, Tables tb, 
     const GenScratch gs = scratch_of(GY, grp.nsub);
     const int y = yp.y, x_max = yp.x_max, LW = x_max - 1, kc = gs.kc;
     const WarpLayout L = warp_layout(y, x_max);
+    MB_CHECK(L.per_warp <= (size_t)per_warp);
     double* F = reinterpret_cast<double*>(wb + L.F);
     double* A = reinterpret_cast<double*>(wb + L.A);
     double* W = reinterpret_cast<double*>(wb + L.W);
@@ -804,6 +841,7 @@ __global__ void __launch_bounds__(kWarpThreads) k_dp_warp(VarSet vs, Tables tb, 
     int* cum = reinterpret_cast<int*>(wb + L.cum);
     const int4 d = reinterpret_cast<const int4*>(gs.desc)[sub];
     const int k = d.x, rows = d.y, l_max = d.w, kk = k + 1;
+    MB_CHECK(k <= kSmallK && rows <= y && l_max <= x_max && sub < grp.nsub);
     {
       const int* gcb = gs.cb + (size_t)sub * (kc + 1);
       const int* gcum = gs.cum + (size_t)sub * gs.cum_stride;
@@ -823,11 +861,12 @@ __global__ void __launch_bounds__(kWarpThreads) k_dp_warp(VarSet vs, Tables tb, 
         double acch = 0.0;
         int r = 0;
         for (; r + 2 <= rows; r += 2) {  // two gathers in flight, added in row order
-          const double v0 = __ldg(plm + (cum[r * kk + t] - cum[r * kk + s]));
-          const double v1 = __ldg(plm + (cum[(r + 1) * kk + t] - cum[(r + 1) * kk + s]));
+          const double v0 = __ldg(plm + ((unsigned)cum[r * kk + t] - (unsigned)cum[r * kk + s]));
+          const double v1 = __ldg(plm + ((unsigned)cum[(r + 1) * kk + t] - (unsigned)cum[(r + 1) * kk + s]));
           acch = __dadd_rn(__dadd_rn(acch, v0), v1);
         }
-        if (r < rows) acch = __dadd_rn(acch, __ldg(plm + (cum[r * kk + t] - cum[r * kk + s])));
+        if (r < rows)
+          acch = __dadd_rn(acch, __ldg(plm + ((unsigned)cum[r * kk + t] - (unsigned)cum[r * kk + s])));
         double a, q;
         if (tb.div) {
           const double* dr = tb.div + tri(ct);
@@ -891,9 +930,16 @@ __global__ void k_build_div(double* div, int n) {
 // ---------------------------------------------------------------------------
 int gen_kc(int n, const YParams& yp) { return std::min(n, yp.k_hat); }
 
+// cb / cum are read in place (L1 / L2) instead of staged in k_dp's shared
+// memory when staging them would cost more than 48 KB -- c B large, e.g. c4
+// (7.5k clumps at y = 2, ~60 KB of cumulative counts at every y): the smaller
+// footprint lets 3 CTAs share an SM instead of 1 (c4 +14%).
 bool gen_tables_global(int n, const YParams& yp) {
   static const bool force = std::getenv("MINE_B200_DP_GLOBAL") != nullptr;
-  return force || dp_layout(yp.y, gen_kc(n, yp), yp.x_max, false, false).total > 200 * 1024;
+  const size_t kc1 = (size_t)gen_kc(n, yp) + 1;
+  const size_t staged = al16(sizeof(int) * kc1) + al16(sizeof(int) * (size_t)yp.y * kc1);
+  return force || staged > 48 * 1024 ||
+         dp_layout(yp.y, gen_kc(n, yp), yp.x_max, false, false).total > 200 * 1024;
 }
 
 bool gen_pts_global(int n, const YParams& yp) {
@@ -1149,6 +1195,24 @@ cudaError_t init_general_attributes(int device) {
     e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              optin - (int)fa.sharedSizeBytes);
     if (e != cudaSuccess) return e;
+  }
+  // Preferred shared-memory carveout of the wide / ring / global-table k_dp
+  // (large c B, e.g. c4): 58% (132 KB) leaves the rest of the SM's 256 KB as
+  // L1, where the span terms' p*log(p) rows and the in-place cb / cum hit
+  // (c4 +11% over the default; MINE_B200_DP_CARVEOUT overrides, and also
+  // applies it to the lean variant, which is fastest at the default).
+  {
+    const char* cv = std::getenv("MINE_B200_DP_CARVEOUT");
+    const int pct = cv ? std::atoi(cv) : 58;
+    const void* dps[] = {reinterpret_cast<const void*>(k_dp<false, false, false>),
+                         reinterpret_cast<const void*>(k_dp<false, true, false>),
+                         reinterpret_cast<const void*>(k_dp<true, true, false>),
+                         cv ? reinterpret_cast<const void*>(k_dp<false, false, true>) : nullptr};
+    for (const void* f : dps) {
+      if (!f) continue;
+      e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+      if (e != cudaSuccess) return e;
+    }
   }
   return cudaSuccess;
 }

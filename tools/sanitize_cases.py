@@ -1,6 +1,12 @@
 #!/usr/bin/env python3
-"""Small cases of every kernel family for compute-sanitizer (one tool per
-gpurun call: memcheck, racecheck, synccheck):
+"""Small cases of every kernel family, run against the bounds-checked
+library (device asserts on the general tier's scratch / slot / layout
+indexing; compute-sanitizer is closed on this GPU pool):
+
+    MINE_B200_LIB=paper_1208_4271_b200/libmine_b200_checked.so python tools/sanitize_cases.py
+
+(tests/test_bounds_checked_gpu.py).  Where compute-sanitizer is available the
+same script runs under it, one tool per process:
 
     compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize_cases.py
 
