@@ -24,6 +24,15 @@ namespace mb200 {
 constexpr double kLowest = -DBL_MAX;  // std::numeric_limits<double>::lowest()
 
 __device__ __forceinline__ unsigned tri(unsigned m) { return m * (m + 1u) / 2u; }
+// start of row m of the half table H2 (rows of floor(m/2) + 1 entries)
+__host__ __device__ __forceinline__ unsigned h2_off(unsigned m) {
+  const unsigned q = m >> 1;
+  return (m & 1u) ? (q + 1u) * (q + 1u) : q * (q + 1u);
+}
+// H2(m, w) = pl(m, w) + pl(m, m - w): a two-row span's entropy sum, one gather
+__device__ __forceinline__ double h2_at(const double* h2, unsigned m, unsigned w) {
+  return __ldg(h2 + h2_off(m) + min(w, m - w));
+}
 
 // std::max / std::min argument order (libstdc++): max(a,b) = a < b ? b : a.
 __device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }

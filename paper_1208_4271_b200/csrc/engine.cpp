@@ -83,8 +83,8 @@ int cell_count(int B) {
 // Host-built constant tables, cached per (n, B) on a context.
 struct TableSet {
   int n = -1, B = -1, ncell = 0;
-  DevBuf pl, logi, log2i, cell_off, cell_tr, cell_xy, cell_edge, cell_cmp, div;
-  bool has_div = false;
+  DevBuf pl, logi, log2i, cell_off, cell_tr, cell_xy, cell_edge, cell_cmp, div, h2;
+  bool has_div = false, has_h2 = false;
   std::vector<int> h_off;
 
   void build(int n_, int B_, cudaStream_t s) {
@@ -157,6 +157,13 @@ struct TableSet {
       launch_build_div(static_cast<double*>(div.ensure(sizeof(double) * div_table_doubles(n_))), n_, s);
       CK(cudaGetLastError());
     }
+    // the two-row span table, derived on the device from pl (same sums)
+    has_h2 = n_ <= kH2MaxN && !std::getenv("MINE_B200_NO_H2");
+    if (has_h2) {
+      launch_build_h2(pl.as<double>(), static_cast<double*>(h2.ensure(sizeof(double) * h2_table_doubles(n_))),
+                      n_, s);
+      CK(cudaGetLastError());
+    }
     CK(cudaStreamSynchronize(s));  // host vectors go out of scope
     n = n_;
     B = B_;
@@ -173,6 +180,7 @@ struct TableSet {
     t.cell_edge = cell_edge.as<uint8_t>();
     t.cell_cmp = cell_cmp.as<int8_t>();
     t.div = has_div ? div.as<double>() : nullptr;
+    t.h2 = has_h2 ? h2.as<double>() : nullptr;
     t.n = n;
     t.B = B;
     t.ncell = ncell;
@@ -189,7 +197,7 @@ struct mine_b200_ctx {
   std::mutex mu;
   TableSet tables;
   DevBuf vals, perm, runid, runstart, nruns, q, yhat, hq, lw, rsmask;
-  DevBuf ocells, stats, flag, idx, counters, memo, memo_vals, memo_val, rec, dx, sxx, micscr, sortscr;
+  DevBuf ocells, stats, flag, idx, counters, memo, memo_vals, memo_val, rec, dx, sxx, micscr, sortscr, mstage;
   // general tier: one launch group per chunk of pairs (or per y-group when
   // the scratch of all y's would not fit): scratch regions, the group's y
   // table and counters, the DP launches' F slots; the DP launches of
@@ -269,6 +277,16 @@ cudaEvent_t ctx_event(mine_b200_ctx* ctx, size_t i) {
     ctx->events.push_back(e);
   }
   return ctx->events[i];
+}
+
+// The memo tier's index-order output staging (MINE_B200_MEMO_STAGE=0: off,
+// the sorted batches then write their statistics scattered in place).
+bool memo_stage_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("MINE_B200_MEMO_STAGE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 // Device memory budget of the general tier's per-chunk scratch
@@ -609,8 +627,10 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
     pc.count = cn;
     if (memo) {
       launch_memo_pairs(vs, tb, ctx->memo.as<double>(), ctx->memo_val.as<double>(), ctx->memo_nval,
-                        pc, par->c,
-                        par->est, so, cells_dst, dcnt, s);
+                        pc, par->c, par->est, so, cells_dst, dcnt,
+                        memo_stage_on() ? static_cast<double*>(ctx->mstage.ensure(memo_stage_bytes()))
+                                        : nullptr,
+                        s);
       ++ctx->launches;
     } else if (tiny) {
       launch_tiny_pairs(vs, tb, pc, par->c, par->est, so, cells_dst, dcnt, s);

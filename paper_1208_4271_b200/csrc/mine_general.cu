@@ -330,10 +330,11 @@ __global__ void __launch_bounds__(kPfThreads, PF_MINB_THREADS / kPfThreads) k_pa
       const unsigned uct = ct, ct0 = cum[t], ct1 = cum[kk + t];
       for (int s = 1 + hl; s < t; s += W) {
         const unsigned cs = cb[s], a0 = cum[s], a1 = cum[kk + s];
-        const double p0 = __ldg(plt + cs), p1 = __ldg(plt + (uct - cs));
+        // H(P) = entropy of (c_s, c_t - c_s): pl + pl, or one H2 gather
+        const double acc2 = tb.h2 ? h2_at(tb.h2, uct, cs)
+                                  : __dadd_rn(__ldg(plt + cs), __ldg(plt + (uct - cs)));
         const double j0 = __ldg(plt + a0), j1 = __ldg(plt + a1);
         const double j2 = __ldg(plt + (ct0 - a0)), j3 = __ldg(plt + (ct1 - a1));
-        const double acc2 = __dadd_rn(p0, p1);
         const double accj = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(0.0, j0), j1), j2), j3);
         best = dmax(best, __dsub_rn(-acc2, -accj));
       }
@@ -486,6 +487,16 @@ __device__ __forceinline__ void span_terms(const Tables& tb, const int* cb, cons
       acch[e] = 0.0;
     }
     int r = 0;
+    if (rows == 2 && tb.h2) {
+      // two rows: the span's sum pl(m, w0) + pl(m, m - w0) is one H2 gather
+      const unsigned ct0 = cum[t];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int s = s0 + base + w0 + e * nw;
+        acch[e] = ok[e] ? h2_at(tb.h2, (unsigned)(ct - cs[e]), ct0 - (unsigned)cum[s]) : 0.0;
+      }
+      r = rows;
+    }
     // unsigned offsets from the row base (one IMAD.WIDE.U32 per address)
 #if KDP_SPAN2
     // two rows per step: all eight gathers are issued before the adds (each
@@ -860,6 +871,10 @@ __global__ void __launch_bounds__(kWarpThreads) k_dp_warp(VarSet vs, Tables tb, 
         const double* plm = tb.pl + tri(ct - cs);
         double acch = 0.0;
         int r = 0;
+        if (rows == 2 && tb.h2) {  // the two-row sum as one H2 gather
+          acch = h2_at(tb.h2, (unsigned)(ct - cs), (unsigned)cum[t] - (unsigned)cum[s]);
+          r = rows;
+        }
         for (; r + 2 <= rows; r += 2) {  // two gathers in flight, added in row order
           const double v0 = __ldg(plm + ((unsigned)cum[r * kk + t] - (unsigned)cum[r * kk + s]));
           const double v1 = __ldg(plm + ((unsigned)cum[(r + 1) * kk + t] - (unsigned)cum[(r + 1) * kk + s]));
@@ -925,7 +940,30 @@ __global__ void k_build_div(double* div, int n) {
   }
 }
 
+// H2(m, w) = pl(m, w) + pl(m, m - w) for w <= m/2: one thread per entry.
+__global__ void k_build_h2(const double* __restrict__ pl, double* __restrict__ h2, int n) {
+  const unsigned long long total = h2_off((unsigned)n + 1u);
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < total;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    // invert i = h2_off(m) + w: h2_off is increasing, ~ m^2 / 4
+    unsigned m = (unsigned)(2.0 * sqrt((double)i));
+    while (m > 0 && h2_off(m) > i) --m;
+    while (h2_off(m + 1u) <= i) ++m;
+    const unsigned w = (unsigned)(i - h2_off(m));
+    const double* row = pl + tri(m);
+    h2[i] = __dadd_rn(row[w], row[m - w]);
+  }
+}
+
 }  // namespace
+
+size_t h2_table_doubles(int n) { return h2_off((unsigned)n + 1u); }
+
+void launch_build_h2(const double* pl, double* h2, int n, cudaStream_t s) {
+  const size_t total = h2_table_doubles(n);
+  const unsigned blocks = (unsigned)std::min<size_t>(8192, (total + 255) / 256);
+  k_build_h2<<<blocks, 256, 0, s>>>(pl, h2, n);
+}
 
 // ---------------------------------------------------------------------------
 int gen_kc(int n, const YParams& yp) { return std::min(n, yp.k_hat); }

@@ -343,9 +343,15 @@ __device__ void tiny_subproblem(const TinyCtx& c, const uint32_t* m, int rows, u
 // Statistics of a B <= 7 matrix (cells 0:(2,2) 1:(3,2) 2:(2,3)) from the two
 // orientations' cells -- update_max merge (char_matrix.cpp:28-35), then
 // statistics.cpp:10-37 and the MIC_e / TIC extensions.
+// kStageStride: doubles per statistic in a memo CTA's staging slot (k_memo_pairs).
+constexpr int kStageStride = 8192;
+
+// slot: non-null -> the statistics go to this CTA's staging slot at index oi
+// (a sorted position), statistic q at q * kStageStride (k_memo_pairs copies
+// them to out in index order); null -> straight to out at oi.
 __device__ __forceinline__ void small_stats(const double (&o)[2][3], int ncell, int est,
                                             const double* lg2, const StatsOut& out,
-                                            long long oi, double* ocells) {
+                                            long long oi, double* ocells, double* slot = nullptr) {
   const int cxy[3] = {4, 6, 6};
   double M[3], E[3];
 #pragma unroll
@@ -369,6 +375,15 @@ __device__ __forceinline__ void small_stats(const double (&o)[2][3], int ncell, 
 #pragma unroll
   for (int i = 0; i < 3; ++i)
     if (i < ncell && M[i] == mic) best = min(best, cxy[i]);
+  if (slot) {
+    if (out.mic) slot[oi] = mic;
+    if (out.mas) slot[kStageStride + oi] = mas;
+    if (out.mev) slot[2 * kStageStride + oi] = mev;
+    if (out.mcn) slot[3 * kStageStride + oi] = lg2[best > 7 ? 0 : best];
+    if (out.mic_e) slot[4 * kStageStride + oi] = mice;
+    if (out.tic) slot[5 * kStageStride + oi] = tic;
+    return;
+  }
   if (out.mic) out.mic[oi] = mic;
   if (out.mas) out.mas[oi] = mas;
   if (out.mev) out.mev[oi] = mev;
@@ -1021,7 +1036,7 @@ __device__ __forceinline__ void memo_pair(const MemoCtx& c, const VarSet& vs, co
                                           int va, int vb, long long wl, bool swap,
                                           int kh2, int kh3, int est, const StatsOut& out, double* ocells,
                                           const double* lg, const double* lg2,
-                                          unsigned long long* wk, int* scr) {
+                                          unsigned long long* wk, int* scr, double* slot = nullptr) {
   const int n = c.n, B = tb.B;
   const int x2 = B / 2;  // 2 or 3
   const bool has_y3 = B >= 6;
@@ -1091,7 +1106,7 @@ __device__ __forceinline__ void memo_pair(const MemoCtx& c, const VarSet& vs, co
       o[1][i] = t[1][i];
     }
   }
-  small_stats(o, has_y3 ? 3 : 1, est, lg2, out, wl, ocells);
+  small_stats(o, has_y3 ? 3 : 1, est, lg2, out, wl, ocells, slot);
 }
 
 // sort buffers after the tables: 1024 bucket counts, then per pair of the
@@ -1114,7 +1129,8 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
                                                                int nval, const MemoLayout L,
                                                                PairSpace ps, double cpar, int est,
                                                                StatsOut out, double* ocells,
-                                                               unsigned long long* counters) {
+                                                               unsigned long long* counters,
+                                                               double* __restrict__ stage) {
   constexpr bool kSort = kSortBatch > 0;
   constexpr int sbatch = kSortBatch > 0 ? kSortBatch : 1024;
   extern __shared__ __align__(16) double msm[];
@@ -1197,16 +1213,47 @@ __global__ void __launch_bounds__(kMemoMaxThreads, 1) k_memo_pairs(VarSet vs, Ta
         const int kv = skey[e];
         const int pos = atomicAdd(&hist[kv & 0x3ff], 1);
         sidx[pos] = e | ((kv >> 15) << 16);
+        skey[e] = (uint16_t)pos;  // the key is consumed: now the inverse order
       }
       __syncthreads();
+      // With a staging slot (no cells requested), the statistics are written
+      // at their SORTED positions of this CTA's slot -- consecutive threads,
+      // consecutive addresses -- and copied to the pairs' own indices after
+      // the batch, whole sectors at a time: no partially written output
+      // sectors for L2 to fill from HBM (round 1: 58.6 MB of fills per c1
+      // launch).
+      double* slot = stage ? stage + (size_t)blockIdx.x * 6 * kStageStride : nullptr;
 #pragma unroll 1
       for (int pos = tid; pos < nb; pos += kMemoMaxThreads) {
         const int v = sidx[pos], e = v & 0xffff;
         const uint32_t pv = svar[e];
-        memo_pair<kCount, kT3C, kRegSlots>(c, vs, tb, (int)(pv & 0xffffu), (int)(pv >> 16), b0 + e,
-                                           (v >> 16) != 0, kh2, kh3, est, out, ocells, lg, lg2, wk, scr);
+        memo_pair<kCount, kT3C, kRegSlots>(c, vs, tb, (int)(pv & 0xffffu), (int)(pv >> 16),
+                                           slot ? pos : b0 + e, (v >> 16) != 0, kh2, kh3, est, out,
+                                           ocells, lg, lg2, wk, scr, slot);
       }
       __syncthreads();
+      if (slot) {
+        // the batch's statistics in index order: all loads first, then the
+        // coalesced stores (whole sectors)
+        constexpr int kPer = sbatch / kMemoMaxThreads;
+        double* const dst[6] = {out.mic, out.mas, out.mev, out.mcn, out.mic_e, out.tic};
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          if (!dst[q]) continue;
+          double v[kPer];
+#pragma unroll
+          for (int i = 0; i < kPer; ++i) {
+            const int e = tid + i * kMemoMaxThreads;
+            v[i] = e < nb ? __ldcg(slot + (size_t)q * kStageStride + skey[e]) : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < kPer; ++i) {
+            const int e = tid + i * kMemoMaxThreads;
+            if (e < nb) dst[q][b0 + e] = v[i];
+          }
+        }
+        __syncthreads();
+      }
     }
   } else {
     const long long stride = (long long)gridDim.x * blockDim.x;
@@ -1436,10 +1483,17 @@ void launch_pack_memo(const VarSet& vs, cudaStream_t s) {
   k_pack_memo<<<(vs.V + 127) / 128, 128, 0, s>>>(vs);
 }
 
+size_t memo_stage_bytes() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sizeof(double) * 6 * 8192 * (size_t)sms;
+}
+
 void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
                        const double* memo_val, int nval, const PairSpace& ps, double c, int est,
                        StatsOut out, double* o_cells, unsigned long long* counters,
-                       cudaStream_t s) {
+                       double* stage, cudaStream_t s) {
   if (ps.count <= 0) return;
   const size_t fixed = memo_smem_fixed(vs.n, nval);
   const size_t budget = 226 * 1024 - fixed;
@@ -1454,7 +1508,8 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
   const MemoLayout L = memo_layout(vs.n);
 #define MEMO_LAUNCH(CNT, T3C, RS, SORT)                                                        \
   k_memo_pairs<CNT, T3C, RS, SORT><<<blocks, threads, sm + (SORT ? memo_sort_bytes(SORT) : 0), s>>>( \
-      vs, tb, memo, memo_val, nval, L, ps, c, est, out, o_cells, CNT ? counters : nullptr)
+      vs, tb, memo, memo_val, nval, L, ps, c, est, out, o_cells, CNT ? counters : nullptr,  \
+      SORT && !o_cells ? stage : nullptr)
   // the compact 3-row table starts above n = 26: never with 23 slots.  The
   // sorted-batch order needs the register-staged variant (no scratch rows)
   // and pays off only with the y = 2 level loop (B >= 6: x_max = 3); the
@@ -1473,7 +1528,8 @@ void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
   }
 #define MEMO_LAUNCH_N(CNT, N)                                                              \
   k_memo_pairs<CNT, false, 23, 8192, N><<<blocks, threads, sm + memo_sort_bytes(8192), s>>>(   \
-      vs, tb, memo, memo_val, nval, L, ps, c, est, out, o_cells, CNT ? counters : nullptr)
+      vs, tb, memo, memo_val, nval, L, ps, c, est, out, o_cells, CNT ? counters : nullptr,  \
+      o_cells ? nullptr : stage)
   // n = 20..24 (the register-staged memo range with a y = 2 level loop, e.g.
   // the 23-sample Spellman-shaped c1): compiled for the exact n, so the mask
   // loops and row indices fold to constants (c1 +1%)

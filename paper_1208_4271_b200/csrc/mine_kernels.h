@@ -50,6 +50,11 @@ struct Tables {
   const uint8_t* cell_edge = nullptr;  // x == 2 || y == 2
   const int8_t* cell_cmp = nullptr;    // sign(x - y): which orientation feeds MIC_e
   const double* div = nullptr;    // w / m at tri(m) + w (exact IEEE quotients), n <= 4096 only
+  // two-row span entropy sums H2(m, w) = pl(m, w) + pl(m, m - w) (the
+  // reference's row-ordered sum of a two-row span, mutual_info.hpp:24-27, as
+  // one term; symmetric in w <-> m - w, so only w <= m/2 is stored, at
+  // h2_off(m) + min(w, m - w)); n <= kH2MaxN only, else null
+  const double* h2 = nullptr;
   int n = 0;
   int B = 0;
   int ncell = 0;
@@ -135,10 +140,14 @@ bool memo_fits(int n, int B, int nval);
 int launch_build_memo(const Tables& tb, double* memo, void* work, double* val, int n,
                       cudaStream_t s);
 void launch_pack_memo(const VarSet& vs, cudaStream_t s);
+// stage: memo_stage_bytes() of scratch (one 8192-pair slot of 6 statistics
+// per SM) through which sorted batches write their statistics in index order;
+// may be null (direct scattered writes).
+size_t memo_stage_bytes();
 void launch_memo_pairs(const VarSet& vs, const Tables& tb, const double* memo,
                        const double* memo_val, int nval, const PairSpace& ps, double c, int est,
                        StatsOut out, double* o_cells, unsigned long long* counters,
-                       cudaStream_t s);
+                       double* stage, cudaStream_t s);
 
 // General tier (mine_general.cu).  One launch GROUP covers many row targets
 // y at once: k_part_f2 over every (y, subproblem) of the group (y-major, so
@@ -205,6 +214,9 @@ int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long 
 cudaError_t init_general_attributes(int device);
 size_t div_table_doubles(int n);
 void launch_build_div(double* div, int n, cudaStream_t s);
+constexpr int kH2MaxN = 20000;
+size_t h2_table_doubles(int n);
+void launch_build_h2(const double* pl, double* h2, int n, cudaStream_t s);
 
 void launch_reduce(const Tables& tb, long long npairs, const double* ocells, int est,
                    StatsOut out, long long out_offset, cudaStream_t s);
