@@ -279,12 +279,18 @@ cudaEvent_t ctx_event(mine_b200_ctx* ctx, size_t i) {
   return ctx->events[i];
 }
 
-// The memo tier's index-order output staging (MINE_B200_MEMO_STAGE=0: off,
-// the sorted batches then write their statistics scattered in place).
+// The memo tier's index-order output staging, MINE_B200_MEMO_STAGE=1 (off
+// by default).  Measured on c1 (B200, 10-step bench): with staging the pair
+// kernel's DRAM traffic is 157.9 MB per launch (algorithmic 153.5 MB) but the
+// launch takes 1.477 ms; without it the sorted batches write their 8-byte
+// statistics scattered inside each batch's 64 KB window, L2 fills 58.6 MB of
+// partially written sectors from HBM (212.7 MB per launch, HBM at ~2% of its
+// peak) and the launch takes 1.425 ms.  The fills cost no time; the staging
+// epilogue does (3.6%).
 bool memo_stage_on() {
   static const bool on = [] {
     const char* e = std::getenv("MINE_B200_MEMO_STAGE");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }
@@ -578,7 +584,20 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   // per SM (the memo kernel deals whole batches), so no SM idles per chunk
   const long long chunk = small ? (dio ? count : std::min<long long>(count, 8192LL * ctx->sms))
                                : gen_chunk;
-  const long long nchunks = (count + chunk - 1) / chunk;
+  // Chunk schedule.  Host io of the small tiers starts with a quarter-size
+  // chunk, so the first device -> host copy (the e2e leg is PCIe-bound)
+  // starts after a quarter of a chunk's kernel time.
+  std::vector<std::pair<long long, long long>> sched;  // (offset, count)
+  {
+    long long c0 = 0;
+    if (small && !dio && count > chunk) {
+      const long long head = std::max<long long>(1, chunk / 4);
+      sched.push_back({0, head});
+      c0 = head;
+    }
+    for (; c0 < count; c0 += chunk) sched.push_back({c0, std::min(chunk, count - c0)});
+  }
+  const long long nchunks = (long long)sched.size();
   const int nslots = dio ? 1 : 2;  // double-buffered staging for host io
   double* stage = nullptr;
   const size_t stage_stats = kStats * (size_t)chunk;
@@ -595,8 +614,8 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   if (opts.ev_begin) CK(cudaEventRecord(static_cast<cudaEvent_t>(opts.ev_begin), s));
 
   for (long long ci = 0; ci < nchunks; ++ci) {
-    const long long c0 = ci * chunk;
-    const long long cn = std::min(chunk, count - c0);
+    const long long c0 = sched[ci].first;
+    const long long cn = sched[ci].second;
     const int slot = (int)(ci % nslots);
     StatsOut so;
     double* so_r = nullptr;   // pearson_r

@@ -536,3 +536,32 @@ def test_memo_sort_off_same_bits(tmp_path):
         subprocess.run([sys.executable, str(script), str(out)], env=env, check=True, timeout=600)
         outs.append(np.load(out))
     assert_bit_equal(outs[0], outs[1], "sorted vs index order")
+
+
+@pytest.mark.parametrize("n", [23, 28])
+def test_memo_output_staging_same_bits(tmp_path, n):
+    """MINE_B200_MEMO_STAGE=1 (sorted batches stage their statistics and
+    store them in index order) gives the default's bits, for pairwise windows
+    spanning several batches and host / device outputs."""
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "run.py"
+    script.write_text(
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        "from paper_1208_4271_b200 import Engine, datagen\n"
+        f"rng = np.random.default_rng({n}); V = rng.standard_normal((600, {n}))\n"
+        "V[::9] = np.round(V[::9])\n"
+        "e = Engine(0)\n"
+        "r = e.pairwise(V, first=1234, count=150000)\n"
+        "r2 = e.pairwise(V, first=0, count=20000, reuse_vars=True)\n"
+        "np.save(sys.argv[1], np.concatenate([np.stack([r[k] for k in ('mic', 'mas', 'mev', 'mcn', 'mic_e', 'tic')]),\n"
+        "                                     np.stack([r2[k] for k in ('mic', 'mas', 'mev', 'mcn', 'mic_e', 'tic')])], 1))\n")
+    outs = []
+    for flag in ("0", "1"):
+        out = tmp_path / f"o{flag}.npy"
+        env = dict(os.environ, MINE_B200_MEMO_STAGE=flag)
+        subprocess.run([sys.executable, str(script), str(out)], env=env, check=True, timeout=600)
+        outs.append(np.load(out))
+    assert_bit_equal(outs[0], outs[1], "staged vs scattered")
