@@ -1043,12 +1043,27 @@ static int pf_variant(int n, const YParams& yp) {
   if (gen_pts_bytes(n, yp)) return kPfGlobalPts;
   return yp.x_max >= 3 && n > pf_small_n() ? kPf256 : kPf128;
 }
-enum { kDpNone = -1, kDpGlobalTables = 0, kDpRing, kDpWide, kDpLean };
+enum { kDpNone = -1, kDpGlobalTables = 0, kDpRing, kDpWide, kDpLean, kDpLeanInPlace };
+// MINE_B200_DP_INPLACE=1: the lean k_dp reads cb / cum in place from the
+// scratch slot (k_part_f2 always writes them there) instead of staging them,
+// for a smaller shared footprint (more L1)
+static bool dp_inplace() {
+  static const bool on = [] {
+    const char* e = std::getenv("MINE_B200_DP_INPLACE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
 static int dp_variant(int n, const YParams& yp) {
   if (yp.x_max < 3) return kDpNone;
   if (gen_tables_global(n, yp)) return kDpGlobalTables;
   if (yp.x_max - 1 > kFRing) return kDpRing;
-  return gen_dp_lean(n, yp) ? kDpLean : kDpWide;
+  if (!gen_dp_lean(n, yp)) return kDpWide;
+  return dp_inplace() ? kDpLeanInPlace : kDpLean;
+}
+static size_t dp_variant_smem(int v, int n, const YParams& yp) {
+  if (v == kDpLeanInPlace) return dp_layout(yp.y, gen_kc(n, yp), yp.x_max, true, true).total;
+  return gen_dp_smem(n, yp);
 }
 
 // The k_dp launches of a group: runs of consecutive y's with one variant.
@@ -1066,7 +1081,7 @@ static std::vector<DpRun> dp_runs(int n, const YParams* yps, int ny, long long n
     if (v != kDpNone) {
       DpRun r{gi, gj - gi, v, 0, 0, 0};
       for (int g = gi; g < gj; ++g) {
-        r.smem = std::max(r.smem, gen_dp_smem(n, yps[g]));
+        r.smem = std::max(r.smem, dp_variant_smem(v, n, yps[g]));
         r.fslot_doubles = std::max(r.fslot_doubles, gen_fslot_bytes(n, yps[g]) / sizeof(double));
       }
       // up to 4 CTAs per SM, as shared memory allows (the wide variants are
@@ -1193,6 +1208,7 @@ int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long 
       case kDpGlobalTables: DP_LAUNCH(true, true, false); break;
       case kDpRing: DP_LAUNCH(false, true, false); break;
       case kDpWide: DP_LAUNCH(false, false, false); break;
+      case kDpLeanInPlace: DP_LAUNCH(true, false, true); break;
       default: DP_LAUNCH(false, false, true); break;
     }
 #undef DP_LAUNCH
@@ -1225,6 +1241,7 @@ cudaError_t init_general_attributes(int device) {
                        reinterpret_cast<const void*>(k_dp<false, false, true>),
                        reinterpret_cast<const void*>(k_dp<false, true, false>),
                        reinterpret_cast<const void*>(k_dp<true, true, false>),
+                       reinterpret_cast<const void*>(k_dp<true, false, true>),
                        reinterpret_cast<const void*>(k_dp_warp)};
   for (const void* f : fns) {
     cudaFuncAttributes fa{};
@@ -1245,7 +1262,8 @@ cudaError_t init_general_attributes(int device) {
     const void* dps[] = {reinterpret_cast<const void*>(k_dp<false, false, false>),
                          reinterpret_cast<const void*>(k_dp<false, true, false>),
                          reinterpret_cast<const void*>(k_dp<true, true, false>),
-                         cv ? reinterpret_cast<const void*>(k_dp<false, false, true>) : nullptr};
+                         cv ? reinterpret_cast<const void*>(k_dp<false, false, true>) : nullptr,
+                         cv ? reinterpret_cast<const void*>(k_dp<true, false, true>) : nullptr};
     for (const void* f : dps) {
       if (!f) continue;
       e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
