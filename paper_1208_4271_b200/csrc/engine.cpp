@@ -196,7 +196,7 @@ struct mine_b200_ctx {
   cudaStream_t copy = nullptr;    // result drain
   std::mutex mu;
   TableSet tables;
-  DevBuf vals, perm, runid, runstart, nruns, q, yhat, hq, lw, rsmask;
+  DevBuf vals, perm, runid, runstart, nruns, q, yhat, hq, lw, rsmask, qsame;
   DevBuf ocells, stats, flag, idx, counters, memo, memo_vals, memo_val, rec, dx, sxx, micscr, sortscr, mstage;
   // general tier: one launch group per chunk of pairs (or per y-group when
   // the scratch of all y's would not fit): scratch regions, the group's y
@@ -218,7 +218,7 @@ struct mine_b200_ctx {
     int kind = -1, va = 0, vb = 0, n = 0, B = 0;
     const void* a = nullptr;
     const void* b = nullptr;
-    bool dio = false, memo = false, tiny = false, centred = false;
+    bool dio = false, memo = false, tiny = false, centred = false, qsame = false;
     const double* dvals = nullptr;
   } prep;
   std::vector<cudaEvent_t> events;
@@ -305,6 +305,16 @@ size_t gen_budget() {
   return b;
 }
 
+// Row-map dedup in the general tier (k_row_same / k_part_f2 / k_copy_dups):
+// on unless MINE_B200_ROW_DEDUP=0 (the A/B and bit-identity tests)
+static bool row_dedup_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("MINE_B200_ROW_DEDUP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static int gen_lanes() {
   static const int v = [] {
     const char* e = std::getenv("MINE_B200_GEN_LANES");
@@ -355,7 +365,7 @@ struct CtxPrepared {
   const Call& call;
   const double* dvals;
   int B;
-  bool dio, memo, tiny, centred = false;
+  bool dio, memo, tiny, centred = false, qsame = false;
   template <typename PrepT>
   void commit(PrepT& P) const {
     P.valid = true;
@@ -370,6 +380,7 @@ struct CtxPrepared {
     P.memo = memo;
     P.tiny = tiny;
     P.centred = centred;
+    P.qsame = qsame;
     P.dvals = dvals;
   }
 };
@@ -476,7 +487,7 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
     CK(launch_sort_vars(vs, ctx->sortscr.ensure(sort_scratch_bytes(V, n)), s));
     launch_equipartition(vs, tb, s);
     ctx->launches += 2;
-    P.memo = P.tiny = P.centred = false;
+    P.memo = P.tiny = P.centred = P.qsame = false;
   }
   if (memo) {
     vs.rec = static_cast<uint4*>(ctx->rec.ensure(sizeof(uint4) * 6 * (size_t)V));
@@ -491,9 +502,16 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
       launch_pack_tiny(vs, s);
       ++ctx->launches;
     }
+  } else if (row_dedup_on()) {  // general tier: row-map equality of consecutive y's
+    vs.qsame = static_cast<uint8_t*>(ctx->qsame.ensure((size_t)V * ny));
+    if (!P.qsame) {
+      launch_row_same(vs, s);
+      ++ctx->launches;
+    }
   }
   // what this call leaves prepared (committed once the call succeeds)
   CtxPrepared done{call, dvals, B, dio, memo || P.memo, tiny || P.tiny};
+  done.qsame = vs.qsame != nullptr || P.qsame;
 
   // ---- pair space
   PairSpace ps;

@@ -109,6 +109,25 @@ __device__ __forceinline__ void sub_vars(const PairSpace& ps, long long pl, int 
   Y = orient ? va : vb;
 }
 
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Row-map dedup (k_row_same): the group index of the smallest row target
+// whose row map equals row target gi's for row variable Yv, or gi itself.
+// Only y's of this group count (their descriptors are live).
+__device__ __forceinline__ int canonical_gi(const VarSet& vs, const GenGroup& grp, int gi, int Yv) {
+  const int yi = grp.ys[gi].yp.yi;
+  const uint8_t* same = vs.qsame + (size_t)Yv * vs.ny;
+  int yc = yi;
+  while (yc > 0 && same[yc]) --yc;
+  if (yc == yi) return gi;
+  const int gc = gi - (yi - yc);  // the group's y's are consecutive
+  return gc >= 0 && grp.ys[gc].yp.yi == yc ? gc : gi;
+}
+
 // Writes the normalised cells of one orientation / row target (char_matrix.cpp:
 // 57-64); I(l) gives the unnormalised I_l.
 template <typename IFn>
@@ -166,6 +185,41 @@ __global__ void __launch_bounds__(kPfThreads, PF_MINB_THREADS / kPfThreads) k_pa
   const int rows = vs.yhat[(size_t)Y * vs.ny + yi];
   const double hq = vs.hq[(size_t)Y * vs.ny + yi];
 
+  // --- row-map dedup: when a smaller y of this group has the same row map
+  // (ties saturate the equipartition), the raw clumps are that y's too; if
+  // they do not superclump here (raw k <= k_hat <= that y's k_hat) the
+  // partition, and so every F(t, l) with l <= min(x_max, k), is that y's, and
+  // so are the cells (l, y), l <= x_max (mutual_info.cpp:68-70 repeats I_k
+  // beyond k in both).  The canonical subproblem has a lower block index (the
+  // grid is y-major) or ran in an earlier launch; its raw k is published in
+  // its descriptor (zeroed per group).  The wait is bounded: on a timeout
+  // the subproblem is computed here, so the result never depends on it.
+  if (vs.qsame && !has_dbg) {
+    if (tid == 0) {
+      int kr = 0;
+      const int gc = canonical_gi(vs, grp, gi, Y);
+      if (gc != gi) {
+        const int* dz = grp.ys[gc].desc + 4 * sub + 2;
+        for (int it = 0; it < 4096 && (kr = ld_relaxed(dz)) == 0; ++it) __nanosleep(128);
+        if (kr > 0 && kr <= k_hat) {
+          reinterpret_cast<int4*>(gs.desc)[sub] = make_int4(kr, rows, gc, -1);  // l_max -1: copy
+          if (counters) {
+            unsigned long long w[kNumCounters] = {};
+            subproblem_work(rows, kr, x_max, n, w);
+            for (int i = 0; i < kNumCounters; ++i)
+              if (w[i]) atomicAdd(counters + i, w[i]);
+          }
+        } else {
+          kr = 0;
+        }
+      }
+      misc[0] = kr;
+    }
+    __syncthreads();
+    if (misc[0] != 0) return;
+    __syncthreads();  // misc is scan scratch below
+  }
+
   // --- row labels in x order (reindex_to_first_order, partition.cpp:94-106)
   for (int t = tid; t < n; t += kPfThreads) {
     lab[t] = qY[permX[t]];
@@ -187,6 +241,9 @@ __global__ void __launch_bounds__(kPfThreads, PF_MINB_THREADS / kPfThreads) k_pa
   }
   __syncthreads();
   const int kraw = block_incl_scan(cl, n, misc) + 1;  // cl[t]: clump of position t
+  if (vs.qsame && tid == 0) {  // for the row-map dedup of larger y's (above)
+    asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(gs.desc + 4 * sub + 2), "r"(kraw) : "memory");
+  }
   for (int t = tid + 1; t < n; t += kPfThreads)
     if (cl[t] != cl[t - 1]) cb[cl[t]] = t;
   if (tid == 0) {
@@ -896,13 +953,28 @@ __global__ void __launch_bounds__(kWarpThreads) k_dp_warp(VarSet vs, Tables tb, 
         W[s] = __dmul_rn(q, -acch);
       }
       __syncwarp();
+      // levels 3 .. l_hi of row t: P lanes per level (P = 32 / levels,
+      // rounded down to a power of two) split the split points s by phase and
+      // max-reduce by shuffles -- large y have few levels, and one lane per
+      // level left most of the warp idle
       const int l_hi = t == k ? min(t, l_max) : min(t, l_max - 1);
-      for (int l = 3 + lane; l <= l_hi; l += 32) {
-        double m = kLowest;
-        const double* fc = F + (l - 3);
-        for (int s = l - 1; s < t; ++s)
-          m = dmax(m, __dsub_rn(__dmul_rn(A[s], fc[s * LW]), W[s]));
-        F[t * LW + (l - 2)] = m;
+      const int nlev = l_hi - 2;
+      if (nlev > 0) {
+        int lp = 0;  // log2 P
+        while (lp < 5 && (nlev << (lp + 1)) <= 32) ++lp;
+        const int P = 1 << lp;
+        for (int base = 0; base < (nlev << lp); base += 32) {
+          const int idx = base + lane, lev = idx >> lp, ph = idx & (P - 1);
+          const int l = 3 + lev;
+          double m = kLowest;
+          if (lev < nlev) {
+            const double* fc = F + (l - 3);
+            for (int s = l - 1 + ph; s < t; s += P)
+              m = dmax(m, __dsub_rn(__dmul_rn(A[s], fc[s * LW]), W[s]));
+          }
+          for (int o = P >> 1; o > 0; o >>= 1) m = dmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+          if (lev < nlev && ph == 0) F[t * LW + (l - 2)] = m;
+        }
       }
       __syncwarp();
     }
@@ -1104,6 +1176,39 @@ size_t gen_group_fslot_bytes(int n, const YParams* yps, int ny, long long nsub) 
   return b;
 }
 
+// Row-map dedup, second half: subproblems k_part_f2 marked as copies
+// (l_max = -1, desc.z = the canonical y's group index) take that y's cells
+// (l, y') for l = 2 .. x_max(y) once every kernel of the group has written
+// them.  One thread per (y, subproblem).
+__global__ void k_copy_dups(VarSet vs, Tables tb, PairSpace ps, long long base, GenGroup grp,
+                            double* __restrict__ ocells, int orient_only) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= grp.nsub * grp.ny) return;
+  const int gi = (int)(i / grp.nsub);
+  const long long sub = i % grp.nsub;
+  const int4 d = reinterpret_cast<const int4*>(grp.ys[gi].desc)[sub];
+  if (d.w != -1) return;
+  const int norient = orient_only >= 0 ? 1 : 2;
+  const long long pl = base + sub / norient;
+  const int orient = orient_only >= 0 ? orient_only : (int)(sub % 2);
+  const int y = grp.ys[gi].yp.y, yc = grp.ys[d.z].yp.y, x_max = grp.ys[gi].yp.x_max;
+  MB_CHECK(d.z < gi && yc < y && grp.ys[d.z].yp.x_max >= x_max);
+  double* oc = ocells + (size_t)pl * 2 * tb.ncell + (size_t)orient * tb.ncell;
+  for (int l = 2; l <= x_max; ++l) {
+    const int to = orient ? tb.cell_off[l] + (y - 2) : tb.cell_off[y] + (l - 2);
+    const int from = orient ? tb.cell_off[l] + (yc - 2) : tb.cell_off[yc] + (l - 2);
+    oc[to] = oc[from];
+  }
+}
+
+static int launch_copy_dups(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
+                            const GenGroup& g, int ny, long long nsub, double* ocells, int orient_only,
+                            cudaStream_t s) {
+  const long long total = nsub * ny;
+  k_copy_dups<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(vs, tb, ps, base, g, ocells, orient_only);
+  return 1;
+}
+
 int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
                   long long npairs, const YParams* yps, int ny, void* scratch, GenY* d_ys,
                   unsigned long long* d_cnt, double* fslots, double* ocells, const SubDebug* dbg,
@@ -1120,15 +1225,20 @@ int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long 
     p += al16(bytes);
     return q;
   };
+  // the descriptors of all y's first, contiguous: one memset clears them for
+  // the row-map dedup (k_part_f2 reads a smaller y's raw k there)
+  for (int gi = 0; gi < ny; ++gi) hy[gi].desc = reinterpret_cast<int*>(carve(sizeof(int4) * nsub));
+  if (vs.qsame) cudaMemsetAsync(hy[0].desc, 0, (size_t)(p - static_cast<char*>(scratch)), s0);
   for (int gi = 0; gi < ny; ++gi) {
     GenY& Y = hy[gi];
+    int* const desc = Y.desc;
     std::memset(&Y, 0, sizeof(Y));
+    Y.desc = desc;
     Y.yp = yps[gi];
     Y.kc = gen_kc(n, Y.yp);
     Y.small_ok = warp_ok(Y.yp);
     Y.tables_global = gen_tables_global(n, Y.yp);
     Y.cum_stride = (unsigned long long)Y.yp.y * (Y.kc + 1);
-    Y.desc = reinterpret_cast<int*>(carve(sizeof(int4) * nsub));
     Y.cb = reinterpret_cast<int*>(carve(sizeof(int) * (size_t)(Y.kc + 1) * nsub));
     Y.cum = reinterpret_cast<int*>(carve(sizeof(int) * Y.cum_stride * nsub));
     Y.f2 = reinterpret_cast<double*>(carve(sizeof(double) * (size_t)(Y.kc + 1) * nsub));
@@ -1178,7 +1288,10 @@ int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long 
       whi = std::max(whi, gi);
       per_warp = std::max(per_warp, warp_per_warp(yps[gi]));
     }
-  if (runs.empty() && whi < wlo) return launches;
+  if (runs.empty() && whi < wlo) {
+    if (vs.qsame) launches += launch_copy_dups(vs, tb, ps, base, g, ny, nsub, ocells, orient_only, s0);
+    return launches;
+  }
   // the warp path on the side lane (its items are disjoint from k_dp's), the
   // k_dp runs in ascending y on the main lane
   cudaStream_t sw = s0;
@@ -1218,6 +1331,7 @@ int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long 
     cudaEventRecord(ev[1], sw);
     cudaStreamWaitEvent(s0, ev[1], 0);
   }
+  if (vs.qsame) launches += launch_copy_dups(vs, tb, ps, base, g, ny, nsub, ocells, orient_only, s0);
   return launches;
 }
 

@@ -184,6 +184,29 @@ __global__ void k_equipartition(VarSet vs, Tables tb) {
   }
 }
 
+// Row-map equality of consecutive row targets: qsame[v][yi] = 1 iff
+// Q(v, y) == Q(v, y - 1) label for label (same rows; ties make the greedy
+// scan saturate, e.g. a Poisson variable with 5 distinct values has the same
+// rows for every y >= 5).  Subproblems whose row map equals a smaller y's
+// need no partition or DP when their raw clumps do not superclump
+// (k_part_f2: the cells are the smaller y's).  One warp per
+// (variable, yi); the label compare runs only when the row counts agree.
+__global__ void k_row_same(VarSet vs) {
+  const long long idx = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (idx >= (long long)vs.V * vs.ny) return;
+  const int yi = (int)(idx % vs.ny), n = vs.n;
+  bool same = yi > 0 && vs.yhat[idx] == vs.yhat[idx - 1];
+  if (same) {
+    const uint16_t* a = vs.q + (size_t)idx * n;
+    const uint16_t* b = a - n;
+    bool diff = false;
+    for (int t = lane; t < n; t += 32) diff |= a[t] != b[t];
+    same = !__any_sync(0xffffffffu, diff);
+  }
+  if (lane == 0) vs.qsame[idx] = same ? 1 : 0;
+}
+
 // Tiny-tier packing: per sample the labels of y=2 and y=3 in one byte, and the
 // run-start bitmask over sorted positions.
 __global__ void k_pack_tiny(VarSet vs) {
@@ -1429,6 +1452,11 @@ cudaError_t launch_sort_vars(const VarSet& vs, void* scratch, cudaStream_t s) {
 void launch_equipartition(const VarSet& vs, const Tables& tb, cudaStream_t s) {
   const long long warps = (long long)vs.V * vs.ny;
   k_equipartition<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(vs, tb);
+}
+
+void launch_row_same(const VarSet& vs, cudaStream_t s) {
+  const long long warps = (long long)vs.V * vs.ny;
+  k_row_same<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(vs);
 }
 
 void launch_pack_tiny(const VarSet& vs, cudaStream_t s) {

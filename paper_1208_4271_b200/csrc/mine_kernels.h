@@ -24,6 +24,7 @@ struct VarSet {
   uint16_t* q = nullptr;         // V x ny x n row label (1-based) of each sample
   int* yhat = nullptr;           // V x ny     realised row count
   double* hq = nullptr;          // V x ny     H(Q), reference-exact (mutual_info.cpp:33)
+  uint8_t* qsame = nullptr;      // V x ny     general tier: Q(y) == Q(y - 1) (k_row_same), or null
   uint8_t* lw = nullptr;         // V x n      tiny tier: packed labels (y=2: bits 0-1, y=3: 2-3)
   uint32_t* rsmask = nullptr;    // V          tiny tier: run-start bitmask over sorted positions
   uint4* rec = nullptr;          // V x 6      memo tier: 96-byte per-variable record
@@ -122,6 +123,8 @@ size_t sort_scratch_bytes(int V, int n);
 cudaError_t launch_sort_vars(const VarSet& vs, void* scratch, cudaStream_t s);
 void launch_equipartition(const VarSet& vs, const Tables& tb, cudaStream_t s);
 void launch_pack_tiny(const VarSet& vs, cudaStream_t s);
+// general tier: vs.qsame from vs.q / vs.yhat (after launch_equipartition)
+void launch_row_same(const VarSet& vs, cudaStream_t s);
 
 // Tiny tier (n <= 32, B <= 7): one thread per pair, stats (and optionally the
 // per-orientation cells o1/o2, ncell each per pair) written directly.

@@ -565,3 +565,68 @@ def test_memo_output_staging_same_bits(tmp_path, n):
         subprocess.run([sys.executable, str(script), str(out)], env=env, check=True, timeout=600)
         outs.append(np.load(out))
     assert_bit_equal(outs[0], outs[1], "staged vs scattered")
+
+
+def _tied_vars(rng, p, n):
+    """Tie-heavy variables whose row maps saturate at small y (the row-map
+    dedup's case): Poisson counts over a range of rates, a few discretised
+    normals and one near-constant variable."""
+    lam = np.exp(rng.uniform(np.log(0.1), np.log(40.0), p))
+    V = rng.poisson(lam[:, None] * np.exp(0.8 * rng.standard_normal(n))[None, :] ** (np.arange(p) % 2)[:, None])
+    V = V.astype(float)
+    V[3::7] = np.round(rng.standard_normal((len(range(3, p, 7)), n)) * 1.5)
+    V[5, :] = 0.0
+    V[5, : n // 3] = 1.0
+    return V
+
+
+@pytest.mark.parametrize("n,alpha,c", [(300, 0.6, 15.0), (500, 0.6, 15.0), (400, 0.7, 0.6), (250, 0.8, 2.0)])
+def test_row_dedup_ties_bit_exact(engine, oracle, n, alpha, c):
+    """Pairs whose row maps repeat over y (ties saturate the equipartition):
+    the subproblems k_part_f2 turns into copies of a smaller y's cells, and
+    the ones it still computes because their raw clumps superclump at the
+    larger y (small c), give the oracle's cells of both orientations and the
+    statistics bit for bit."""
+    rng = np.random.default_rng(n + int(100 * c))
+    V = _tied_vars(rng, 24, n)
+    res = engine.pairwise(V, Parameters(alpha, c, 1), cells=True)
+    want = oracle.pairwise(V, alpha, c, 1)
+    assert_bit_equal(stats_matrix(res), want, "tied pairwise")
+    k = 0
+    for i in range(V.shape[0]):
+        for j in range(i + 1, V.shape[0]):
+            if k % 7 == 0:
+                _, o1, o2, _m = oracle.score(V[i], V[j], alpha, c)
+                assert_bit_equal(res["cells"][k, 0], o1, f"o1 pair {i},{j}")
+                assert_bit_equal(res["cells"][k, 1], o2, f"o2 pair {i},{j}")
+            k += 1
+
+
+def test_row_dedup_off_same_bits(tmp_path):
+    """MINE_B200_ROW_DEDUP=0 (every subproblem computed) gives the default's
+    bits: statistics and cells of a c2 window, a cross call and a list call
+    on one orientation's worth of tied variables."""
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "run.py"
+    script.write_text(
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        "from paper_1208_4271_b200 import Engine, Parameters, datagen\n"
+        "w = datagen.make(2); P = Parameters(w.alpha, w.c, w.est)\n"
+        "e = Engine(0)\n"
+        "r = e.pairwise(w.X, P, first=5000, count=6000, cells=True)\n"
+        "X, Y = w.X[:20], w.X[1500:1530]\n"
+        "r2 = e.cross(X, Y, Parameters(0.6, 3.0, 1), cells=True)\n"
+        "cols = ('mic', 'mas', 'mev', 'mcn', 'mic_e', 'tic')\n"
+        "a = np.concatenate([np.stack([r[k] for k in cols]).ravel(), r['cells'].ravel(),\n"
+        "                    np.stack([r2[k] for k in cols]).ravel(), r2['cells'].ravel()])\n"
+        "np.save(sys.argv[1], a)\n")
+    outs = []
+    for flag in ("0", "1"):
+        out = tmp_path / f"o{flag}.npy"
+        env = dict(os.environ, MINE_B200_ROW_DEDUP=flag)
+        subprocess.run([sys.executable, str(script), str(out)], env=env, check=True, timeout=600)
+        outs.append(np.load(out))
+    assert_bit_equal(outs[1], outs[0], "row-map dedup vs every subproblem computed")
