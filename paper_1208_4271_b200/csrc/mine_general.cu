@@ -48,6 +48,10 @@ namespace {
 #endif
 constexpr int kDpThreads = KDP_THREADS;
 constexpr int kMaxTile = KDP_TILE;  // t-tile / s-chunk edge
+#ifndef KDP_SUBTILE
+#define KDP_SUBTILE 8
+#endif
+constexpr int kSubTile = KDP_SUBTILE;  // k_dp inner part: rows per sequential sub-tile
 constexpr int kAccStride = 9;  // doubles per thread in the accumulator hand-over (odd: no bank conflicts)
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -802,26 +806,49 @@ __global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : 3) k_dp(V
         for (int tl = tid; tl < nt; tl += kDpThreads)  // column 0: level l0 - 1
           ft[tl * ftw] = F[(size_t)(t0 + tl) * RW + ((l0 - 3) & cm)];
         __syncthreads();
-        if (tid < inner_threads) {
-          const int ll = tid, l = l0 + ll;
-          for (int tl = 0; tl < nt; ++tl) {
-            const int tt = t0 + tl;
-            if (ll < nl && tt >= l && !(l == l_max && tt != k)) {
-              // owner of cell (tl, ll): thread (tl/2)*ng + ll/4, slot (tl&1)*4 + (ll&3)
-              double m = accS[((tl >> 1) * ng + (ll >> 2)) * kAccStride + (tl & 1) * 4 + (ll & 3)];
-              const double* Ap = A + tl;
-              const double* Wp = W + tl;
-              for (int s = max(t0, l - 1); s < tt; ++s) {
-                const int sl = s - t0;
-                m = dmax(m, __dsub_rn(__dmul_rn(Ap[sl * kMaxTile], ft[sl * ftw + ll]),
-                                      Wp[sl * kMaxTile]));
+        // The tile's rows in sub-tiles of kSubTile: a sub-tile's own split
+        // points run sequentially (a step per row, chains of < kSubTile
+        // candidates), then its rows' candidates for every later row of the
+        // tile -- independent -- are folded into the hand-over by all threads.
+        // (Row by row over the whole tile, chains of up to 31 candidates left
+        // 6 of 8 warps waiting at the tile's barrier.)
+        for (int sb0 = 0; sb0 < nt; sb0 += kSubTile) {
+          const int sb1 = min(sb0 + kSubTile, nt);
+          if (tid < inner_threads) {
+            const int ll = tid, l = l0 + ll;
+            for (int tl = sb0; tl < sb1; ++tl) {
+              const int tt = t0 + tl;
+              if (ll < nl && tt >= l && !(l == l_max && tt != k)) {
+                // owner of cell (tl, ll): thread (tl/2)*ng + ll/4, slot (tl&1)*4 + (ll&3)
+                double m = accS[((tl >> 1) * ng + (ll >> 2)) * kAccStride + (tl & 1) * 4 + (ll & 3)];
+                const double* Ap = A + tl;
+                const double* Wp = W + tl;
+                for (int s = max(t0 + sb0, l - 1); s < tt; ++s) {
+                  const int sl = s - t0;
+                  m = dmax(m, __dsub_rn(__dmul_rn(Ap[sl * kMaxTile], ft[sl * ftw + ll]),
+                                        Wp[sl * kMaxTile]));
+                }
+                ft[tl * ftw + ll + 1] = m;
+                F[(size_t)tt * RW + ((l - 2) & cm)] = m;
+                if (kRing && tt == k) fk[l - 2] = m;
               }
-              ft[tl * ftw + ll + 1] = m;
-              F[(size_t)tt * RW + ((l - 2) & cm)] = m;
-              if (kRing && tt == k) fk[l - 2] = m;
+              named_sync(1, inner_threads);
             }
-            named_sync(1, inner_threads);
           }
+          if (sb1 >= nt) break;
+          __syncthreads();
+          // rows [sb1, nt) x levels: candidates s in [t0 + sb0, t0 + sb1)
+          const int ncell = (nt - sb1) * nl;
+          for (int c = tid; c < ncell; c += kDpThreads) {
+            const int tl = sb1 + c / nl, ll = c - (c / nl) * nl, l = l0 + ll, tt = t0 + tl;
+            if (tt < l || (l == l_max && tt != k)) continue;
+            double* slot = accS + ((tl >> 1) * ng + (ll >> 2)) * kAccStride + (tl & 1) * 4 + (ll & 3);
+            double m = *slot;
+            for (int sl = max(sb0, l - 1 - t0); sl < sb1; ++sl)
+              m = dmax(m, __dsub_rn(__dmul_rn(A[sl * kMaxTile + tl], ft[sl * ftw + ll]), W[sl * kMaxTile + tl]));
+            *slot = m;
+          }
+          __syncthreads();
         }
         __syncthreads();
       }
