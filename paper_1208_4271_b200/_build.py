@@ -73,7 +73,7 @@ def _build_into(BUILD: str, LIB: str, defs: list, force: bool, verbose: bool, pr
                   "-I", os.path.join(ROOT, "include"), "-I", CUDA_INC, "-c", s, "-o", o])
         objs.append(o)
     if force or not _newer(LIB, objs):
-        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lpthread"])
+        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lpthread", "-ldl"])
     probe_src = os.path.join(CSRC, "probes.cu")
     if probes and (force or not _newer(PROBES, [probe_src] + [os.path.normpath(os.path.join(CSRC, h)) for h in HEADERS])):
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",

@@ -21,9 +21,20 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "mine_b200.h"
 #include "mine_kernels.h"
+
+// NVTX ranges per call stage (SURVEY 5 tracing): host-side push/pop around
+// the enqueue of each stage, so a timeline tool (nsys) lines the stages up
+// with their kernels; free when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 using namespace mb200;
 
@@ -330,6 +341,7 @@ static int gen_lanes() {
 int run_gen_group(mine_b200_ctx* ctx, const VarSet& vs, const Tables& tb, const PairSpace& pc,
                   long long npairs, const YParams* yps, int ny, double* ocells, const SubDebug* dbg,
                   int orient_only, unsigned long long* dcnt, cudaStream_t s) {
+  NvtxRange nv("general: partitions + DP group");
   const long long nsub = npairs * (orient_only >= 0 ? 1 : 2);
   const int G = std::min(gen_lanes(), ny);
   CK(cudaEventRecord(ctx_event(ctx, 4), s));
@@ -347,7 +359,7 @@ int run_gen_group(mine_b200_ctx* ctx, const VarSet& vs, const Tables& tb, const 
     for (const auto& yp : mine) scr += nsub * (gen_scratch_per_sub(vs.n, yp) + 16 * 8);
     void* scratch = L.scr.ensure(scr);
     GenY* d_ys = static_cast<GenY*>(L.ys.ensure(sizeof(GenY) * mine.size()));
-    auto* d_cnt = static_cast<unsigned long long*>(L.cnt.ensure(sizeof(unsigned long long) * 4 * mine.size()));
+    auto* d_cnt = static_cast<unsigned long long*>(L.cnt.ensure(sizeof(unsigned long long) * (4 * mine.size() + 4)));
     double* fslots = static_cast<double*>(
         L.fslots.ensure(gen_group_fslot_bytes(vs.n, mine.data(), (int)mine.size(), nsub)));
     CK(cudaStreamWaitEvent(L.s, ctx_event(ctx, 4), 0));
@@ -390,6 +402,7 @@ struct CtxPrepared {
 // (cached) and launch bookkeeping.
 void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
               const mine_b200_opts* opts_in, mine_stats_out* out) {
+  NvtxRange nv_call("mine_b200 call");
   validate_param(par);
   mine_b200_opts opts{};
   if (opts_in) opts = *opts_in;
@@ -484,6 +497,7 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   vs.yhat = static_cast<int*>(ctx->yhat.ensure(sizeof(int) * (size_t)V * ny));
   vs.hq = static_cast<double*>(ctx->hq.ensure(sizeof(double) * (size_t)V * ny));
   if (!reuse) {
+    NvtxRange nv("K1 sort + K2 equipartition");
     CK(launch_sort_vars(vs, ctx->sortscr.ensure(sort_scratch_bytes(V, n)), s));
     launch_equipartition(vs, tb, s);
     ctx->launches += 2;
@@ -624,6 +638,7 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
   if (opts.ev_begin) CK(cudaEventRecord(static_cast<cudaEvent_t>(opts.ev_begin), s));
 
   for (long long ci = 0; ci < nchunks; ++ci) {
+    NvtxRange nv_chunk(memo ? "chunk: memo tier" : tiny ? "chunk: tiny tier" : "chunk: general tier");
     const long long c0 = sched[ci].first;
     const long long cn = sched[ci].second;
     const int slot = (int)(ci % nslots);

@@ -168,8 +168,11 @@ __global__ void __launch_bounds__(kPfThreads, PF_MINB_THREADS / kPfThreads) k_pa
   const GenScratch gs = scratch_of(GY, grp.nsub);
   const long long pl = base + sub / norient;
   const int orient = orient_only >= 0 ? orient_only : (int)(sub % 2);
-  int X, Y;
-  sub_vars(ps, pl, orient, X, Y);
+  // the pair's variables: one thread inverts the condensed index
+  __shared__ int s_xy[2];
+  if (tid == 0) sub_vars(ps, pl, orient, s_xy[0], s_xy[1]);
+  __syncthreads();
+  const int X = s_xy[0], Y = s_xy[1];
   const int y = yp.y, yi = yp.yi, x_max = yp.x_max, k_hat = yp.k_hat, kc = gs.kc;
 
   const PfLayout L = pf_layout(n, y, kc, kPtsGlobal, kCumGlobal);
@@ -440,6 +443,335 @@ __global__ void __launch_bounds__(kPfThreads, PF_MINB_THREADS / kPfThreads) k_pa
   if (l_max <= 2) {  // done: I_l = I_2 for every l (mutual_info.cpp:68-70)
     const double i2 = k >= 2 ? dmax(0.0, __dadd_rn(hq, dmisc[0])) : 0.0;
     write_cells(tb, ocells, pl, orient, y, x_max, rows, [&](int) { return i2; }, dbg, has_dbg != 0);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Warp partition path (n <= kWarpPartMaxN, per-point arrays on chip): the
+// same partition, cell counts and F(t,2) level as k_part_f2, but one WARP per
+// (y, subproblem) with no block barrier.  A subproblem at n = 500 is ~16
+// chunks of 32 x-sorted positions per pass; in a 128-thread CTA its ~10 block
+// barriers, block scans and per-CTA setup cost more than the partition
+// itself (c2: every pair has 38 such subproblems).  Here the passes run over
+// 32-position chunks with ballots:
+//   1. labels in x order (partition.cpp:94-106), label changes inside an x
+//      tie run mark the run fused (Alg. 1, :116-133) in a bitmask by run;
+//   2. clump starts (:135-144) as one ballot word per chunk; the boundaries
+//      by popcount prefix;
+//   3. superclumps (Alg. 2) by the ballot greedy of k_part_f2, their starts
+//      re-marked in the start mask;
+//   4. cell counts: clump of a position = popcount prefix of the start mask,
+//      shared atomics, then a warp scan per row (mutual_info.cpp:9-24);
+//   5. F(t,2) (mutual_info.cpp:47-56), half-warps or the warp per t.
+constexpr int kWarpPartMaxN = 1024;
+constexpr int kWpWarps = 8;  // warps per CTA
+
+struct WpLayout {
+  size_t lab, rid, fm, sm, cb, cum, per_warp;
+};
+__host__ __device__ inline WpLayout wp_layout(int n, size_t cum_ints) {
+  WpLayout L;
+  size_t o = 0;
+  const size_t nw = (size_t)(n + 31) >> 5;
+  L.lab = o;
+  o += al16(sizeof(uint16_t) * n);
+  L.rid = o;  // x tie-run ordinal per position (< n <= 1024)
+  o += al16(sizeof(uint16_t) * n);
+  L.fm = o;  // fused runs, by run ordinal
+  o += al16(4 * nw);
+  L.sm = o;  // (super)clump starts, by position
+  o += al16(4 * nw);
+  L.cb = o;
+  o += al16(sizeof(int) * (n + 1));
+  L.cum = o;
+  o += al16(sizeof(int) * cum_ints);
+  L.per_warp = o;
+  return L;
+}
+
+__device__ __forceinline__ void part_warp_item(const VarSet& vs, const Tables& tb, const PairSpace& ps,
+                                               long long base, const GenGroup& grp, int gi, long long sub,
+                                               int per_warp, double* __restrict__ ocells, int orient_only,
+                                               unsigned long long* counters, unsigned char* wb) {
+  const int lane = threadIdx.x & 31;
+  const int n = vs.n, nwd = (n + 31) >> 5;
+  const GenY& GY = grp.ys[gi];
+  const YParams yp = GY.yp;
+  const GenScratch gs = scratch_of(GY, grp.nsub);
+  const int norient = orient_only >= 0 ? 1 : 2;
+  const long long pl = base + sub / norient;
+  const int orient = orient_only >= 0 ? orient_only : (int)(sub % 2);
+  int X = 0, Y = 0;
+  if (lane == 0) sub_vars(ps, pl, orient, X, Y);
+  X = __shfl_sync(0xffffffffu, X, 0);
+  Y = __shfl_sync(0xffffffffu, Y, 0);
+  const int y = yp.y, yi = yp.yi, x_max = yp.x_max, k_hat = yp.k_hat, kc = gs.kc;
+  const int rows = vs.yhat[(size_t)Y * vs.ny + yi];
+  const double hq = vs.hq[(size_t)Y * vs.ny + yi];
+  const WpLayout L = wp_layout(n, (size_t)y * (kc + 1));
+  uint16_t* lab = reinterpret_cast<uint16_t*>(wb + L.lab);
+  uint16_t* rid = reinterpret_cast<uint16_t*>(wb + L.rid);
+  uint32_t* fm = reinterpret_cast<uint32_t*>(wb + L.fm);
+  uint32_t* sm = reinterpret_cast<uint32_t*>(wb + L.sm);
+  int* cb = reinterpret_cast<int*>(wb + L.cb);
+  int* cum = reinterpret_cast<int*>(wb + L.cum);
+  MB_CHECK(L.per_warp <= (size_t)per_warp && n <= kWarpPartMaxN);
+
+  // --- row-map dedup (as in k_part_f2): a smaller y of this group with the
+  // same row map whose raw clumps do not superclump here gives the cells
+  if (vs.qsame) {
+    int kr = 0;
+    if (lane == 0) {
+      const int gc = canonical_gi(vs, grp, gi, Y);
+      if (gc != gi) {
+        const int* dz = grp.ys[gc].desc + 4 * sub + 2;
+        for (int it = 0; it < 4096 && (kr = ld_relaxed(dz)) == 0; ++it) __nanosleep(128);
+        if (kr > 0 && kr <= k_hat) {
+          reinterpret_cast<int4*>(gs.desc)[sub] = make_int4(kr, rows, gc, -1);
+          if (counters) {
+            unsigned long long w[kNumCounters] = {};
+            subproblem_work(rows, kr, x_max, n, w);
+            for (int i = 0; i < kNumCounters; ++i)
+              if (w[i]) atomicAdd(counters + i, w[i]);
+          }
+        } else {
+          kr = 0;
+        }
+      }
+    }
+    if (__shfl_sync(0xffffffffu, kr, 0) != 0) return;
+  }
+
+  const int* permX = vs.perm + (size_t)X * n;
+  const int* ridX = vs.runid + (size_t)X * n;
+  const uint16_t* qY = vs.q + ((size_t)Y * vs.ny + yi) * n;
+  const unsigned lt = (1u << lane) - 1u;
+
+  // --- pass 0: labels in x order (the dependent gathers of every chunk in
+  // flight together) and the x tie-run ordinals, into this warp's slice
+  for (int w = lane; w < nwd; w += 32) fm[w] = 0u;
+#pragma unroll 4
+  for (int t = lane; t < n; t += 32) {
+    lab[t] = qY[__ldg(permX + t)];
+    rid[t] = (uint16_t)__ldg(ridX + t);
+  }
+  __syncwarp();
+  // --- pass 1: a label change inside an x tie run fuses the run
+#pragma unroll 4
+  for (int t = 1 + lane; t < n; t += 32) {
+    const int rd = rid[t];
+    if (rd == rid[t - 1] && lab[t] != lab[t - 1]) atomicOr(fm + (rd >> 5), 1u << (rd & 31));
+  }
+  __syncwarp();
+  // --- pass 2: clump starts (a run start whose run or predecessor run is
+  // fused, or whose label changes); boundaries by popcount prefix
+  int kraw;
+  {
+    int cnt = 0;
+    for (int t0 = 0, c = 0; t0 < n; t0 += 32, ++c) {
+      const int t = t0 + lane;
+      bool st = false;
+      if (t < n && t > 0) {
+        const int rd = rid[t], rd1 = rid[t - 1];
+        if (rd != rd1)
+          st = ((fm[rd >> 5] >> (rd & 31)) & 1u) || ((fm[rd1 >> 5] >> (rd1 & 31)) & 1u) || lab[t] != lab[t - 1];
+      }
+      const uint32_t m = __ballot_sync(0xffffffffu, st);
+      if (lane == 0) sm[c] = m;
+      if (st) cb[cnt + __popc(m & lt) + 1] = t;
+      cnt += __popc(m);
+    }
+    kraw = cnt + 1;
+  }
+  if (vs.qsame && lane == 0)  // for the row-map dedup of larger y's
+    asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(gs.desc + 4 * sub + 2), "r"(kraw) : "memory");
+  if (lane == 0) {
+    cb[0] = 0;
+    cb[kraw] = n;
+  }
+  __syncwarp();
+  // --- superclumps (Alg. 2, partition.cpp:148-165): the ballot greedy of
+  // k_part_f2, then the start mask rebuilt from the group starts
+  int k = kraw;
+  if (kraw > k_hat) {
+    double desired = (double)n / (double)k_hat;
+    int curr = 1, i0 = 0, j = 1;
+    while (j < kraw) {
+      const int jj = j + lane;
+      bool close = false;
+      if (jj < kraw) {
+        const int in_row = cb[jj] - cb[i0], run = cb[jj + 1] - cb[jj];
+        close = fabs((double)(in_row + run) - desired) >= fabs((double)in_row - desired);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, close);
+      if (m) {
+        const int jc = j + __ffs(m) - 1;
+        const int i = cb[jc];
+        ++curr;
+        desired = (double)(n - i) / (double)(k_hat - curr + 1);
+        __syncwarp();
+        if (lane == 0) cb[curr - 1] = i;
+        __syncwarp();
+        i0 = jc;
+        j = jc + 1;
+      } else {
+        j += 32;
+      }
+    }
+    k = curr;
+    __syncwarp();
+    if (lane == 0) cb[k] = n;
+    for (int w = lane; w < nwd; w += 32) sm[w] = 0u;
+    __syncwarp();
+    for (int jj = 1 + lane; jj < k; jj += 32) atomicOr(sm + (cb[jj] >> 5), 1u << (cb[jj] & 31));
+    __syncwarp();
+  }
+  // --- cell counts and the cumulative table cum[r][j] (mutual_info.cpp:9-24)
+  const int kk = k + 1;
+  MB_CHECK(k >= 1 && k <= kc && rows >= 1 && rows <= y && (size_t)rows * kk <= (size_t)y * (kc + 1));
+  for (int i = lane; i < rows * kk; i += 32) cum[i] = 0;
+  __syncwarp();
+  {
+    int cl0 = 0;  // starts before this chunk
+    for (int t0 = 0, c = 0; t0 < n; t0 += 32, ++c) {
+      const int t = t0 + lane;
+      const uint32_t m = sm[c];
+      if (t < n) atomicAdd(cum + (lab[t] - 1) * kk + cl0 + __popc(m & (lt | (1u << lane))) + 1, 1);
+      cl0 += __popc(m);
+    }
+  }
+  __syncwarp();
+  for (int r = 0; r < rows; ++r) {
+    int carry = 0;
+    for (int j0 = 1; j0 <= k; j0 += 32) {
+      const int j = j0 + lane;
+      int v = j <= k ? cum[r * kk + j] : 0;
+      v = warp_incl_scan(v) + carry;
+      if (j <= k) cum[r * kk + j] = v;
+      carry = __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncwarp();
+
+  const int l_max = min(x_max, k);
+  if (counters && lane == 0) {
+    unsigned long long w[kNumCounters] = {};
+    subproblem_work(rows, k, x_max, n, w);
+    for (int i = 0; i < kNumCounters; ++i)
+      if (w[i]) atomicAdd(counters + i, w[i]);
+  }
+  // hand the partition to k_dp_warp (k <= kSmallK) or k_dp
+  if (lane == 0) {
+    reinterpret_cast<int4*>(gs.desc)[sub] = make_int4(k, rows, kraw, l_max);
+    if (l_max >= 3) {
+      if (gs.small_ok && k <= kSmallK) {
+        const unsigned long long q = atomicAdd(grp.cnt + gi, 1ull);
+        MB_CHECK(q < (unsigned long long)grp.nsub);
+        GY.small_list[q] = sub;
+      } else {
+        const unsigned long long q = atomicAdd(grp.cnt + grp.ny + gi, 1ull);
+        MB_CHECK(q < (unsigned long long)grp.nsub);
+        GY.big_list[q] = sub;
+      }
+    }
+  }
+  if (l_max >= 3) {
+    int* gcb = gs.cb + (size_t)sub * (kc + 1);
+    int* gcum = gs.cum + (size_t)sub * gs.cum_stride;
+    for (int j = lane; j <= k; j += 32) gcb[j] = cb[j];
+    for (int i = lane; i < rows * kk; i += 32) gcum[i] = cum[i];
+  }
+  // --- F(t,2) = max_s H(P) - H(P,Q) (mutual_info.cpp:47-56): half-warps per
+  // t up to 16 candidates, then the warp per t; the p*log(p) terms from row
+  // c_t of the table, in the reference's order
+  double* gf2 = gs.f2 + (size_t)sub * (kc + 1);
+  auto f2_best = [&](int t, int hl, int W) {
+    const int ct = cb[t];
+    const double* plt = tb.pl + tri(ct);
+    double best = kLowest;
+    if (rows == 2) {
+      const unsigned uct = ct, ct0 = cum[t], ct1 = cum[kk + t];
+      for (int s = 1 + hl; s < t; s += W) {
+        const unsigned cs = cb[s], a0 = cum[s], a1 = cum[kk + s];
+        const double acc2 = tb.h2 ? h2_at(tb.h2, uct, cs)
+                                  : __dadd_rn(__ldg(plt + cs), __ldg(plt + (uct - cs)));
+        const double j0 = __ldg(plt + a0), j1 = __ldg(plt + a1);
+        const double j2 = __ldg(plt + (ct0 - a0)), j3 = __ldg(plt + (ct1 - a1));
+        const double accj = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(0.0, j0), j1), j2), j3);
+        best = dmax(best, __dsub_rn(-acc2, -accj));
+      }
+    } else {
+      const unsigned uct = ct;
+      for (int s = 1 + hl; s < t; s += W) {
+        const unsigned cs = cb[s];
+        const double acc2 = __dadd_rn(__ldg(plt + cs), __ldg(plt + (uct - cs)));
+        double accj = 0.0;
+        for (int r = 0; r < rows; ++r) accj = __dadd_rn(accj, __ldg(plt + (unsigned)cum[r * kk + s]));
+        for (int r = 0; r < rows; ++r)
+          accj = __dadd_rn(accj, __ldg(plt + ((unsigned)cum[r * kk + t] - (unsigned)cum[r * kk + s])));
+        best = dmax(best, __dsub_rn(-acc2, -accj));
+      }
+    }
+    return best;
+  };
+  double f2k = 0.0;  // F(k, 2), held by the lanes that computed it
+  bool has_k = false;
+  if (k >= 2) {
+    const int t_lo = l_max >= 3 ? 2 : k;
+    const int t_mid = min(k, 17);
+    for (int t2 = t_lo; t2 <= t_mid; t2 += 2) {
+      const int half = lane >> 4, t = t2 + half;
+      const bool ok = t <= t_mid;
+      double best = ok ? f2_best(t, lane & 15, 16) : kLowest;
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) best = dmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+      if (ok && (lane & 15) == 0 && l_max >= 3) gf2[t] = best;
+      if (ok && t == k) {
+        f2k = best;
+        has_k = true;
+      }
+    }
+    for (int t = max(t_lo, t_mid + 1); t <= k; ++t) {
+      const double best = warp_max(f2_best(t, lane, 32));
+      if (lane == 0 && l_max >= 3) gf2[t] = best;
+      if (t == k) {
+        f2k = best;
+        has_k = true;
+      }
+    }
+  }
+  {
+    const unsigned hm = __ballot_sync(0xffffffffu, has_k);
+    if (hm) f2k = __shfl_sync(0xffffffffu, f2k, __ffs(hm) - 1);
+  }
+  if (l_max <= 2) {  // done: I_l = I_2 for every l (mutual_info.cpp:68-70)
+    const double i2 = k >= 2 ? dmax(0.0, __dadd_rn(hq, f2k)) : 0.0;
+    double* oc = ocells + (size_t)pl * 2 * tb.ncell + (size_t)orient * tb.ncell;
+    const double logy = tb.logi[rows];
+    for (int l = 2 + lane; l <= x_max; l += 32) {
+      const int cell = orient ? tb.cell_off[l] + (y - 2) : tb.cell_off[y] + (l - 2);
+      oc[cell] = norm_cell(i2, tb.logi[l], logy);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kWpWarps * 32) k_part_warp(VarSet vs, Tables tb, PairSpace ps,
+                                                            long long base, GenGroup grp, int gi0,
+                                                            int gcount, int per_warp,
+                                                            double* __restrict__ ocells,
+                                                            int orient_only,
+                                                            unsigned long long* counters) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  // persistent warps: items in y-major order from a ticket (grp.cnt[4 ny]),
+  // so a smaller y's subproblem is always taken before (the dedup wait)
+  for (;;) {
+    long long wg = 0;
+    if (lane == 0) wg = (long long)atomicAdd(grp.cnt + 4 * grp.ny, 1ull);
+    wg = __shfl_sync(0xffffffffu, wg, 0);
+    if (wg >= grp.nsub * gcount) return;
+    part_warp_item(vs, tb, ps, base, grp, gi0 + (int)(wg / grp.nsub), wg % grp.nsub, per_warp, ocells,
+                   orient_only, counters, smem + (size_t)wib * per_warp);
   }
 }
 
@@ -1228,6 +1560,35 @@ __global__ void k_copy_dups(VarSet vs, Tables tb, PairSpace ps, long long base, 
   }
 }
 
+// Which y's of a group take k_part_warp: the suffix wp0 .. ny-1 of y's whose
+// clump budget min(n, k_hat) is at most 160000 / n (MINE_B200_WARP_PART_KC
+// overrides; 0 turns the warp kernel off) -- with more clumps the F(t,2)
+// level, not the partition, dominates and the CTA kernel's 4-8 warps per
+// subproblem win (measured: c2, n = 500, fastest with every y here, 13.1 ->
+// 10.8 ms; c0, n = 1000, with k_hat <= 64..160) -- and n <= kWarpPartMaxN
+// with the point arrays on chip, no debug export.  Returns the per-warp
+// shared memory (0: none).
+static size_t warp_part_bytes(int n, const YParams* yps, int ny, bool dbg, int& wp0) {
+  static const int kc_env = [] {
+    const char* e = std::getenv("MINE_B200_WARP_PART_KC");
+    return e ? std::atoi(e) : -1;
+  }();
+  const int kc_max = kc_env >= 0 ? kc_env : std::max(64, 160000 / std::max(n, 1));
+  wp0 = ny;
+  if (kc_max <= 0 || dbg || n > kWarpPartMaxN) return 0;
+  while (wp0 > 0 && gen_kc(n, yps[wp0 - 1]) <= kc_max && !gen_tables_global(n, yps[wp0 - 1]) &&
+         !gen_pts_global(n, yps[wp0 - 1]))
+    --wp0;
+  size_t cum = 0;
+  for (int gi = wp0; gi < ny; ++gi) cum = std::max(cum, (size_t)yps[gi].y * (gen_kc(n, yps[gi]) + 1));
+  const size_t b = wp_layout(n, cum).per_warp;
+  if (wp0 == ny || b * kWpWarps > 200 * 1024) {
+    wp0 = ny;
+    return 0;
+  }
+  return b;
+}
+
 static int launch_copy_dups(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
                             const GenGroup& g, int ny, long long nsub, double* ocells, int orient_only,
                             cudaStream_t s) {
@@ -1275,7 +1636,7 @@ int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long 
     Y.big_list = reinterpret_cast<long long*>(carve(sizeof(long long) * nsub));
   }
   cudaMemcpyAsync(d_ys, hy.data(), sizeof(GenY) * ny, cudaMemcpyHostToDevice, s0);
-  cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 4 * ny, s0);
+  cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * (4 * ny + 4), s0);
   GenGroup g;
   g.ys = d_ys;
   g.ny = ny;
@@ -1285,11 +1646,15 @@ int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long 
   if (dbg) d = *dbg;
   const int dg = dbg ? 1 : 0;
   int launches = 0;
-  // ---- partitions + F(t,2): one launch per run of one variant, y-major
-  for (int gi = 0; gi < ny;) {
+  // ---- partitions + F(t,2): the warp kernel over every (y, subproblem) of
+  // the group when the per-point arrays fit a warp's slice of shared memory,
+  // else one k_part_f2 launch per run of one variant; y-major either way
+  int wp0 = ny;  // the y's from wp0 on take the warp kernel
+  const size_t wpw = warp_part_bytes(n, yps, ny, dbg != nullptr, wp0);
+  for (int gi = 0; gi < wp0;) {
     const int v = pf_variant(n, yps[gi]);
     int gj = gi + 1;
-    while (gj < ny && pf_variant(n, yps[gj]) == v) ++gj;
+    while (gj < wp0 && pf_variant(n, yps[gj]) == v) ++gj;
     size_t sm = 0;
     for (int q = gi; q < gj; ++q) sm = std::max(sm, gen_pf_smem(n, yps[q]));
     const unsigned blocks = (unsigned)(nsub * (gj - gi));
@@ -1304,6 +1669,14 @@ int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long 
 #undef PF_LAUNCH
     ++launches;
     gi = gj;
+  }
+  if (wp0 < ny) {  // after the CTA launches: their y's are smaller (row-map dedup order)
+    const long long warps = nsub * (ny - wp0);
+    const int per = (int)std::max<size_t>(1, std::min<size_t>(4, (228 * 1024) / (kWpWarps * wpw + 1024)));
+    const long long grid = std::min<long long>((warps + kWpWarps - 1) / kWpWarps, (long long)sm_count() * per);
+    k_part_warp<<<(unsigned)grid, kWpWarps * 32, kWpWarps * wpw, s0>>>(
+        vs, tb, ps, base, g, wp0, ny - wp0, (int)wpw, ocells, orient_only, counters);
+    ++launches;
   }
   // ---- levels >= 3: the k_dp runs and the warp path, each on its own lane
   const std::vector<DpRun> runs = dp_runs(n, yps, ny, nsub);
@@ -1383,7 +1756,8 @@ cudaError_t init_general_attributes(int device) {
                        reinterpret_cast<const void*>(k_dp<false, true, false>),
                        reinterpret_cast<const void*>(k_dp<true, true, false>),
                        reinterpret_cast<const void*>(k_dp<true, false, true>),
-                       reinterpret_cast<const void*>(k_dp_warp)};
+                       reinterpret_cast<const void*>(k_dp_warp),
+                       reinterpret_cast<const void*>(k_part_warp)};
   for (const void* f : fns) {
     cudaFuncAttributes fa{};
     e = cudaFuncGetAttributes(&fa, f);

@@ -205,7 +205,7 @@ size_t gen_fslot_bytes(int n, const YParams& yp);
 size_t gen_group_fslot_bytes(int n, const YParams* yps, int ny, long long nsub);
 // Runs the whole general tier for `yps` over pairs [base, base + npairs) of
 // ps: writes both orientations' cells of every y into ocells.  scratch:
-// >= nsub * sum gen_scratch_per_sub; d_ys: >= ny GenY; d_cnt: >= 4 ny
+// >= nsub * sum gen_scratch_per_sub; d_ys: >= ny GenY; d_cnt: >= 4 ny + 4
 // counters; fslots: gen_group_fslot_bytes.  Everything runs on s0 except the
 // warp path, which runs on `side` (if non-null) forked / joined with ev[0],
 // ev[1].  Returns the launch count.
