@@ -218,8 +218,8 @@ struct mine_b200_ctx {
   // and a side stream and its own buffers.
   static constexpr int kGenLanes = 8;
   struct GenLane {
-    cudaStream_t s = nullptr, side = nullptr;
-    cudaEvent_t ev[3] = {};
+    cudaStream_t s = nullptr, side[kGenSides] = {};
+    cudaEvent_t ev[2 + kGenSides] = {};  // fork, side joins, lane done
     DevBuf scr, ys, cnt, fslots;
   } glane[kGenLanes];
   int memo_n = -1, memo_nval = 0;
@@ -350,7 +350,7 @@ int run_gen_group(mine_b200_ctx* ctx, const VarSet& vs, const Tables& tb, const 
     auto& L = ctx->glane[g];
     if (!L.s) {
       CK(cudaStreamCreateWithFlags(&L.s, cudaStreamNonBlocking));
-      CK(cudaStreamCreateWithFlags(&L.side, cudaStreamNonBlocking));
+      for (auto& sd : L.side) CK(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
       for (auto& e : L.ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     std::vector<YParams> mine;
@@ -365,8 +365,8 @@ int run_gen_group(mine_b200_ctx* ctx, const VarSet& vs, const Tables& tb, const 
     CK(cudaStreamWaitEvent(L.s, ctx_event(ctx, 4), 0));
     launches += gen_run_group(vs, tb, pc, 0, npairs, mine.data(), (int)mine.size(), scratch, d_ys, d_cnt,
                               fslots, ocells, dbg, orient_only, dcnt, L.s, L.side, L.ev);
-    CK(cudaEventRecord(L.ev[2], L.s));
-    CK(cudaStreamWaitEvent(s, L.ev[2], 0));
+    CK(cudaEventRecord(L.ev[1 + kGenSides], L.s));
+    CK(cudaStreamWaitEvent(s, L.ev[1 + kGenSides], 0));
   }
   CK(cudaGetLastError());
   return launches;
@@ -914,7 +914,8 @@ void mine_b200_destroy(mine_b200_ctx* ctx) {
   }
   for (auto& L : ctx->glane) {
     if (L.s) cudaStreamDestroy(L.s);
-    if (L.side) cudaStreamDestroy(L.side);
+    for (auto sd : L.side)
+      if (sd) cudaStreamDestroy(sd);
     for (auto e : L.ev)
       if (e) cudaEventDestroy(e);
   }

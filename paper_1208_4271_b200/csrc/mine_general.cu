@@ -1201,14 +1201,18 @@ __global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : 3) k_dp(V
 
 // ---------------------------------------------------------------------------
 // Warp path: one warp per small subproblem (k <= kSmallK), t-outer with the
-// whole F table, the span column and the partition in this warp's slice of
-// shared memory -- no block-level synchronisation, so 16+ independent
-// subproblems interleave per SM.
+// whole F table, the span column and the clump bounds in this warp's slice of
+// shared memory (the cumulative counts are read in place, L1) -- no
+// block-level synchronisation, so 16+ independent subproblems interleave per
+// SM.  The y's are launched in classes of F width (x_max - 1 <= 3, 7, 15,
+// 31, more), each sized for its own widest F: one launch sized for y = 2 left
+// c3's many narrow items (y >= 19, x_max = 3) at one CTA per SM.
 struct WarpLayout {
-  size_t F, A, W, cb, cum, per_warp;
+  size_t F, A, W, cb, per_warp;
 };
 
 __host__ __device__ inline WarpLayout warp_layout(int y, int x_max) {
+  (void)y;
   WarpLayout L;
   size_t o = 0;
   L.F = o;
@@ -1219,10 +1223,12 @@ __host__ __device__ inline WarpLayout warp_layout(int y, int x_max) {
   o += al16(sizeof(double) * (kSmallK + 1));
   L.cb = o;
   o += al16(sizeof(int) * (kSmallK + 1));
-  L.cum = o;
-  o += al16(sizeof(int) * (size_t)y * (kSmallK + 1));
   L.per_warp = o;
   return L;
+}
+__host__ __device__ inline int warp_class(int x_max) {
+  const int w = x_max - 1;
+  return w <= 3 ? 0 : w <= 7 ? 1 : w <= 15 ? 2 : w <= 31 ? 3 : 4;
 }
 
 constexpr int kWarpThreads = 256;
@@ -1265,16 +1271,14 @@ __global__ void __launch_bounds__(kWarpThreads) k_dp_warp(VarSet vs, Tables tb, 
     double* A = reinterpret_cast<double*>(wb + L.A);
     double* W = reinterpret_cast<double*>(wb + L.W);
     int* cb = reinterpret_cast<int*>(wb + L.cb);
-    int* cum = reinterpret_cast<int*>(wb + L.cum);
+    const int* __restrict__ cum = gs.cum + (size_t)sub * gs.cum_stride;  // in place (L1)
     const int4 d = reinterpret_cast<const int4*>(gs.desc)[sub];
     const int k = d.x, rows = d.y, l_max = d.w, kk = k + 1;
     MB_CHECK(k <= kSmallK && rows <= y && l_max <= x_max && sub < grp.nsub);
     {
       const int* gcb = gs.cb + (size_t)sub * (kc + 1);
-      const int* gcum = gs.cum + (size_t)sub * gs.cum_stride;
       const double* gf2 = gs.f2 + (size_t)sub * (kc + 1);
       for (int j = lane; j <= k; j += 32) cb[j] = gcb[j];
-      for (int j = lane; j < rows * kk; j += 32) cum[j] = gcum[j];
       for (int t = 2 + lane; t <= k; t += 32) F[t * LW] = gf2[t];
     }
     __syncwarp();
@@ -1600,8 +1604,8 @@ static int launch_copy_dups(const VarSet& vs, const Tables& tb, const PairSpace&
 int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
                   long long npairs, const YParams* yps, int ny, void* scratch, GenY* d_ys,
                   unsigned long long* d_cnt, double* fslots, double* ocells, const SubDebug* dbg,
-                  int orient_only, unsigned long long* counters, cudaStream_t s0, cudaStream_t side,
-                  cudaEvent_t* ev) {
+                  int orient_only, unsigned long long* counters, cudaStream_t s0,
+                  const cudaStream_t* sides, cudaEvent_t* ev) {
   if (npairs <= 0 || ny <= 0) return 0;
   const int n = vs.n;
   const long long nsub = npairs * (orient_only >= 0 ? 1 : 2);
@@ -1681,12 +1685,10 @@ int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long 
   // ---- levels >= 3: the k_dp runs and the warp path, each on its own lane
   const std::vector<DpRun> runs = dp_runs(n, yps, ny, nsub);
   int wlo = ny, whi = -1;
-  size_t per_warp = 0;
   for (int gi = 0; gi < ny; ++gi)
     if (warp_ok(yps[gi])) {
       wlo = std::min(wlo, gi);
       whi = std::max(whi, gi);
-      per_warp = std::max(per_warp, warp_per_warp(yps[gi]));
     }
   if (runs.empty() && whi < wlo) {
     if (vs.qsame) launches += launch_copy_dups(vs, tb, ps, base, g, ny, nsub, ocells, orient_only, s0);
@@ -1694,43 +1696,95 @@ int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long 
   }
   // the warp path on the side lane (its items are disjoint from k_dp's), the
   // k_dp runs in ascending y on the main lane
-  cudaStream_t sw = s0;
-  if (whi >= wlo && side) {
-    cudaEventRecord(ev[0], s0);
-    cudaStreamWaitEvent(side, ev[0], 0);
-    sw = side;
-  }
-  if (whi >= wlo) {
-    const int warps = kWarpThreads / 32;
-    const size_t sm = per_warp * warps;
-    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / (sm + 1024)));
-    const int grid = (int)std::max<long long>(
-        1, std::min<long long>((nsub * (whi - wlo + 1) + warps - 1) / warps, (long long)sm_count() * per_sm));
-    k_dp_warp<<<grid, kWarpThreads, sm, sw>>>(vs, tb, ps, base, g, wlo, whi - wlo + 1, (int)per_warp,
-                                              ocells, d, dg, orient_only);
-    ++launches;
-  }
+  const bool forked = whi >= wlo && sides && sides[0];
+  if (forked) cudaEventRecord(ev[0], s0);
+  bool used[kGenSides] = {};
+  auto launch_dp = [&] {
   char* fp = reinterpret_cast<char*>(fslots);
-  for (const DpRun& r : runs) {
-    double* fs = reinterpret_cast<double*>(fp);
-    fp += al16(8 * r.fslot_doubles * (size_t)r.grid);
-#define DP_LAUNCH(GT, RG, LN)                                                                 \
-  k_dp<GT, RG, LN><<<r.grid, kDpThreads, r.smem, s0>>>(vs, tb, ps, base, g, r.gi0, r.count, fs, \
-                                                        r.fslot_doubles, ocells, d, dg, orient_only)
-    switch (r.variant) {
-      case kDpGlobalTables: DP_LAUNCH(true, true, false); break;
-      case kDpRing: DP_LAUNCH(false, true, false); break;
-      case kDpWide: DP_LAUNCH(false, false, false); break;
-      case kDpLeanInPlace: DP_LAUNCH(true, false, true); break;
-      default: DP_LAUNCH(false, false, true); break;
+    for (const DpRun& r : runs) {
+      double* fs = reinterpret_cast<double*>(fp);
+      fp += al16(8 * r.fslot_doubles * (size_t)r.grid);
+  #define DP_LAUNCH(GT, RG, LN)                                                                 \
+    k_dp<GT, RG, LN><<<r.grid, kDpThreads, r.smem, s0>>>(vs, tb, ps, base, g, r.gi0, r.count, fs, \
+                                                          r.fslot_doubles, ocells, d, dg, orient_only)
+      switch (r.variant) {
+        case kDpGlobalTables: DP_LAUNCH(true, true, false); break;
+        case kDpRing: DP_LAUNCH(false, true, false); break;
+        case kDpWide: DP_LAUNCH(false, false, false); break;
+        case kDpLeanInPlace: DP_LAUNCH(true, false, true); break;
+        default: DP_LAUNCH(false, false, true); break;
+      }
+  #undef DP_LAUNCH
+      ++launches;
     }
-#undef DP_LAUNCH
-    ++launches;
+  };
+  auto launch_warp = [&] {
+  // the warp path after the k_dp runs are enqueued: the persistent k_dp CTAs
+    // (the long y = 2 items) are dispatched first, the warp CTAs fill the rest
+    // one k_dp_warp launch per F-width class (consecutive y's), in ascending y
+    // Five classes in sequence on one side stream for large batches (c2 -4%,
+    // c3 -2.4% against concurrent), on concurrent side streams for small
+    // ones (c0, 512 subproblems per y: -6%; a class with few long items
+    // would otherwise hold up the next).  MINE_B200_DPW_MODE (A/B): 0 five
+    // classes concurrent, 1 five in sequence, 2 / 3 two classes (F width
+    // <= 7, wider) concurrent / in sequence, 4 one launch.
+    static const int mode_env = [] {
+      const char* e = std::getenv("MINE_B200_DPW_MODE");
+      return e ? std::atoi(e) : -1;
+    }();
+    const int mode = mode_env >= 0 ? mode_env : (nsub > 2048 ? 1 : 0);
+    auto wclass = [&](int x_max) {
+      if (mode == 4) return 0;
+      const int c = warp_class(x_max);
+      return mode >= 2 ? (c <= 1 ? 0 : 1) : c;
+    };
+    const bool seq = mode == 1 || mode == 3;
+    for (int gi = wlo; gi <= whi;) {
+      const int cls = wclass(yps[gi].x_max);
+      int gj = gi;
+      size_t per_warp = 0;
+      while (gj <= whi && warp_ok(yps[gj]) && wclass(yps[gj].x_max) == cls)
+        per_warp = std::max(per_warp, warp_per_warp(yps[gj++]));
+      if (gj == gi) {  // not on the warp path
+        ++gi;
+        continue;
+      }
+      const int warps = kWarpThreads / 32;
+      const size_t sm = per_warp * warps;
+      const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / (sm + 1024)));
+      const int grid = (int)std::max<long long>(
+          1, std::min<long long>((nsub * (gj - gi) + warps - 1) / warps, (long long)sm_count() * per_sm));
+      // each class on its own side stream: the classes run concurrently
+      cudaStream_t sw = s0;
+      if (forked) {
+        const int si = seq ? 0 : cls % kGenSides;
+        sw = sides[si];
+        if (!used[si]) cudaStreamWaitEvent(sw, ev[0], 0);
+        used[si] = true;
+      }
+      k_dp_warp<<<grid, kWarpThreads, sm, sw>>>(vs, tb, ps, base, g, gi, gj - gi, (int)per_warp, ocells, d,
+                                                dg, orient_only);
+      ++launches;
+      gi = gj;
+    }
+  };
+  // MINE_B200_DPW_FIRST=1: the warp path enqueued first (A/B)
+  static const bool warp_first = [] {
+    const char* e = std::getenv("MINE_B200_DPW_FIRST");
+    return e && e[0] == '1';
+  }();
+  if (warp_first) {
+    launch_warp();
+    launch_dp();
+  } else {
+    launch_dp();
+    launch_warp();
   }
-  if (sw != s0) {
-    cudaEventRecord(ev[1], sw);
-    cudaStreamWaitEvent(s0, ev[1], 0);
-  }
+  for (int si = 0; si < kGenSides; ++si)
+    if (used[si]) {
+      cudaEventRecord(ev[1 + si], sides[si]);
+      cudaStreamWaitEvent(s0, ev[1 + si], 0);
+    }
   if (vs.qsame) launches += launch_copy_dups(vs, tb, ps, base, g, ny, nsub, ocells, orient_only, s0);
   return launches;
 }

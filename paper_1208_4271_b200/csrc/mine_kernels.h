@@ -193,6 +193,7 @@ struct GenGroup {
   unsigned long long* cnt = nullptr;
 };
 constexpr int kSmallK = 64;   // subproblems with k <= kSmallK take the warp path
+constexpr int kGenSides = 5;  // side streams of a launch group: one per k_dp_warp F-width class
 int gen_kc(int n, const YParams& yp);
 size_t gen_scratch_per_sub(int n, const YParams& yp);  // incl. list entries
 size_t gen_pts_bytes(int n, const YParams& yp);  // 0: the point arrays fit on chip
@@ -207,13 +208,14 @@ size_t gen_group_fslot_bytes(int n, const YParams* yps, int ny, long long nsub);
 // ps: writes both orientations' cells of every y into ocells.  scratch:
 // >= nsub * sum gen_scratch_per_sub; d_ys: >= ny GenY; d_cnt: >= 4 ny + 4
 // counters; fslots: gen_group_fslot_bytes.  Everything runs on s0 except the
-// warp path, which runs on `side` (if non-null) forked / joined with ev[0],
-// ev[1].  Returns the launch count.
+// warp path, whose launches (one per F-width class) run concurrently on
+// sides[0 .. kGenSides) (when non-null), forked with ev[0] and joined with
+// ev[1 .. kGenSides].  Returns the launch count.
 int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long long base,
                   long long npairs, const YParams* yps, int ny, void* scratch, GenY* d_ys,
                   unsigned long long* d_cnt, double* fslots, double* ocells, const SubDebug* dbg,
-                  int orient_only, unsigned long long* counters, cudaStream_t s0, cudaStream_t side,
-                  cudaEvent_t* ev);
+                  int orient_only, unsigned long long* counters, cudaStream_t s0,
+                  const cudaStream_t* sides, cudaEvent_t* ev);
 cudaError_t init_general_attributes(int device);
 size_t div_table_doubles(int n);
 void launch_build_div(double* div, int n, cudaStream_t s);
