@@ -1458,7 +1458,12 @@ static int sm_count() {
 }
 
 static size_t warp_per_warp(const YParams& yp) { return warp_layout(yp.y, yp.x_max).per_warp; }
-static bool warp_ok(const YParams& yp) { return yp.x_max >= 3 && warp_per_warp(yp) <= 24 * 1024; }
+// The warp path takes y's whose items' tables are small: the cumulative
+// counts are read in place, but their y (kSmallK + 1) ints per item must stay
+// L1-friendly (c4's y ~ 300 items are faster on k_dp).
+static bool warp_ok(const YParams& yp) {
+  return yp.x_max >= 3 && warp_per_warp(yp) + sizeof(int) * (size_t)yp.y * (kSmallK + 1) <= 24 * 1024;
+}
 
 // up to this many samples the F(t,2) level runs on 128 threads too (c2,
 // n = 500: +8%; 64 threads measured slower)
