@@ -956,6 +956,9 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 #ifndef KDP_MIN_BLOCKS
 #define KDP_MIN_BLOCKS 4
 #endif
+#ifndef KDP_CTAS_PER_SM
+#define KDP_CTAS_PER_SM 4
+#endif
 // kLean: x_max <= kLeanXMax (one level tile of <= 62 levels): compiled for 64
 // registers so 4 CTAs share an SM; the wider variants keep 80 (3 per SM).
 
@@ -1526,7 +1529,7 @@ static std::vector<DpRun> dp_runs(int n, const YParams* yps, int ny, long long n
       }
       // up to 4 CTAs per SM, as shared memory allows (the wide variants are
       // register-bound at 3 resident; their extra CTAs start as others finish)
-      const int per = (int)std::max<size_t>(1, std::min<size_t>(4, (228 * 1024) / (r.smem + 1024)));
+      const int per = (int)std::max<size_t>(1, std::min<size_t>(KDP_CTAS_PER_SM, (228 * 1024) / (r.smem + 1024)));
       // the F slots of one run stay within 4 GB (very large c B)
       const long long cap = std::max<long long>(1, (4LL << 30) / (long long)(8 * r.fslot_doubles));
       r.grid = (int)std::min<long long>(std::min<long long>((long long)sms * per, cap),
