@@ -22,3 +22,10 @@ for a in "0 256" "2 20000" "3 2000"; do
   set -- $a
   tools/gen_profile.sh $P $1 $2
 done
+# general-tier top kernels: ncu full set (after the timing runs above exited 0)
+timeout 600 ncu --set full --import-source on --clock-control none -k k_dp -c 1 \
+  -o $P/c3_k_dp python tools/gen_timing.py 3 500 1 > $P/ncu_c3_dp.log 2>&1
+ncu -i $P/c3_k_dp.ncu-rep --page details --csv > $P/c3_k_dp_details.csv 2>/dev/null
+timeout 600 ncu --set full --import-source on --clock-control none -k k_part_warp -c 1 \
+  -o $P/c2_k_part_warp python tools/gen_timing.py 2 4000 1 > $P/ncu_c2_pw.log 2>&1
+ncu -i $P/c2_k_part_warp.ncu-rep --page details --csv > $P/c2_k_part_warp_details.csv 2>/dev/null
