@@ -31,7 +31,7 @@ __host__ __device__ __forceinline__ unsigned h2_off(unsigned m) {
 }
 // H2(m, w) = pl(m, w) + pl(m, m - w): a two-row span's entropy sum, one gather
 __device__ __forceinline__ double h2_at(const double* h2, unsigned m, unsigned w) {
-  return __ldg(h2 + h2_off(m) + min(w, m - w));
+  return __ldg(h2 + (h2_off(m) + min(w, m - w)));  // one 32-bit index: IMAD.WIDE.U32
 }
 
 // std::max / std::min argument order (libstdc++): max(a,b) = a < b ? b : a.

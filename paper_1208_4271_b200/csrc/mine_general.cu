@@ -385,7 +385,10 @@ __global__ void __launch_bounds__(kPfThreads, PF_MINB_THREADS / kPfThreads) k_pa
   // of a W-lane segment (W = 32: a warp; W = 16: a half-warp)
   auto f2_best = [&](int t, int hl, int W) {
     const int ct = cb[t];
-    const double* plt = tb.pl + tri(ct);
+    // p*log(p) row c_t as a 32-bit index base: tri(65535) + 65535 < 2^32, so
+    // every lookup is one IADD + IMAD.WIDE.U32 (64-bit pointer sums cost four)
+    const double* __restrict__ pl = tb.pl;
+    const unsigned plt = tri(ct);
     double best = kLowest;
     if (rows == 2) {
       // two rows (y = 2, the heaviest level): all six gathers of a
@@ -396,9 +399,9 @@ __global__ void __launch_bounds__(kPfThreads, PF_MINB_THREADS / kPfThreads) k_pa
         const unsigned cs = cb[s], a0 = cum[s], a1 = cum[kk + s];
         // H(P) = entropy of (c_s, c_t - c_s): pl + pl, or one H2 gather
         const double acc2 = tb.h2 ? h2_at(tb.h2, uct, cs)
-                                  : __dadd_rn(__ldg(plt + cs), __ldg(plt + (uct - cs)));
-        const double j0 = __ldg(plt + a0), j1 = __ldg(plt + a1);
-        const double j2 = __ldg(plt + (ct0 - a0)), j3 = __ldg(plt + (ct1 - a1));
+                                  : __dadd_rn(__ldg(pl + (plt + cs)), __ldg(pl + (plt + (uct - cs))));
+        const double j0 = __ldg(pl + (plt + a0)), j1 = __ldg(pl + (plt + a1));
+        const double j2 = __ldg(pl + (plt + (ct0 - a0))), j3 = __ldg(pl + (plt + (ct1 - a1)));
         const double accj = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(0.0, j0), j1), j2), j3);
         best = dmax(best, __dsub_rn(-acc2, -accj));
       }
@@ -406,11 +409,11 @@ __global__ void __launch_bounds__(kPfThreads, PF_MINB_THREADS / kPfThreads) k_pa
       const unsigned uct = ct;
       for (int s = 1 + hl; s < t; s += W) {
         const unsigned cs = cb[s];
-        const double acc2 = __dadd_rn(__ldg(plt + cs), __ldg(plt + (uct - cs)));
+        const double acc2 = __dadd_rn(__ldg(pl + (plt + cs)), __ldg(pl + (plt + (uct - cs))));
         double accj = 0.0;
-        for (int r = 0; r < rows; ++r) accj = __dadd_rn(accj, __ldg(plt + (unsigned)cum[r * kk + s]));
+        for (int r = 0; r < rows; ++r) accj = __dadd_rn(accj, __ldg(pl + (plt + (unsigned)cum[r * kk + s])));
         for (int r = 0; r < rows; ++r)
-          accj = __dadd_rn(accj, __ldg(plt + ((unsigned)cum[r * kk + t] - (unsigned)cum[r * kk + s])));
+          accj = __dadd_rn(accj, __ldg(pl + (plt + ((unsigned)cum[r * kk + t] - (unsigned)cum[r * kk + s]))));
         best = dmax(best, __dsub_rn(-acc2, -accj));
       }
     }
@@ -687,16 +690,19 @@ __device__ __forceinline__ void part_warp_item(const VarSet& vs, const Tables& t
   double* gf2 = gs.f2 + (size_t)sub * (kc + 1);
   auto f2_best = [&](int t, int hl, int W) {
     const int ct = cb[t];
-    const double* plt = tb.pl + tri(ct);
+    // p*log(p) row c_t as a 32-bit index base: tri(65535) + 65535 < 2^32, so
+    // every lookup is one IADD + IMAD.WIDE.U32 (64-bit pointer sums cost four)
+    const double* __restrict__ pl = tb.pl;
+    const unsigned plt = tri(ct);
     double best = kLowest;
     if (rows == 2) {
       const unsigned uct = ct, ct0 = cum[t], ct1 = cum[kk + t];
       for (int s = 1 + hl; s < t; s += W) {
         const unsigned cs = cb[s], a0 = cum[s], a1 = cum[kk + s];
         const double acc2 = tb.h2 ? h2_at(tb.h2, uct, cs)
-                                  : __dadd_rn(__ldg(plt + cs), __ldg(plt + (uct - cs)));
-        const double j0 = __ldg(plt + a0), j1 = __ldg(plt + a1);
-        const double j2 = __ldg(plt + (ct0 - a0)), j3 = __ldg(plt + (ct1 - a1));
+                                  : __dadd_rn(__ldg(pl + (plt + cs)), __ldg(pl + (plt + (uct - cs))));
+        const double j0 = __ldg(pl + (plt + a0)), j1 = __ldg(pl + (plt + a1));
+        const double j2 = __ldg(pl + (plt + (ct0 - a0))), j3 = __ldg(pl + (plt + (ct1 - a1)));
         const double accj = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(0.0, j0), j1), j2), j3);
         best = dmax(best, __dsub_rn(-acc2, -accj));
       }
@@ -704,11 +710,11 @@ __device__ __forceinline__ void part_warp_item(const VarSet& vs, const Tables& t
       const unsigned uct = ct;
       for (int s = 1 + hl; s < t; s += W) {
         const unsigned cs = cb[s];
-        const double acc2 = __dadd_rn(__ldg(plt + cs), __ldg(plt + (uct - cs)));
+        const double acc2 = __dadd_rn(__ldg(pl + (plt + cs)), __ldg(pl + (plt + (uct - cs))));
         double accj = 0.0;
-        for (int r = 0; r < rows; ++r) accj = __dadd_rn(accj, __ldg(plt + (unsigned)cum[r * kk + s]));
+        for (int r = 0; r < rows; ++r) accj = __dadd_rn(accj, __ldg(pl + (plt + (unsigned)cum[r * kk + s])));
         for (int r = 0; r < rows; ++r)
-          accj = __dadd_rn(accj, __ldg(plt + ((unsigned)cum[r * kk + t] - (unsigned)cum[r * kk + s])));
+          accj = __dadd_rn(accj, __ldg(pl + (plt + ((unsigned)cum[r * kk + t] - (unsigned)cum[r * kk + s]))));
         best = dmax(best, __dsub_rn(-acc2, -accj));
       }
     }
@@ -868,7 +874,8 @@ __device__ __forceinline__ void span_terms(const Tables& tb, const int* cb, cons
   const int w0 = threadIdx.x >> 5;
   for (int base = 0; base < ns; base += 4 * nw) {
     int cs[4];
-    const double* plm[4];
+    unsigned plm[4];  // 32-bit row bases (one IMAD.WIDE.U32 per lookup)
+    const double* __restrict__ pl = tb.pl;
     bool ok[4];
     double acch[4];
 #pragma unroll
@@ -876,7 +883,7 @@ __device__ __forceinline__ void span_terms(const Tables& tb, const int* cb, cons
       const int sl = base + w0 + e * nw, s = s0 + sl;
       ok[e] = sl < ns && s < t;
       cs[e] = ok[e] ? cb[s] : ct;
-      plm[e] = tb.pl + tri(ct - cs[e]);
+      plm[e] = tri(ct - cs[e]);
       acch[e] = 0.0;
     }
     int r = 0;
@@ -900,8 +907,8 @@ __device__ __forceinline__ void span_terms(const Tables& tb, const int* cb, cons
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int s = s0 + base + w0 + e * nw;
-        v[0][e] = ok[e] ? __ldg(plm[e] + (ctr0 - (unsigned)cum[r * kk + s])) : 0.0;
-        v[1][e] = ok[e] ? __ldg(plm[e] + (ctr1 - (unsigned)cum[(r + 1) * kk + s])) : 0.0;
+        v[0][e] = ok[e] ? __ldg(pl + (plm[e] + (ctr0 - (unsigned)cum[r * kk + s]))) : 0.0;
+        v[1][e] = ok[e] ? __ldg(pl + (plm[e] + (ctr1 - (unsigned)cum[(r + 1) * kk + s]))) : 0.0;
       }
 #pragma unroll
       for (int e = 0; e < 4; ++e) acch[e] = __dadd_rn(__dadd_rn(acch[e], v[0][e]), v[1][e]);
@@ -913,7 +920,7 @@ __device__ __forceinline__ void span_terms(const Tables& tb, const int* cb, cons
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int s = s0 + base + w0 + e * nw;
-        v[e] = ok[e] ? __ldg(plm[e] + (ctr - (unsigned)cum[r * kk + s])) : 0.0;
+        v[e] = ok[e] ? __ldg(pl + (plm[e] + (ctr - (unsigned)cum[r * kk + s]))) : 0.0;
       }
 #pragma unroll
       for (int e = 0; e < 4; ++e) acch[e] = __dadd_rn(acch[e], v[e]);
@@ -1291,7 +1298,8 @@ __global__ void __launch_bounds__(kWarpThreads) k_dp_warp(VarSet vs, Tables tb, 
       const double dct = (double)ct, rct = __drcp_rn(dct);
       for (int s = 2 + lane; s < t; s += 32) {
         const int cs = cb[s];
-        const double* plm = tb.pl + tri(ct - cs);
+        const unsigned plm = tri(ct - cs);  // 32-bit row base
+        const double* __restrict__ pl = tb.pl;
         double acch = 0.0;
         int r = 0;
         if (rows == 2 && tb.h2) {  // the two-row sum as one H2 gather
@@ -1299,12 +1307,12 @@ __global__ void __launch_bounds__(kWarpThreads) k_dp_warp(VarSet vs, Tables tb, 
           r = rows;
         }
         for (; r + 2 <= rows; r += 2) {  // two gathers in flight, added in row order
-          const double v0 = __ldg(plm + ((unsigned)cum[r * kk + t] - (unsigned)cum[r * kk + s]));
-          const double v1 = __ldg(plm + ((unsigned)cum[(r + 1) * kk + t] - (unsigned)cum[(r + 1) * kk + s]));
+          const double v0 = __ldg(pl + (plm + ((unsigned)cum[r * kk + t] - (unsigned)cum[r * kk + s])));
+          const double v1 = __ldg(pl + (plm + ((unsigned)cum[(r + 1) * kk + t] - (unsigned)cum[(r + 1) * kk + s])));
           acch = __dadd_rn(__dadd_rn(acch, v0), v1);
         }
         if (r < rows)
-          acch = __dadd_rn(acch, __ldg(plm + ((unsigned)cum[r * kk + t] - (unsigned)cum[r * kk + s])));
+          acch = __dadd_rn(acch, __ldg(pl + (plm + ((unsigned)cum[r * kk + t] - (unsigned)cum[r * kk + s]))));
         double a, q;
         if (tb.div) {
           const double* dr = tb.div + tri(ct);
