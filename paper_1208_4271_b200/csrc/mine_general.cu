@@ -830,7 +830,7 @@ __host__ __device__ inline DpLayout dp_layout(int y, int kc, int x_max, bool glo
   if (!global_tables) o += al16(sizeof(int) * (size_t)y * (kc + 1));
   L.A = o;
   o += al16(sizeof(double) * kMaxTile * kMaxTile);
-  L.W = o;
+  L.W = o;  // = L.A + kMaxTile^2 doubles (the accumulation loop relies on it)
   o += al16(sizeof(double) * kMaxTile * kMaxTile);
   // compact widths for the lean variant only (gen_dp_lean); the others use
   // 64 / 65
@@ -1121,12 +1121,16 @@ __global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : 3) k_dp(V
                   acc[4 + i] = dmax(acc[4 + i], __dsub_rn(__dmul_rn(a.y, f), w.y));
                 }
             }
+            // running addresses (W sits kMaxTile^2 doubles after A): the loop
+            // body is the 4 loads and the 8 candidates, no index arithmetic
+            const double* ap = A + sl * kMaxTile + my_tl;
+            const double* fp = fr + sl * fsw;
 #pragma unroll 2
-            for (; sl < ns; ++sl) {
-              const double2 a = *reinterpret_cast<const double2*>(A + sl * kMaxTile + my_tl);
-              const double2 w = *reinterpret_cast<const double2*>(W + sl * kMaxTile + my_tl);
-              const double2 f01 = *reinterpret_cast<const double2*>(fr + sl * fsw);
-              const double2 f23 = *reinterpret_cast<const double2*>(fr + sl * fsw + fo);
+            for (; sl < ns; ++sl, ap += kMaxTile, fp += fsw) {
+              const double2 a = *reinterpret_cast<const double2*>(ap);
+              const double2 w = *reinterpret_cast<const double2*>(ap + kMaxTile * kMaxTile);
+              const double2 f01 = *reinterpret_cast<const double2*>(fp);
+              const double2 f23 = *reinterpret_cast<const double2*>(fp + fo);
               acc[0] = dmax(acc[0], __dsub_rn(__dmul_rn(a.x, f01.x), w.x));
               acc[1] = dmax(acc[1], __dsub_rn(__dmul_rn(a.x, f01.y), w.x));
               acc[2] = dmax(acc[2], __dsub_rn(__dmul_rn(a.x, f23.x), w.x));
