@@ -862,7 +862,10 @@ __host__ __device__ inline DpLayout dp_layout(int y, int kc, int x_max, bool glo
 __device__ __forceinline__ void span_terms(const Tables& tb, const int* cb, const int* cum, int kk,
                                            int rows, int k, int s0, int ns, int t0, int nt,
                                            double* A, double* W) {
-  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  // k_dp's block size is a compile-time constant: no blockDim reads (the
+  // compiler rematerialises the index math under k_dp's register budget)
+  constexpr int nw = kDpThreads >> 5;
+  const int lane = threadIdx.x & 31;
   // a lane keeps one t (nt <= 32): c_t and its reciprocal once per call
   const int tl = lane, t = t0 + tl;
   if (tl >= nt || t > k) return;
