@@ -411,9 +411,14 @@ __global__ void __launch_bounds__(kPfThreads, PF_MINB_THREADS / kPfThreads) k_pa
         const unsigned cs = cb[s];
         const double acc2 = __dadd_rn(__ldg(pl + (plt + cs)), __ldg(pl + (plt + (uct - cs))));
         double accj = 0.0;
-        for (int r = 0; r < rows; ++r) accj = __dadd_rn(accj, __ldg(pl + (plt + (unsigned)cum[r * kk + s])));
-        for (int r = 0; r < rows; ++r)
-          accj = __dadd_rn(accj, __ldg(pl + (plt + ((unsigned)cum[r * kk + t] - (unsigned)cum[r * kk + s]))));
+        // columns s and t of cum walked by pointer (stride kk): one IADD per
+        // row instead of re-deriving r * kk + s
+        const int* cps = cum + s;
+        for (int r = 0; r < rows; ++r, cps += kk) accj = __dadd_rn(accj, __ldg(pl + (plt + (unsigned)*cps)));
+        const int* cpt = cum + t;
+        cps = cum + s;
+        for (int r = 0; r < rows; ++r, cps += kk, cpt += kk)
+          accj = __dadd_rn(accj, __ldg(pl + (plt + ((unsigned)*cpt - (unsigned)*cps))));
         best = dmax(best, __dsub_rn(-acc2, -accj));
       }
     }
@@ -712,9 +717,14 @@ __device__ __forceinline__ void part_warp_item(const VarSet& vs, const Tables& t
         const unsigned cs = cb[s];
         const double acc2 = __dadd_rn(__ldg(pl + (plt + cs)), __ldg(pl + (plt + (uct - cs))));
         double accj = 0.0;
-        for (int r = 0; r < rows; ++r) accj = __dadd_rn(accj, __ldg(pl + (plt + (unsigned)cum[r * kk + s])));
-        for (int r = 0; r < rows; ++r)
-          accj = __dadd_rn(accj, __ldg(pl + (plt + ((unsigned)cum[r * kk + t] - (unsigned)cum[r * kk + s]))));
+        // columns s and t of cum walked by pointer (stride kk): one IADD per
+        // row instead of re-deriving r * kk + s
+        const int* cps = cum + s;
+        for (int r = 0; r < rows; ++r, cps += kk) accj = __dadd_rn(accj, __ldg(pl + (plt + (unsigned)*cps)));
+        const int* cpt = cum + t;
+        cps = cum + s;
+        for (int r = 0; r < rows; ++r, cps += kk, cpt += kk)
+          accj = __dadd_rn(accj, __ldg(pl + (plt + ((unsigned)*cpt - (unsigned)*cps))));
         best = dmax(best, __dsub_rn(-acc2, -accj));
       }
     }
