@@ -1196,16 +1196,23 @@ __global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : 3) k_dp(V
           }
           if (sb1 >= nt) break;
           __syncthreads();
-          // rows [sb1, nt) x levels: candidates s in [t0 + sb0, t0 + sb1)
-          const int ncell = (nt - sb1) * nl;
-          for (int c = tid; c < ncell; c += kDpThreads) {
-            const int tl = sb1 + c / nl, ll = c - (c / nl) * nl, l = l0 + ll, tt = t0 + tl;
-            if (tt < l || (l == l_max && tt != k)) continue;
-            double* slot = accS + ((tl >> 1) * ng + (ll >> 2)) * kAccStride + (tl & 1) * 4 + (ll & 3);
-            double m = *slot;
-            for (int sl = max(sb0, l - 1 - t0); sl < sb1; ++sl)
-              m = dmax(m, __dsub_rn(__dmul_rn(A[sl * kMaxTile + tl], ft[sl * ftw + ll]), W[sl * kMaxTile + tl]));
-            *slot = m;
+          // rows [sb1, nt) x levels: candidates s in [t0 + sb0, t0 + sb1);
+          // cell (tl, ll) = (sb1, 0) + thread index, walked without a division
+          for (int tl = sb1 + st_sl, ll = st_j; tl < nt;) {
+            const int l = l0 + ll, tt = t0 + tl;
+            if (tt >= l && !(l == l_max && tt != k)) {
+              double* slot = accS + ((tl >> 1) * ng + (ll >> 2)) * kAccStride + (tl & 1) * 4 + (ll & 3);
+              double m = *slot;
+              for (int sl = max(sb0, l - 1 - t0); sl < sb1; ++sl)
+                m = dmax(m, __dsub_rn(__dmul_rn(A[sl * kMaxTile + tl], ft[sl * ftw + ll]), W[sl * kMaxTile + tl]));
+              *slot = m;
+            }
+            tl += st_dsl;
+            ll += st_dj;
+            if (ll >= nl) {
+              ll -= nl;
+              ++tl;
+            }
           }
           __syncthreads();
         }
