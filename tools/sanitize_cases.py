@@ -48,6 +48,11 @@ def main():
     p0 = Parameters(w0.alpha, w0.c, w0.est)
     check(eng.pairs(w0.X, w0.xi, w0.yi, p0, cells=True), orc.pairs(w0.X, w0.xi, w0.yi, w0.alpha, w0.c, w0.est),
           "general c0 (lean k_dp, warp path, both k_part_f2 widths)")
+    w2 = datagen.make(2)
+    V2 = w2.X[[0, 1, 2, 3, 10, 11, 500, 501, 1000, 1001, 1998, 1999, 7, 8, 9, 40, 41, 42]]
+    p2 = Parameters(w2.alpha, w2.c, w2.est)
+    check(eng.pairwise(V2, p2), orc.pairwise(V2, w2.alpha, w2.c, w2.est),
+          "general c2 ties (row-map dedup, warp partition kernel, warp DP width classes)")
     xs, ys = [], []
     for it in range(8):
         x, y = random_pair(rng, 300, it % 4)
