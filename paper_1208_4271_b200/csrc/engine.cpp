@@ -517,7 +517,7 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
       ++ctx->launches;
     }
   } else if (row_dedup_on()) {  // general tier: row-map equality of consecutive y's
-    vs.qsame = static_cast<uint8_t*>(ctx->qsame.ensure((size_t)V * ny));
+    vs.qsame = static_cast<uint16_t*>(ctx->qsame.ensure(sizeof(uint16_t) * (size_t)V * ny));
     if (!P.qsame) {
       launch_row_same(vs, s);
       ++ctx->launches;

@@ -124,9 +124,7 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
 // Only y's of this group count (their descriptors are live).
 __device__ __forceinline__ int canonical_gi(const VarSet& vs, const GenGroup& grp, int gi, int Yv) {
   const int yi = grp.ys[gi].yp.yi;
-  const uint8_t* same = vs.qsame + (size_t)Yv * vs.ny;
-  int yc = yi;
-  while (yc > 0 && same[yc]) --yc;
+  const int yc = vs.qsame[(size_t)Yv * vs.ny + yi];
   if (yc == yi) return gi;
   const int gc = gi - (yi - yc);  // the group's y's are consecutive
   return gc >= 0 && grp.ys[gc].yp.yi == yc ? gc : gi;

@@ -184,27 +184,34 @@ __global__ void k_equipartition(VarSet vs, Tables tb) {
   }
 }
 
-// Row-map equality of consecutive row targets: qsame[v][yi] = 1 iff
-// Q(v, y) == Q(v, y - 1) label for label (same rows; ties make the greedy
-// scan saturate, e.g. a Poisson variable with 5 distinct values has the same
-// rows for every y >= 5).  Subproblems whose row map equals a smaller y's
-// need no partition or DP when their raw clumps do not superclump
-// (k_part_f2: the cells are the smaller y's).  One warp per
-// (variable, yi); the label compare runs only when the row counts agree.
+// Row-map equality of consecutive row targets, as the canonical row target:
+// qsame[v][yi] = the smallest yi' whose row map equals yi's label for label
+// (ties make the greedy scan saturate, e.g. a Poisson variable with 5
+// distinct values has the same rows for every y >= 5; only consecutive y's
+// are compared).  Subproblems whose row map equals a smaller y's need no
+// partition or DP when their raw clumps do not superclump (k_part_f2 /
+// k_part_warp: the cells are the smaller y's).  One warp per
+// variable walks its y's; the label compare runs only when the row counts
+// agree.
 __global__ void k_row_same(VarSet vs) {
-  const long long idx = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long var = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (idx >= (long long)vs.V * vs.ny) return;
-  const int yi = (int)(idx % vs.ny), n = vs.n;
-  bool same = yi > 0 && vs.yhat[idx] == vs.yhat[idx - 1];
-  if (same) {
-    const uint16_t* a = vs.q + (size_t)idx * n;
-    const uint16_t* b = a - n;
-    bool diff = false;
-    for (int t = lane; t < n; t += 32) diff |= a[t] != b[t];
-    same = !__any_sync(0xffffffffu, diff);
+  if (var >= vs.V) return;
+  const int n = vs.n;
+  const size_t row0 = (size_t)var * vs.ny;
+  int canon = 0;
+  for (int yi = 0; yi < vs.ny; ++yi) {
+    bool same = yi > 0 && vs.yhat[row0 + yi] == vs.yhat[row0 + yi - 1];
+    if (same) {
+      const uint16_t* a = vs.q + (row0 + yi) * n;
+      const uint16_t* b = a - n;
+      bool diff = false;
+      for (int t = lane; t < n; t += 32) diff |= a[t] != b[t];
+      same = !__any_sync(0xffffffffu, diff);
+    }
+    if (!same) canon = yi;
+    if (lane == 0) vs.qsame[row0 + yi] = (uint16_t)canon;
   }
-  if (lane == 0) vs.qsame[idx] = same ? 1 : 0;
 }
 
 // Tiny-tier packing: per sample the labels of y=2 and y=3 in one byte, and the
@@ -1455,7 +1462,7 @@ void launch_equipartition(const VarSet& vs, const Tables& tb, cudaStream_t s) {
 }
 
 void launch_row_same(const VarSet& vs, cudaStream_t s) {
-  const long long warps = (long long)vs.V * vs.ny;
+  const long long warps = (long long)vs.V;
   k_row_same<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(vs);
 }
 

@@ -24,7 +24,7 @@ struct VarSet {
   uint16_t* q = nullptr;         // V x ny x n row label (1-based) of each sample
   int* yhat = nullptr;           // V x ny     realised row count
   double* hq = nullptr;          // V x ny     H(Q), reference-exact (mutual_info.cpp:33)
-  uint8_t* qsame = nullptr;      // V x ny     general tier: Q(y) == Q(y - 1) (k_row_same), or null
+  uint16_t* qsame = nullptr;     // V x ny     general tier: smallest yi' with Q(yi') == Q(yi) (k_row_same), or null
   uint8_t* lw = nullptr;         // V x n      tiny tier: packed labels (y=2: bits 0-1, y=3: 2-3)
   uint32_t* rsmask = nullptr;    // V          tiny tier: run-start bitmask over sorted positions
   uint4* rec = nullptr;          // V x 6      memo tier: 96-byte per-variable record
