@@ -1242,6 +1242,10 @@ __global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : 3) k_dp(V
 // SM.  The y's are launched in classes of F width (x_max - 1 <= 3, 7, 15,
 // 31, more), each sized for its own widest F: one launch sized for y = 2 left
 // c3's many narrow items (y >= 19, x_max = 3) at one CTA per SM.
+#ifndef KDPW_SPAN_T
+#define KDPW_SPAN_T 2  // measured: 2 best (c0 -5.6%, c2 -3.1%); 4 and 8 cost occupancy
+#endif
+constexpr int kWarpSpanT = KDPW_SPAN_T;  // span columns gathered together
 struct WarpLayout {
   size_t F, A, W, cb, per_warp;
 };
@@ -1253,9 +1257,9 @@ __host__ __device__ inline WarpLayout warp_layout(int y, int x_max) {
   L.F = o;
   o += al16(sizeof(double) * (kSmallK + 1) * (size_t)(x_max - 1));
   L.A = o;
-  o += al16(sizeof(double) * (kSmallK + 1));
+  o += al16(sizeof(double) * kWarpSpanT * (kSmallK + 1));
   L.W = o;
-  o += al16(sizeof(double) * (kSmallK + 1));
+  o += al16(sizeof(double) * kWarpSpanT * (kSmallK + 1));
   L.cb = o;
   o += al16(sizeof(int) * (kSmallK + 1));
   L.per_warp = o;
@@ -1307,8 +1311,10 @@ __global__ void __launch_bounds__(kWarpThreads, kMinBlocks) k_dp_warp(VarSet vs,
     const WarpLayout L = warp_layout(y, x_max);
     MB_CHECK(L.per_warp <= (size_t)per_warp);
     double* F = reinterpret_cast<double*>(wb + L.F);
-    double* A = reinterpret_cast<double*>(wb + L.A);
+    double* A = reinterpret_cast<double*>(wb + L.A);  // kWarpSpanT columns of kSmallK + 1
     double* W = reinterpret_cast<double*>(wb + L.W);
+    double* const A0 = A;
+    double* const W0 = W;
     int* cb = reinterpret_cast<int*>(wb + L.cb);
     const int* __restrict__ cum = gs.cum + (size_t)sub * gs.cum_stride;  // in place (L1)
     const int4 d = reinterpret_cast<const int4*>(gs.desc)[sub];
@@ -1321,11 +1327,23 @@ __global__ void __launch_bounds__(kWarpThreads, kMinBlocks) k_dp_warp(VarSet vs,
       for (int t = 2 + lane; t <= k; t += 32) F[t * LW] = gf2[t];
     }
     __syncwarp();
-    for (int t = 3; t <= k; ++t) {
-      // span column A(s,t), W(s,t) for s in [2, t)
-      const int ct = cb[t];
-      const double dct = (double)ct, rct = __drcp_rn(dct);
-      for (int s = 2 + lane; s < t; s += 32) {
+    // span columns in blocks of kWarpSpanT t's: their entries (independent
+    // of the DP) are gathered together -- one column at a time left each t's
+    // L2 latency exposed, with few lanes busy at small t
+    for (int tb0 = 3; tb0 <= k; tb0 += kWarpSpanT) {
+      const int tb1 = min(tb0 + kWarpSpanT - 1, k);
+      // entries (s, t), t in [tb0, tb1], s in [2, t): column j = t - tb0
+      // starts at entry off_j = sum_{i<j} (tb0 + i - 2)
+      const int nent = (tb1 - tb0 + 1) * (tb0 - 2) + (tb1 - tb0) * (tb1 - tb0 + 1) / 2;
+      for (int e = lane; e < nent; e += 32) {
+        int j = 0, off = 0;
+        while (j + 1 <= tb1 - tb0 && e >= off + (tb0 + j - 2)) {
+          off += tb0 + j - 2;
+          ++j;
+        }
+        const int t = tb0 + j, s = 2 + (e - off);
+        const int ct = cb[t];
+        const double dct = (double)ct, rct = __drcp_rn(dct);
         const int cs = cb[s];
         const unsigned plm = tri(ct - cs);  // 32-bit row base
         const double* __restrict__ pl = tb.pl;
@@ -1352,10 +1370,13 @@ __global__ void __launch_bounds__(kWarpThreads, kMinBlocks) k_dp_warp(VarSet vs,
           a = int_quot(dcs, dct, rct);
           q = int_quot(__dsub_rn(dct, dcs), dct, rct);
         }
-        A[s] = a;
-        W[s] = __dmul_rn(q, -acch);
+        A[j * (kSmallK + 1) + s] = a;
+        W[j * (kSmallK + 1) + s] = __dmul_rn(q, -acch);
       }
       __syncwarp();
+    for (int t = tb0; t <= tb1; ++t) {
+      const double* A = A0 + (t - tb0) * (kSmallK + 1);
+      const double* W = W0 + (t - tb0) * (kSmallK + 1);
       // levels 3 .. l_hi of row t: P lanes per level (P = 32 / levels,
       // rounded down to a power of two) split the split points s by phase and
       // max-reduce by shuffles -- large y have few levels, and one lane per
@@ -1380,6 +1401,7 @@ __global__ void __launch_bounds__(kWarpThreads, kMinBlocks) k_dp_warp(VarSet vs,
         }
       }
       __syncwarp();
+    }
     }
     // I_l (mutual_info.cpp:68-70) and the cells (char_matrix.cpp:57-64)
     const long long pl = base + sub / norient;
