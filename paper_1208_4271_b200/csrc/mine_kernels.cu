@@ -86,6 +86,65 @@ __global__ void k_sort_vars(VarSet vs) {
   }
 }
 
+// K1 for 64 < n <= kBitonicMaxN: a bitonic sort of (order key, sample index)
+// pairs in shared memory -- O(n log^2 n) compare-exchanges instead of
+// k_sort_vars' O(n^2) ranking (c0's 512 variables of n = 1000: 8% of the call).
+// Sorting by (key, index) is the stable order of the ranking (ties by sample
+// index); keys map -0.0 to +0.0 and NaN to +inf exactly as k_sort_vars
+// compares (order_key below).  Padding keys (all ones) sort last.
+__device__ __forceinline__ unsigned long long order_key(double x);
+constexpr int kBitonicMaxN = 8192;
+__global__ void k_sort_bitonic(VarSet vs, int N) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = vs.n, tid = threadIdx.x;
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(smem);
+  uint16_t* idx = reinterpret_cast<uint16_t*>(key + N);
+  int* rs = reinterpret_cast<int*>(smem + 8 * (size_t)N + ((2 * (size_t)N + 15) & ~size_t(15)));
+  int* tmp = rs + n;
+  const int var = blockIdx.x;
+  const double* src = vs.vals + (size_t)var * n;
+  for (int i = tid; i < N; i += blockDim.x) {
+    key[i] = i < n ? order_key(src[i]) : ~0ull;
+    idx[i] = (uint16_t)(i < n ? i : 0xffff);
+  }
+  for (int size = 2; size <= N; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int i = tid; i < (N >> 1); i += blockDim.x) {
+        const int a = 2 * i - (i & (stride - 1)), b = a + stride;
+        const unsigned long long ka = key[a], kb = key[b];
+        const uint16_t ia = idx[a], ib = idx[b];
+        const bool gt = ka > kb || (ka == kb && ia > ib);
+        if (gt == ((a & size) == 0)) {
+          key[a] = kb;
+          key[b] = ka;
+          idx[a] = ib;
+          idx[b] = ia;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  int* perm = vs.perm + (size_t)var * n;
+  for (int i = tid; i < n; i += blockDim.x) {
+    perm[i] = idx[i];
+    rs[i] = i == 0 || key[i] != key[i - 1];
+  }
+  __syncthreads();
+  const int runs = block_incl_scan(rs, n, tmp);
+  int* runid = vs.runid + (size_t)var * n;
+  int* rstart = vs.runstart + (size_t)var * (n + 1);
+  for (int i = tid; i < n; i += blockDim.x) {
+    const int r = rs[i] - 1;
+    runid[i] = r;
+    if (i == 0 || rs[i - 1] != rs[i]) rstart[r] = i;
+  }
+  if (tid == 0) {
+    rstart[runs] = n;
+    vs.nruns[var] = runs;
+  }
+}
+
 // K1 for large n (the 12n-byte working set of k_sort_vars no longer fits on
 // chip, or the O(n^2) ranking costs more than a sort): a stable segmented
 // radix sort of order-preserving 64-bit keys (cub), then the tie-run scan.
@@ -1362,6 +1421,7 @@ cudaError_t init_kernel_attributes(int device) {
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (e != cudaSuccess) return e;
   const void* fns[] = {reinterpret_cast<const void*>(k_sort_vars),
+                       reinterpret_cast<const void*>(k_sort_bitonic),
                        reinterpret_cast<const void*>(k_memo_pairs<false, false, 23, 8192, 20>),
                        reinterpret_cast<const void*>(k_memo_pairs<false, false, 23, 8192, 21>),
                        reinterpret_cast<const void*>(k_memo_pairs<false, false, 23, 8192, 22>),
@@ -1431,7 +1491,24 @@ size_t sort_scratch_bytes(int V, int n) {
   return 2 * 8 * items + 4 * items + 4 * (size_t)(V + 1) + 3 * 256 + cub_sort_bytes(V, n);
 }
 
+// MINE_B200_BITONIC=0: the O(n^2) ranking for every n <= kRadixSortN (A/B)
+static bool bitonic_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("MINE_B200_BITONIC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 cudaError_t launch_sort_vars(const VarSet& vs, void* scratch, cudaStream_t s) {
+  if (vs.n > 64 && vs.n <= kBitonicMaxN && bitonic_on()) {
+    int N = 128;
+    while (N < vs.n) N <<= 1;
+    const int threads = std::min(1024, std::max(128, N / 2));
+    const size_t sm = 8 * (size_t)N + ((2 * (size_t)N + 15) & ~size_t(15)) + sizeof(int) * (vs.n + 64);
+    k_sort_bitonic<<<vs.V, threads, sm, s>>>(vs, N);
+    return cudaGetLastError();
+  }
   if (!radix_sort_vars(vs.n)) {
     const int threads = vs.n <= 256 ? 128 : (vs.n <= 2048 ? 256 : 1024);
     const size_t sm = sizeof(double) * vs.n + sizeof(int) * (vs.n + 64);

@@ -630,3 +630,42 @@ def test_row_dedup_off_same_bits(tmp_path):
         subprocess.run([sys.executable, str(script), str(out)], env=env, check=True, timeout=600)
         outs.append(np.load(out))
     assert_bit_equal(outs[1], outs[0], "row-map dedup vs every subproblem computed")
+
+
+def test_bitonic_sort_same_bits(tmp_path):
+    """K1's bitonic shared-memory sort (64 < n <= 8192) gives the O(n^2)
+    ranking's bits (MINE_B200_BITONIC=0): ties, -0.0 against +0.0, huge and
+    tiny magnitudes, constant variables, n not a power of two; statistics,
+    cells and the debug partition."""
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "run.py"
+    script.write_text(
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        "from paper_1208_4271_b200 import Engine, Parameters\n"
+        "rng = np.random.default_rng(5)\n"
+        "e = Engine(0)\n"
+        "out = []\n"
+        "for n in (65, 100, 333, 1000, 2049):\n"
+        "    V = rng.standard_normal((10, n))\n"
+        "    V[1] = np.round(V[1] * 2)\n"
+        "    V[2, ::3] = -0.0\n"
+        "    V[2, 1::3] = 0.0\n"
+        "    V[3] = 7.0\n"
+        "    V[4] *= 1e300\n"
+        "    V[5] *= 1e-300\n"
+        "    V[6] = rng.integers(0, 3, n)\n"
+        "    r = e.pairwise(V, Parameters(0.6, 15.0, 1), cells=True)\n"
+        "    out += [np.stack([r[k] for k in ('mic', 'mas', 'mev', 'mcn', 'mic_e', 'tic')]).ravel(), r['cells'].ravel()]\n"
+        "    d = e.debug_subproblem(V[1], V[6], 2, 5, 30)\n"
+        "    out += [np.asarray(d['bounds'], float), np.asarray(d['q_x'], float)]\n"
+        "np.save(sys.argv[1], np.concatenate(out))\n")
+    outs = []
+    for flag in ("0", "1"):
+        out = tmp_path / f"o{flag}.npy"
+        env = dict(os.environ, MINE_B200_BITONIC=flag)
+        subprocess.run([sys.executable, str(script), str(out)], env=env, check=True, timeout=600)
+        outs.append(np.load(out))
+    assert_bit_equal(outs[1], outs[0], "bitonic sort vs ranking")
