@@ -318,9 +318,18 @@ def run_ours(args, world, rank, local):
             for k in outs:
                 dist.all_gather_into_tensor(gathered[k], outs[k])
 
-    for _ in range(args.warmup):
+    # the first call pays the per-n constants (host-built glibc p*log(p)
+    # triangle, memo tables, kernel attributes), cached on the context for
+    # every later call: reported as setup, outside the steps
+    torch.cuda.synchronize()
+    first_call_ms = None
+    t_setup = time.perf_counter()
+    for i in range(args.warmup):
         flush.zero_()
         step()
+        if i == 0:
+            torch.cuda.synchronize()
+            first_call_ms = (time.perf_counter() - t_setup) * 1e3
     torch.cuda.synchronize()
     # untimed instrumented pass: realised algorithmic work of one step
     work = eng.pairwise_device(dv.data_ptr(), p, n, params, ptrs, stream=stream.cuda_stream,
@@ -429,6 +438,10 @@ def run_ours(args, world, rank, local):
             "gpu_launches": int(launches) * args.steps,
             "clocks": clk.summary(),
             "roofline": roof,
+            "setup": {"first_call_ms": first_call_ms,
+                      "note": "the first call on a context builds the per-n tables (host glibc "
+                              "p*log(p) triangle, memo candidate tables) and caches them; later "
+                              "calls (every timed step) reuse them"},
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_reference(w, p, args.cpu_seconds, os.cpu_count() or 1)
