@@ -92,10 +92,22 @@ int cell_count(int B) {
 }
 
 // Host-built constant tables, cached per (n, B) on a context.
+// Off by default: measured slower than the table gathers on every config
+// (c3 48.0 -> 61.2 ms, c2 9.0 -> 11.1, c0 3.6 -> 4.6, c4 2.02 -> 2.59 s per
+// window; ~35 instructions per computed term against one L2 gather).
+// MINE_B200_SPAN_LOG=1 turns it on (still only after k_check_plog passed).
+static bool span_log_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("MINE_B200_SPAN_LOG");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 struct TableSet {
   int n = -1, B = -1, ncell = 0;
-  DevBuf pl, logi, log2i, cell_off, cell_tr, cell_xy, cell_edge, cell_cmp, div, h2;
-  bool has_div = false, has_h2 = false;
+  DevBuf pl, logi, log2i, cell_off, cell_tr, cell_xy, cell_edge, cell_cmp, div, h2, chk;
+  bool has_div = false, has_h2 = false, span_log = false;
   std::vector<int> h_off;
 
   void build(int n_, int B_, cudaStream_t s) {
@@ -176,6 +188,16 @@ struct TableSet {
       CK(cudaGetLastError());
     }
     CK(cudaStreamSynchronize(s));  // host vectors go out of scope
+    // span terms of >= 3 rows may compute p*log(p) on the device (plog.cuh):
+    // only if the device replay of this host's libm log reproduces every
+    // entry of the table just built (opt-in: MINE_B200_SPAN_LOG=1)
+    span_log = false;
+    if (span_log_on()) {
+      const long long bad = check_plog_table(pl.as<double>(), n_,
+                                             static_cast<unsigned long long*>(chk.ensure(8)), s);
+      CK(cudaGetLastError());
+      span_log = bad == 0;
+    }
     n = n_;
     B = B_;
   }
@@ -192,6 +214,7 @@ struct TableSet {
     t.cell_cmp = cell_cmp.as<int8_t>();
     t.div = has_div ? div.as<double>() : nullptr;
     t.h2 = has_h2 ? h2.as<double>() : nullptr;
+    t.span_log = span_log ? 1 : 0;
     t.n = n;
     t.B = B;
     t.ncell = ncell;

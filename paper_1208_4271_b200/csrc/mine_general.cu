@@ -25,6 +25,7 @@
 
 #include "device_common.cuh"
 #include "mine_kernels.h"
+#include "plog.cuh"
 
 namespace mb200 {
 
@@ -911,6 +912,24 @@ __device__ __forceinline__ void span_terms(const Tables& tb, const int* cb, cons
       }
       r = rows;
     }
+#if MB_HAVE_LOGDATA
+    if (r < rows && tb.span_log) {
+      // three or more rows: p*log(p) computed (plog.cuh), no table gathers;
+      // each entry's sum still runs in row order
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (!ok[e]) continue;
+        const int s = s0 + base + w0 + e * nw;
+        const unsigned m = (unsigned)(ct - cs[e]);
+        const double rm = __drcp_rn((double)m);
+        double a = 0.0;
+        for (int rr = 0; rr < rows; ++rr)
+          a = __dadd_rn(a, plog_dev((unsigned)cum[rr * kk + t] - (unsigned)cum[rr * kk + s], m, rm));
+        acch[e] = a;
+      }
+      r = rows;
+    }
+#endif
     // unsigned offsets from the row base (one IMAD.WIDE.U32 per address)
 #if KDP_SPAN2
     // two rows per step: all eight gathers are issued before the adds (each
@@ -1353,6 +1372,14 @@ __global__ void __launch_bounds__(kWarpThreads, kMinBlocks) k_dp_warp(VarSet vs,
           acch = h2_at(tb.h2, (unsigned)(ct - cs), (unsigned)cum[t] - (unsigned)cum[s]);
           r = rows;
         }
+#if MB_HAVE_LOGDATA
+        if (r < rows && tb.span_log) {  // computed p*log(p) (plog.cuh), row order
+          const unsigned m = (unsigned)(ct - cs);
+          const double rm = __drcp_rn((double)m);
+          for (; r < rows; ++r)
+            acch = __dadd_rn(acch, plog_dev((unsigned)cum[r * kk + t] - (unsigned)cum[r * kk + s], m, rm));
+        }
+#endif
         for (; r + 2 <= rows; r += 2) {  // two gathers in flight, added in row order
           const double v0 = __ldg(pl + (plm + ((unsigned)cum[r * kk + t] - (unsigned)cum[r * kk + s])));
           const double v1 = __ldg(pl + (plm + ((unsigned)cum[(r + 1) * kk + t] - (unsigned)cum[(r + 1) * kk + s])));
@@ -1421,6 +1448,25 @@ __global__ void __launch_bounds__(kWarpThreads, kMinBlocks) k_dp_warp(VarSet vs,
     __syncwarp();
   }
 }
+
+#if MB_HAVE_LOGDATA
+// Every table entry pl[tri(m) + w] against plog_dev(w, m): counts differing bits.
+__global__ void k_check_plog(const double* __restrict__ pl, int n, unsigned long long* bad) {
+  const unsigned long long total = (unsigned long long)(n + 1) * (n + 2) / 2;
+  unsigned long long nb = 0;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < total;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    unsigned long long m = (unsigned long long)((sqrt(8.0 * (double)i + 1.0) - 1.0) / 2.0);
+    while (m * (m + 1) / 2 > i) --m;
+    while ((m + 1) * (m + 2) / 2 <= i) ++m;
+    const unsigned w = (unsigned)(i - m * (m + 1) / 2);
+    if (m == 0) continue;
+    const double v = plog_dev(w, (unsigned)m, __drcp_rn((double)m));
+    nb += __double_as_longlong(v) != __double_as_longlong(pl[i]);
+  }
+  if (nb) atomicAdd(bad, nb);
+}
+#endif
 
 // Exact quotient table div[tri(m) + w] = w / m (IEEE, as the reference's
 // c[s] / c[t]), so the span terms need no DDIV.
@@ -1861,6 +1907,22 @@ int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long 
 }
 
 size_t div_table_doubles(int n) { return (size_t)(n + 1) * (n + 2) / 2; }
+
+long long check_plog_table(const double* pl, int n, unsigned long long* scratch, cudaStream_t s) {
+#if MB_HAVE_LOGDATA
+  const size_t total = (size_t)(n + 1) * (n + 2) / 2;
+  cudaMemsetAsync(scratch, 0, sizeof(unsigned long long), s);
+  const unsigned blocks = (unsigned)std::min<size_t>(4096, (total + 255) / 256);
+  k_check_plog<<<blocks, 256, 0, s>>>(pl, n, scratch);
+  unsigned long long bad = 0;
+  if (cudaMemcpyAsync(&bad, scratch, sizeof(bad), cudaMemcpyDeviceToHost, s) != cudaSuccess) return -1;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
+  return (long long)bad;
+#else
+  (void)pl, (void)n, (void)scratch, (void)s;
+  return -1;
+#endif
+}
 
 void launch_build_div(double* div, int n, cudaStream_t s) {
   const size_t total = div_table_doubles(n);

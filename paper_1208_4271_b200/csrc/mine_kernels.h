@@ -59,6 +59,11 @@ struct Tables {
   int n = 0;
   int B = 0;
   int ncell = 0;
+  // span terms of three or more rows compute p*log(p) with the device replay
+  // of the host libm's log (plog.cuh) instead of gathering table rows
+  // c_t - c_s scattered over L2; set only after k_check_plog found every
+  // table entry identical
+  int span_log = 0;
 };
 
 // Which pairs of the variable set to score: work item w in [first, first+count).
@@ -217,6 +222,10 @@ int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long 
                   int orient_only, unsigned long long* counters, cudaStream_t s0,
                   const cudaStream_t* sides, cudaEvent_t* ev);
 cudaError_t init_general_attributes(int device);
+// Device p*log(p) against the host-built table pl (all (n+1)(n+2)/2
+// entries): the number of differing entries (synchronises the stream), or -1
+// when the build had no libm log data (plog.cuh).
+long long check_plog_table(const double* pl, int n, unsigned long long* scratch, cudaStream_t s);
 size_t div_table_doubles(int n);
 void launch_build_div(double* div, int n, cudaStream_t s);
 constexpr int kH2MaxN = 20000;

@@ -669,3 +669,34 @@ def test_bitonic_sort_same_bits(tmp_path):
         subprocess.run([sys.executable, str(script), str(out)], env=env, check=True, timeout=600)
         outs.append(np.load(out))
     assert_bit_equal(outs[1], outs[0], "bitonic sort vs ranking")
+
+
+def test_device_plog_span_terms_same_bits(tmp_path):
+    """MINE_B200_SPAN_LOG=1: span terms of three or more rows compute
+    p*log(p) with the device replay of the host libm's log (plog.cuh),
+    enabled only after every host-table entry matched (k_check_plog); the
+    results equal the table-gather default bit for bit (c3 / c0 slices, and
+    a cross call at n = 2500 where rows reach 12)."""
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "run.py"
+    script.write_text(
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        "from paper_1208_4271_b200 import Engine, Parameters, datagen\n"
+        "e = Engine(0)\n"
+        "cols = ('mic', 'mas', 'mev', 'mcn', 'mic_e', 'tic')\n"
+        "w3 = datagen.make(3); r3 = e.pairwise(w3.X[:8], Parameters(w3.alpha, w3.c, 1), cells=True)\n"
+        "w0 = datagen.make(0, npairs=12); r0 = e.pairs(w0.X, w0.xi, w0.yi, Parameters(w0.alpha, w0.c, 1), cells=True)\n"
+        "rng = np.random.default_rng(3); X = rng.standard_normal((3, 2500)); Y = np.tanh(X) + rng.standard_normal((3, 2500))\n"
+        "rc = e.cross(X, Y, Parameters(0.6, 5.0, 1), cells=True)\n"
+        "np.save(sys.argv[1], np.concatenate([np.stack([r[k] for k in cols]).ravel() for r in (r3, r0, rc)]\n"
+        "                                    + [r['cells'].ravel() for r in (r3, r0, rc)]))\n")
+    outs = []
+    for flag in ("0", "1"):
+        out = tmp_path / f"o{flag}.npy"
+        env = dict(os.environ, MINE_B200_SPAN_LOG=flag)
+        subprocess.run([sys.executable, str(script), str(out)], env=env, check=True, timeout=600)
+        outs.append(np.load(out))
+    assert_bit_equal(outs[1], outs[0], "computed p*log(p) vs table gathers")
