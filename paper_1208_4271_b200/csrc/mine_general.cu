@@ -1349,7 +1349,9 @@ __global__ void __launch_bounds__(kWarpThreads, kMinBlocks) k_dp_warp(VarSet vs,
     // span columns in blocks of kWarpSpanT t's: their entries (independent
     // of the DP) are gathered together -- one column at a time left each t's
     // L2 latency exposed, with few lanes busy at small t
-    for (int tb0 = 3; tb0 <= k; tb0 += kWarpSpanT) {
+    // with l_max = 3 only F(k, 3) is needed (rows t < k would feed level 3
+    // of a later t, and there is none): only column k's span terms
+    for (int tb0 = l_max >= 4 ? 3 : k; tb0 <= k; tb0 += kWarpSpanT) {
       const int tb1 = min(tb0 + kWarpSpanT - 1, k);
       // entries (s, t), t in [tb0, tb1], s in [2, t): column j = t - tb0
       // starts at entry off_j = sum_{i<j} (tb0 + i - 2)
