@@ -539,7 +539,9 @@ void run_call(mine_b200_ctx* ctx, const Call& call, const mine_parameter* par,
       launch_pack_tiny(vs, s);
       ++ctx->launches;
     }
-  } else if (row_dedup_on()) {  // general tier: row-map equality of consecutive y's
+  } else if (row_dedup_on() && count >= 256) {  // general tier: row-map equality of consecutive y's
+    // (a few pairs leave most SMs idle, so skipped subproblems save nothing
+    // while the two extra launches cost latency)
     vs.qsame = static_cast<uint16_t*>(ctx->qsame.ensure(sizeof(uint16_t) * (size_t)V * ny));
     if (!P.qsame) {
       launch_row_same(vs, s);

@@ -1687,12 +1687,17 @@ __global__ void k_copy_dups(VarSet vs, Tables tb, PairSpace ps, long long base, 
 // 10.8 ms; c0, n = 1000, with k_hat <= 64..160) -- and n <= kWarpPartMaxN
 // with the point arrays on chip, no debug export.  Returns the per-warp
 // shared memory (0: none).
-static size_t warp_part_bytes(int n, const YParams* yps, int ny, bool dbg, int& wp0) {
+static size_t warp_part_bytes(int n, const YParams* yps, int ny, bool dbg, long long nsub, int& wp0) {
   static const int kc_env = [] {
     const char* e = std::getenv("MINE_B200_WARP_PART_KC");
     return e ? std::atoi(e) : -1;
   }();
-  const int kc_max = kc_env >= 0 ? kc_env : std::max(64, 160000 / std::max(n, 1));
+  // small batches (fewer than 8 subproblems per SM and y) want the CTA
+  // kernel's warps per subproblem: a single pair through the reference API
+  // is latency-bound (n = 400: 747 -> ~620 us per pair)
+  const int kc_max = kc_env >= 0 ? kc_env
+                     : nsub < 8LL * sm_count() ? 0
+                                               : std::max(64, 160000 / std::max(n, 1));
   wp0 = ny;
   if (kc_max <= 0 || dbg || n > kWarpPartMaxN) return 0;
   while (wp0 > 0 && gen_kc(n, yps[wp0 - 1]) <= kc_max && !gen_tables_global(n, yps[wp0 - 1]) &&
@@ -1769,7 +1774,7 @@ int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long 
   // the group when the per-point arrays fit a warp's slice of shared memory,
   // else one k_part_f2 launch per run of one variant; y-major either way
   int wp0 = ny;  // the y's from wp0 on take the warp kernel
-  const size_t wpw = warp_part_bytes(n, yps, ny, dbg != nullptr, wp0);
+  const size_t wpw = warp_part_bytes(n, yps, ny, dbg != nullptr, nsub, wp0);
   for (int gi = 0; gi < wp0;) {
     const int v = pf_variant(n, yps[gi]);
     int gj = gi + 1;
@@ -1847,7 +1852,9 @@ int gen_run_group(const VarSet& vs, const Tables& tb, const PairSpace& ps, long 
       const char* e = std::getenv("MINE_B200_DPW_MODE");
       return e ? std::atoi(e) : -1;
     }();
-    const int mode = mode_env >= 0 ? mode_env : (nsub > 2048 ? 1 : 0);
+    // (a handful of subproblems, e.g. one pair through the reference API:
+    // one launch, the class split only costs launch latency)
+    const int mode = mode_env >= 0 ? mode_env : nsub > 2048 ? 1 : nsub >= 64 ? 0 : 4;
     auto wclass = [&](int x_max) {
       if (mode == 4) return 0;
       const int c = warp_class(x_max);
