@@ -700,3 +700,17 @@ def test_device_plog_span_terms_same_bits(tmp_path):
         subprocess.run([sys.executable, str(script), str(out)], env=env, check=True, timeout=600)
         outs.append(np.load(out))
     assert_bit_equal(outs[1], outs[0], "computed p*log(p) vs table gathers")
+
+
+@pytest.mark.parametrize("n", [1024, 1025])
+def test_warp_partition_kernel_limit(engine, oracle, n):
+    """n = 1024 is the warp partition kernel's limit (positions staged in a
+    warp's slice), n = 1025 takes the CTA kernel; both with tied variables,
+    superclumps (c = 1) and enough pairs for the batch paths (row-map dedup,
+    warp DP classes): statistics bit-exact against the oracle."""
+    rng = np.random.default_rng(n)
+    V = _tied_vars(rng, 52, n)
+    V[::4] = rng.standard_normal((13, n))
+    res = engine.pairwise(V, Parameters(0.55, 1.0, 1))
+    want = oracle.pairwise(V, 0.55, 1.0, 1)
+    assert_bit_equal(stats_matrix(res), want, f"n={n}")
