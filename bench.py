@@ -573,7 +573,21 @@ def secondary_block(eng, device, peaks, args):
                 "note": "C = every exact DP candidate (levels 2 .. l_max) at the measured "
                         "candidate rate; span_lookups = the span terms' p*log(p) lookups (rows "
                         "m = c_t - c_s scattered over the table) at the measured random L2 "
-                        "gather rate"}
+                        "gather rate (= one divergent lane per clock per SM through the L1/TEX "
+                        "pipe, the pipe ncu shows busiest: ncu_top_kernel)"}
+        # the config's top kernel under ncu (a committed capture, not this run):
+        # which pipe is busiest and how busy -- the limiting-pipe fraction
+        try:
+            pp = json.load(open(os.path.join(ROOT, "profiles", "ncu_pipes.json"))).get(f"c{cfg}")
+        except (OSError, ValueError):
+            pp = None
+        if pp:
+            entry["ncu_top_kernel"] = {
+                "kernel": pp["kernel"], "limiting_pipe": pp.get("limiting_pipe"),
+                "limiting_pipe_pct": pp.get("limiting_pipe_pct"),
+                "pipes_pct_of_peak": pp["pipes_pct_of_peak"], "capture": pp.get("capture"),
+                "source": "profiles/ncu_pipes.json (ncu --set full --clock-control none, "
+                          "tools/refresh_profiles.sh + tools/ncu_pipes.py); not measured in this run"}
         got = {k: t.cpu().numpy() for k, t in douts.items()}
         if cfg == 4:
             # the 32 pairs of the full-size reference fixture, scored separately

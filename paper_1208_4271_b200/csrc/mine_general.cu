@@ -56,7 +56,20 @@ constexpr int kMaxTile = KDP_TILE;  // t-tile / s-chunk edge
 #define KDP_SUBTILE 8
 #endif
 constexpr int kSubTile = KDP_SUBTILE;  // k_dp inner part: rows per sequential sub-tile
-constexpr int kAccStride = 9;  // doubles per thread in the accumulator hand-over (odd: no bank conflicts)
+// Levels per thread in k_dp's register tile (2 adjacent t x GL consecutive
+// levels): 4 or 8, per variant.  Every operand of the tile comes from shared
+// memory by 16-byte loads, which cost 4 wavefronts per warp whatever the
+// lanes share, so the loop runs at 16 GL / (4 + GL) candidates per wavefront:
+// 16 at GL = 4, 21.3 at GL = 8 (the L1 pipe is k_dp's busiest, ncu).
+#ifndef KDP_GL_LEAN
+#define KDP_GL_LEAN 4
+#endif
+#ifndef KDP_GL_WIDE
+#define KDP_GL_WIDE 4
+#endif
+__host__ __device__ constexpr int dp_gl(bool lean) { return lean ? KDP_GL_LEAN : KDP_GL_WIDE; }
+// doubles per thread in the accumulator hand-over (odd: no bank conflicts)
+__host__ __device__ constexpr int dp_acc_stride(bool lean) { return 2 * dp_gl(lean) + 1; }
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -411,7 +424,8 @@ __global__ void __launch_bounds__(kPfThreads, PF_MINB_THREADS / kPfThreads) k_pa
       const unsigned uct = ct;
       for (int s = 1 + hl; s < t; s += W) {
         const unsigned cs = cb[s];
-        const double acc2 = __dadd_rn(__ldg(pl + (plt + cs)), __ldg(pl + (plt + (uct - cs))));
+        const double acc2 = tb.h2 ? h2_at(tb.h2, uct, cs)
+                                  : __dadd_rn(__ldg(pl + (plt + cs)), __ldg(pl + (plt + (uct - cs))));
         double accj = 0.0;
         // columns s and t of cum walked by pointer (stride kk): one IADD per
         // row instead of re-deriving r * kk + s
@@ -717,7 +731,8 @@ __device__ __forceinline__ void part_warp_item(const VarSet& vs, const Tables& t
       const unsigned uct = ct;
       for (int s = 1 + hl; s < t; s += W) {
         const unsigned cs = cb[s];
-        const double acc2 = __dadd_rn(__ldg(pl + (plt + cs)), __ldg(pl + (plt + (uct - cs))));
+        const double acc2 = tb.h2 ? h2_at(tb.h2, uct, cs)
+                                  : __dadd_rn(__ldg(pl + (plt + cs)), __ldg(pl + (plt + (uct - cs))));
         double accj = 0.0;
         // columns s and t of cum walked by pointer (stride kk): one IADD per
         // row instead of re-deriving r * kk + s
@@ -810,15 +825,16 @@ struct DpLayout {
   int fsw, ftw;  // staged / tile F row widths (doubles)
 };
 
-// Staged F rows (levels l0-1 .. l1-1) are 4 ngc doubles wide, ngc = the
-// level groups of the widest level tile (nlc = min(64, x_max - 2) levels).
-// Level offset j = 4 g + i (g: the consumer's group) sits at 2 g + i for
-// i < 2 and at 2 ng + 2 g + (i - 2) otherwise (ng: this tile's groups; 32 in
-// the 64-wide rows of the wide variants), so the 16-byte loads of consecutive
-// groups are contiguous (no bank conflicts).
-__host__ __device__ inline int fs_col(int j, int fo) {  // fo: offset of levels 2, 3 (2 ng)
-  const int g = j >> 2, i = j & 3;
-  return (i < 2 ? 0 : fo - 2) + 2 * g + i;
+// Staged F rows (levels l0-1 .. l1-1) are GL ngc doubles wide, ngc = the
+// level groups (GL levels each, dp_gl) of the widest level tile (nlc =
+// min(64, x_max - 2) levels).  Level offset j = GL g + i (g: the consumer's
+// group) sits at (i / 2) fo + 2 g + (i & 1), fo = 2 ng (ng: this tile's
+// groups; 64 / GL in the 64-wide rows of the wide variants), so the 16-byte
+// loads of consecutive groups are contiguous (no bank conflicts).
+template <int GL>
+__host__ __device__ inline int fs_col(int j, int fo) {  // fo: offset between level pairs (2 ng)
+  const int g = j / GL, i = j % GL;
+  return (i >> 1) * fo + 2 * g + (i & 1);
 }
 #ifndef KDP_LEAN_XMAX
 #define KDP_LEAN_XMAX 64
@@ -828,7 +844,7 @@ constexpr int kLeanXMax = KDP_LEAN_XMAX;
 #define DP_COMPACT 1
 #endif
 __host__ __device__ inline int dp_nlc(int x_max) { return !DP_COMPACT || x_max - 2 >= 64 ? 64 : x_max - 2; }
-__host__ __device__ inline int dp_ngc(int x_max) { return (dp_nlc(x_max) + 3) >> 2; }
+__host__ __device__ inline int dp_ngc(int x_max, int gl) { return (dp_nlc(x_max) + gl - 1) / gl; }
 
 // kGlobalTables: cb and cum are read in place from the subproblem's
 // GenScratch slot instead of being staged (for c B too large for the chip).
@@ -849,20 +865,20 @@ __host__ __device__ inline DpLayout dp_layout(int y, int kc, int x_max, bool glo
   o += al16(sizeof(double) * kMaxTile * kMaxTile);
   // compact widths for the lean variant only (gen_dp_lean); the others use
   // 64 / 65
-  const int ngc = lean ? dp_ngc(x_max) : 16;
-  L.fsw = 4 * ngc;
+  const int gl = dp_gl(lean), kAccStride = dp_acc_stride(lean);
+  const int ngc = lean ? dp_ngc(x_max, gl) : 64 / gl;
+  L.fsw = gl * ngc;
   L.ftw = lean ? dp_nlc(x_max) + 1 : 65;
   const size_t acc_b = sizeof(double) * (size_t)(kMaxTile / 2) * ngc * kAccStride;
   const size_t fs_b = sizeof(double) * (size_t)kMaxTile * L.fsw;
   L.acc = o;
   if (!lean && !KDP_WIDE_SHARED_ACC) {  // wide variants: separate regions, as sized before the lean variant
-    o += al16(sizeof(double) * kDpThreads * kAccStride);
+    o += al16(acc_b);
     L.fs = o;
     o += al16(fs_b);
   } else if (!lean) {  // wide, shared: the hand-over (inner part) and the staged rows (chunks) alternate
     L.fs = o;
-    const size_t wacc = sizeof(double) * kDpThreads * kAccStride;
-    o += al16(wacc > fs_b ? wacc : fs_b);
+    o += al16(acc_b > fs_b ? acc_b : fs_b);
   } else {
     L.fs = o;
     o += al16(acc_b > fs_b ? acc_b : fs_b);
@@ -1003,6 +1019,9 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 #ifndef KDP_MIN_BLOCKS
 #define KDP_MIN_BLOCKS 4
 #endif
+#ifndef KDP_WIDE_MIN_BLOCKS
+#define KDP_WIDE_MIN_BLOCKS 3
+#endif
 #ifndef KDP_CTAS_PER_SM
 #define KDP_CTAS_PER_SM 4
 #endif
@@ -1014,7 +1033,7 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 // set up per item (the launch's shared memory is the maximum over its y's);
 // F lives in this CTA's HBM slot of fslot_stride doubles.
 template <bool kGlobalTables, bool kRing, bool kLean>
-__global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : 3) k_dp(VarSet vs, Tables tb, PairSpace ps,
+__global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : KDP_WIDE_MIN_BLOCKS) k_dp(VarSet vs, Tables tb, PairSpace ps,
                                                       long long base, GenGroup grp, int gi0,
                                                       int gcount, double* __restrict__ fslots,
                                                       unsigned long long fslot_stride,
@@ -1053,6 +1072,7 @@ __global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : 3) k_dp(V
     const DpLayout L = dp_layout(y, kc, x_max, kGlobalTables, kLean);
     // row widths: compile-time for the wide variants (x_max > 64: 64 / 65)
     const int fsw = kLean ? L.fsw : 64, ftw = kLean ? L.ftw : 65;
+    constexpr int GL = dp_gl(kLean), kAccStride = dp_acc_stride(kLean);
     int* cb = reinterpret_cast<int*>(smem + L.cb);
     int* cum = reinterpret_cast<int*>(smem + L.cum);
     double* A = reinterpret_cast<double*>(smem + L.A);
@@ -1090,32 +1110,32 @@ __global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : 3) k_dp(V
     }
     __syncthreads();
 
-    // Level tiles of <= 64 levels.  A thread owns 8 cells: two adjacent t
-    // (t0 + 2p, t0 + 2p + 1) x a group of 4 consecutive levels, so each s
-    // costs one 16-byte load for both A, one for both W and two for four F
-    // values, feeding 8 independent max chains.  (T/2) * groups <= 256.
+    // Level tiles of <= 64 levels.  A thread owns 2 GL cells: two adjacent t
+    // (t0 + 2p, t0 + 2p + 1) x a group of GL consecutive levels, so each s
+    // costs one 16-byte load for both A, one for both W and GL / 2 for the F
+    // values, feeding 2 GL independent max chains.  (T/2) * groups <= 256.
     // (Splitting a chunk's rows over several owner sets when the level tile
     // is narrow was measured: no gain, and the larger hand-over region cost
     // L1 capacity -- c3 -13%.)
     for (int l0 = 3; l0 <= l_max; l0 += 64) {
       const int l1 = min(l0 + 63, l_max), nl = l1 - l0 + 1;
-      const int ng = (nl + 3) >> 2;
-      const int fo = kLean ? 2 * ng : 32;  // staged row offset of levels 2, 3 of a group
+      const int ng = (nl + GL - 1) / GL;
+      const int fo = kLean ? 2 * ng : 128 / GL;  // staged row offset between a group's level pairs
       // this thread's first staged element and its stride in (row, level)
       const int st_sl = tid / nl, st_j = tid - st_sl * nl;
       const int st_dsl = kDpThreads / nl, st_dj = kDpThreads - st_dsl * nl;
       const int T = max(2, min(kMaxTile, 2 * (kDpThreads / ng)));
       const int t_lo = (l0 == l_max) ? k : l0;  // level l_max is needed at t = k only
       const int my_tp = tid / ng, my_g = tid - my_tp * ng;
-      const int my_l = l0 + 4 * my_g;  // first of my 4 levels
+      const int my_l = l0 + GL * my_g;  // first of my GL levels
       const int my_tl = 2 * my_tp;     // first of my 2 t's (tile-local)
       const int inner_threads = ((nl + 31) >> 5) << 5;
       for (int t0 = t_lo; t0 <= k; t0 += T) {
         const int nt = min(T, k - t0 + 1);
         const bool owner = my_tl < nt;
-        double acc[8];
+        double acc[2 * GL];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = kLowest;
+        for (int i = 0; i < 2 * GL; ++i) acc[i] = kLowest;
         // ---- outer part: every s < t0 (independent candidates)
         for (int s0 = max(2, l0 - 1); s0 < t0; s0 += T) {
           const int ns = min(T, t0 - s0);
@@ -1125,7 +1145,7 @@ __global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : 3) k_dp(V
           // element i = tid + 256 u of the (row, level) grid, walked without
           // a division per element
           for (int sl = st_sl, j = st_j; sl < ns;) {
-            cp_async8(fs + sl * fsw + fs_col(j, fo), F + (size_t)(s0 + sl) * RW + (((l0 - 3) + j) & cm));
+            cp_async8(fs + sl * fsw + fs_col<GL>(j, fo), F + (size_t)(s0 + sl) * RW + (((l0 - 3) + j) & cm));
             sl += st_dsl;
             j += st_dj;
             if (j >= nl) {
@@ -1139,52 +1159,50 @@ __global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : 3) k_dp(V
           span_terms(tb, cb, cum, kk, rows, k, s0, ns, t0, nt, A, W);
           for (int i = tid; i < ns * nl; i += kDpThreads) {  // stage F(s, l0-1 .. l1-1)
             const int sl = i / nl, j = i - sl * nl;
-            fs[sl * fsw + fs_col(j, fo)] = F[(size_t)(s0 + sl) * RW + (((l0 - 3) + j) & cm)];
+            fs[sl * fsw + fs_col<GL>(j, fo)] = F[(size_t)(s0 + sl) * RW + (((l0 - 3) + j) & cm)];
           }
 #endif
           __syncthreads();
           if (owner) {
-            // s >= l - 1 holds for all 4 levels once s >= my_l + 2; only the
-            // chunk(s) near the diagonal need the per-level test.  Cells that
-            // are not valid accumulate garbage that is never read.
+            // s >= l - 1 holds for all GL levels once s >= my_l + GL - 2; only
+            // the chunk(s) near the diagonal need the per-level test.  Cells
+            // that are not valid accumulate garbage that is never read.
             const double* fr = fs + 2 * my_g;
             int sl = 0;
-            for (; sl < ns && s0 + sl < my_l + 2; ++sl) {
+            for (; sl < ns && s0 + sl < my_l + GL - 2; ++sl) {
               const int s = s0 + sl;
               const double2 a = *reinterpret_cast<const double2*>(A + sl * kMaxTile + my_tl);
               const double2 w = *reinterpret_cast<const double2*>(W + sl * kMaxTile + my_tl);
 #pragma unroll
-              for (int i = 0; i < 4; ++i)
+              for (int i = 0; i < GL; ++i)
                 if (s >= my_l + i - 1) {
-                  const double f = fr[sl * fsw + (i < 2 ? i : fo - 2 + i)];
+                  const double f = fr[sl * fsw + (i >> 1) * fo + (i & 1)];
                   acc[i] = dmax(acc[i], __dsub_rn(__dmul_rn(a.x, f), w.x));
-                  acc[4 + i] = dmax(acc[4 + i], __dsub_rn(__dmul_rn(a.y, f), w.y));
+                  acc[GL + i] = dmax(acc[GL + i], __dsub_rn(__dmul_rn(a.y, f), w.y));
                 }
             }
             // running addresses (W sits kMaxTile^2 doubles after A): the loop
             // body is the 4 loads and the 8 candidates, no index arithmetic
             const double* ap = A + sl * kMaxTile + my_tl;
             const double* fp = fr + sl * fsw;
-#pragma unroll 2
+#pragma unroll(GL == 4 ? 2 : 1)
             for (; sl < ns; ++sl, ap += kMaxTile, fp += fsw) {
               const double2 a = *reinterpret_cast<const double2*>(ap);
               const double2 w = *reinterpret_cast<const double2*>(ap + kMaxTile * kMaxTile);
-              const double2 f01 = *reinterpret_cast<const double2*>(fp);
-              const double2 f23 = *reinterpret_cast<const double2*>(fp + fo);
-              acc[0] = dmax(acc[0], __dsub_rn(__dmul_rn(a.x, f01.x), w.x));
-              acc[1] = dmax(acc[1], __dsub_rn(__dmul_rn(a.x, f01.y), w.x));
-              acc[2] = dmax(acc[2], __dsub_rn(__dmul_rn(a.x, f23.x), w.x));
-              acc[3] = dmax(acc[3], __dsub_rn(__dmul_rn(a.x, f23.y), w.x));
-              acc[4] = dmax(acc[4], __dsub_rn(__dmul_rn(a.y, f01.x), w.y));
-              acc[5] = dmax(acc[5], __dsub_rn(__dmul_rn(a.y, f01.y), w.y));
-              acc[6] = dmax(acc[6], __dsub_rn(__dmul_rn(a.y, f23.x), w.y));
-              acc[7] = dmax(acc[7], __dsub_rn(__dmul_rn(a.y, f23.y), w.y));
+#pragma unroll
+              for (int q = 0; q < GL / 2; ++q) {
+                const double2 f = *reinterpret_cast<const double2*>(fp + q * fo);
+                acc[2 * q] = dmax(acc[2 * q], __dsub_rn(__dmul_rn(a.x, f.x), w.x));
+                acc[2 * q + 1] = dmax(acc[2 * q + 1], __dsub_rn(__dmul_rn(a.x, f.y), w.x));
+                acc[GL + 2 * q] = dmax(acc[GL + 2 * q], __dsub_rn(__dmul_rn(a.y, f.x), w.y));
+                acc[GL + 2 * q + 1] = dmax(acc[GL + 2 * q + 1], __dsub_rn(__dmul_rn(a.y, f.y), w.y));
+              }
             }
           }
           __syncthreads();
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < 2 * GL; ++i)
           if (my_tp < kMaxTile / 2) accS[tid * kAccStride + i] = acc[i];
         // ---- inner part: s inside the tile, one t at a time, a level per
         // thread; only the warps holding levels take part (named barrier).
@@ -1205,8 +1223,8 @@ __global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : 3) k_dp(V
             for (int tl = sb0; tl < sb1; ++tl) {
               const int tt = t0 + tl;
               if (ll < nl && tt >= l && !(l == l_max && tt != k)) {
-                // owner of cell (tl, ll): thread (tl/2)*ng + ll/4, slot (tl&1)*4 + (ll&3)
-                double m = accS[((tl >> 1) * ng + (ll >> 2)) * kAccStride + (tl & 1) * 4 + (ll & 3)];
+                // owner of cell (tl, ll): thread (tl/2)*ng + ll/GL, slot (tl&1)*GL + ll%GL
+                double m = accS[((tl >> 1) * ng + ll / GL) * kAccStride + (tl & 1) * GL + ll % GL];
                 const double* Ap = A + tl;
                 const double* Wp = W + tl;
                 for (int s = max(t0 + sb0, l - 1); s < tt; ++s) {
@@ -1228,7 +1246,7 @@ __global__ void __launch_bounds__(kDpThreads, kLean ? KDP_MIN_BLOCKS : 3) k_dp(V
           for (int tl = sb1 + st_sl, ll = st_j; tl < nt;) {
             const int l = l0 + ll, tt = t0 + tl;
             if (tt >= l && !(l == l_max && tt != k)) {
-              double* slot = accS + ((tl >> 1) * ng + (ll >> 2)) * kAccStride + (tl & 1) * 4 + (ll & 3);
+              double* slot = accS + ((tl >> 1) * ng + ll / GL) * kAccStride + (tl & 1) * GL + ll % GL;
               double m = *slot;
               for (int sl = max(sb0, l - 1 - t0); sl < sb1; ++sl)
                 m = dmax(m, __dsub_rn(__dmul_rn(A[sl * kMaxTile + tl], ft[sl * ftw + ll]), W[sl * kMaxTile + tl]));

@@ -702,6 +702,43 @@ def test_device_plog_span_terms_same_bits(tmp_path):
     assert_bit_equal(outs[1], outs[0], "computed p*log(p) vs table gathers")
 
 
+def test_h2_table_same_bits(tmp_path):
+    """The two-term table H2(m, w) = pl(m, w) + pl(m, m - w) (one gather for a
+    two-row span and for every F(t,2) candidate's H(P), any row count, in
+    k_part_f2, k_part_warp, k_dp and k_dp_warp) against the two p*log(p)
+    gathers it replaces (MINE_B200_NO_H2=1, the path n > 20000 takes): bit
+    for bit on c3 / c2 (ties) / c0 slices and a cross call with up to 12
+    rows."""
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "run.py"
+    script.write_text(
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        "from paper_1208_4271_b200 import Engine, Parameters, datagen\n"
+        "e = Engine(0)\n"
+        "cols = ('mic', 'mas', 'mev', 'mcn', 'mic_e', 'tic')\n"
+        "w3 = datagen.make(3); r3 = e.pairwise(w3.X[:8], Parameters(w3.alpha, w3.c, 1), cells=True)\n"
+        "w2 = datagen.make(2); r2 = e.pairwise(w2.X[:24], Parameters(w2.alpha, w2.c, 1), cells=True)\n"
+        "w0 = datagen.make(0, npairs=12); r0 = e.pairs(w0.X, w0.xi, w0.yi, Parameters(w0.alpha, w0.c, 1), cells=True)\n"
+        "rng = np.random.default_rng(3); X = rng.standard_normal((3, 2500)); Y = np.tanh(X) + rng.standard_normal((3, 2500))\n"
+        "rc = e.cross(X, Y, Parameters(0.6, 5.0, 1), cells=True)\n"
+        "rs = (r3, r2, r0, rc)\n"
+        "np.save(sys.argv[1], np.concatenate([np.stack([r[k] for k in cols]).ravel() for r in rs]\n"
+        "                                    + [r['cells'].ravel() for r in rs]))\n")
+    outs = []
+    for flag in (None, "1"):
+        out = tmp_path / f"o{flag}.npy"
+        env = dict(os.environ)
+        env.pop("MINE_B200_NO_H2", None)
+        if flag:
+            env["MINE_B200_NO_H2"] = flag
+        subprocess.run([sys.executable, str(script), str(out)], env=env, check=True, timeout=600)
+        outs.append(np.load(out))
+    assert_bit_equal(outs[1], outs[0], "H2 table vs two p*log(p) gathers")
+
+
 @pytest.mark.parametrize("n", [1024, 1025])
 def test_warp_partition_kernel_limit(engine, oracle, n):
     """n = 1024 is the warp partition kernel's limit (positions staged in a
