@@ -20,7 +20,6 @@
 #include <cstdlib>
 #include <cstring>
 
-#include <cub/device/device_segmented_radix_sort.cuh>
 
 #include "device_common.cuh"
 #include "mine_kernels.h"
@@ -146,8 +145,11 @@ __global__ void k_sort_bitonic(VarSet vs, int N) {
 }
 
 // K1 for large n (the 12n-byte working set of k_sort_vars no longer fits on
-// chip, or the O(n^2) ranking costs more than a sort): a stable segmented
-// radix sort of order-preserving 64-bit keys (cub), then the tie-run scan.
+// chip, or the O(n^2) ranking costs more than a sort): k_sort_big, the same
+// bitonic network over (order key, sample index) with the array in an HBM
+// scratch slot per variable -- compare-exchange distances below kBigChunk
+// run on 8192-element chunks staged in shared memory, the few longer ones
+// in place through L2 -- then the tie-run scan (k_sorted_runs).
 // -0.0 is keyed as +0.0 (C++ ==), NaN as +inf, as in k_sort_vars.
 __device__ __forceinline__ unsigned long long order_key(double x) {
   if (isnan(x)) x = HUGE_VAL;
@@ -156,15 +158,92 @@ __device__ __forceinline__ unsigned long long order_key(double x) {
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
 
-__global__ void k_sort_keys(VarSet vs, unsigned long long* keys, int* idx, int* offs) {
-  const long long total = (long long)vs.V * vs.n;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    keys[i] = order_key(vs.vals[i]);
-    idx[i] = (int)(i % vs.n);
-    if (i % vs.n == 0) offs[i / vs.n] = (int)i;
+constexpr int kBigChunk = 8192;  // elements per shared-memory chunk (80 KB: keys + 16-bit indices)
+
+// One CTA per variable; N = the power of two >= n (<= 65536).  gkey / gidx:
+// this variable's N-element scratch arrays; skeys: the n sorted keys, packed
+// per variable for k_sorted_runs.  Element a of a size-`size` bitonic stage
+// sorts ascending iff (a & size) == 0, with a the index in the whole array.
+__global__ void __launch_bounds__(1024) k_sort_big(VarSet vs, int N, unsigned long long* gkeys,
+                                                   uint16_t* gidxs, unsigned long long* skeys) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = vs.n, tid = threadIdx.x, var = blockIdx.x;
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(smem);
+  uint16_t* idx = reinterpret_cast<uint16_t*>(key + kBigChunk);
+  unsigned long long* gkey = gkeys + (size_t)var * N;
+  uint16_t* gidx = gidxs + (size_t)var * N;
+  const double* src = vs.vals + (size_t)var * n;
+  const int C = min(N, kBigChunk);
+  // compare-exchange distances stride_hi, stride_hi / 2, .. 1 of stage `size`
+  // on the staged chunk whose first element is `c0` in the whole array
+  auto chunk_strides = [&](int c0, int size, int stride_hi) {
+    for (int stride = stride_hi; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int i = tid; i < (C >> 1); i += blockDim.x) {
+        const int a = 2 * i - (i & (stride - 1)), b = a + stride;
+        const unsigned long long ka = key[a], kb = key[b];
+        const uint16_t ia = idx[a], ib = idx[b];
+        const bool gt = ka > kb || (ka == kb && ia > ib);
+        if (gt == (((c0 + a) & size) == 0)) {
+          key[a] = kb;
+          key[b] = ka;
+          idx[a] = ib;
+          idx[b] = ia;
+        }
+      }
+    }
+    __syncthreads();
+  };
+  // phase A: every chunk fully sorted (stages 2 .. C), direction by its place
+  for (int c0 = 0; c0 < N; c0 += C) {
+    for (int i = tid; i < C; i += blockDim.x) {
+      const int g = c0 + i;
+      key[i] = g < n ? order_key(src[g]) : ~0ull;
+      idx[i] = (uint16_t)(g < n ? g : 0xffff);
+    }
+    for (int size = 2; size <= C; size <<= 1) chunk_strides(c0, size, size >> 1);
+    for (int i = tid; i < C; i += blockDim.x) {
+      __stcg(gkey + c0 + i, key[i]);
+      __stcg(gidx + c0 + i, idx[i]);
+    }
+    __syncthreads();
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) offs[vs.V] = (int)total;
+  // phase B: stages 2 C .. N; distances >= C in place (L2), the rest per chunk
+  for (int size = 2 * C; size <= N; size <<= 1) {
+    for (int stride = size >> 1; stride >= C; stride >>= 1) {
+      for (int i = tid; i < (N >> 1); i += blockDim.x) {
+        const int a = 2 * i - (i & (stride - 1)), b = a + stride;
+        const unsigned long long ka = __ldcg(gkey + a), kb = __ldcg(gkey + b);
+        const uint16_t ia = __ldcg(gidx + a), ib = __ldcg(gidx + b);
+        const bool gt = ka > kb || (ka == kb && ia > ib);
+        if (gt == ((a & size) == 0)) {
+          __stcg(gkey + a, kb);
+          __stcg(gkey + b, ka);
+          __stcg(gidx + a, ib);
+          __stcg(gidx + b, ia);
+        }
+      }
+      __syncthreads();
+    }
+    for (int c0 = 0; c0 < N; c0 += C) {
+      for (int i = tid; i < C; i += blockDim.x) {
+        key[i] = __ldcg(gkey + c0 + i);
+        idx[i] = __ldcg(gidx + c0 + i);
+      }
+      chunk_strides(c0, size, C >> 1);
+      for (int i = tid; i < C; i += blockDim.x) {
+        __stcg(gkey + c0 + i, key[i]);
+        __stcg(gidx + c0 + i, idx[i]);
+      }
+      __syncthreads();
+    }
+  }
+  int* perm = vs.perm + (size_t)var * n;
+  unsigned long long* sk = skeys + (size_t)var * n;
+  for (int i = tid; i < n; i += blockDim.x) {
+    perm[i] = __ldcg(gidx + i);
+    sk[i] = __ldcg(gkey + i);
+  }
 }
 
 __global__ void k_sorted_runs(VarSet vs, const unsigned long long* skeys) {
@@ -1422,6 +1501,7 @@ cudaError_t init_kernel_attributes(int device) {
   if (e != cudaSuccess) return e;
   const void* fns[] = {reinterpret_cast<const void*>(k_sort_vars),
                        reinterpret_cast<const void*>(k_sort_bitonic),
+                       reinterpret_cast<const void*>(k_sort_big),
                        reinterpret_cast<const void*>(k_memo_pairs<false, false, 23, 8192, 20>),
                        reinterpret_cast<const void*>(k_memo_pairs<false, false, 23, 8192, 21>),
                        reinterpret_cast<const void*>(k_memo_pairs<false, false, 23, 8192, 22>),
@@ -1476,19 +1556,16 @@ static bool radix_sort_vars(int n) {
   return n > kRadixSortN;
 }
 
-static size_t cub_sort_bytes(int V, int n) {
-  size_t tmp = 0;
-  cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, (const unsigned long long*)nullptr,
-                                           (unsigned long long*)nullptr, (const int*)nullptr,
-                                           (int*)nullptr, (long long)V * n, V, (const int*)nullptr,
-                                           (const int*)nullptr);
-  return tmp;
+static int big_sort_N(int n) {
+  int N = 128;
+  while (N < n) N <<= 1;
+  return N;
 }
 
 size_t sort_scratch_bytes(int V, int n) {
   if (!radix_sort_vars(n)) return 0;
-  const size_t items = (size_t)V * n;
-  return 2 * 8 * items + 4 * items + 4 * (size_t)(V + 1) + 3 * 256 + cub_sort_bytes(V, n);
+  const size_t N = (size_t)big_sort_N(n);
+  return 8 * N * V + 256 + 2 * N * V + 256 + 8 * (size_t)V * n + 256;
 }
 
 // MINE_B200_BITONIC=0: the O(n^2) ranking for every n <= kRadixSortN (A/B)
@@ -1515,21 +1592,17 @@ cudaError_t launch_sort_vars(const VarSet& vs, void* scratch, cudaStream_t s) {
     k_sort_vars<<<vs.V, threads, sm, s>>>(vs);
     return cudaGetLastError();
   }
-  const size_t items = (size_t)vs.V * vs.n;
+  const int N = big_sort_N(vs.n);
   auto a256 = [](size_t x) { return (x + 255) & ~size_t(255); };
   char* p = static_cast<char*>(scratch);
-  auto* kin = reinterpret_cast<unsigned long long*>(p);
-  auto* kout = reinterpret_cast<unsigned long long*>(p + a256(8 * items));
-  int* idx = reinterpret_cast<int*>(p + 2 * a256(8 * items));
-  int* offs = reinterpret_cast<int*>(p + 2 * a256(8 * items) + a256(4 * items));
-  void* tmp = p + 2 * a256(8 * items) + a256(4 * items) + a256(4 * (size_t)(vs.V + 1));
-  const unsigned blocks = (unsigned)std::min<size_t>(4 * 148, (items + 255) / 256);
-  k_sort_keys<<<blocks, 256, 0, s>>>(vs, kin, idx, offs);
-  size_t tb = cub_sort_bytes(vs.V, vs.n);
-  cudaError_t e = cub::DeviceSegmentedRadixSort::SortPairs(
-      tmp, tb, kin, kout, idx, vs.perm, (long long)items, vs.V, offs, offs + 1, 0, 64, s);
+  auto* gkeys = reinterpret_cast<unsigned long long*>(p);
+  auto* gidxs = reinterpret_cast<uint16_t*>(p + a256(8 * (size_t)N * vs.V));
+  auto* skeys = reinterpret_cast<unsigned long long*>(p + a256(8 * (size_t)N * vs.V) + a256(2 * (size_t)N * vs.V));
+  const int C = std::min(N, kBigChunk);
+  k_sort_big<<<vs.V, 1024, (size_t)C * 10, s>>>(vs, N, gkeys, gidxs, skeys);
+  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_sorted_runs<<<vs.V, 1024, 0, s>>>(vs, kout);
+  k_sorted_runs<<<vs.V, 1024, 0, s>>>(vs, skeys);
   return cudaGetLastError();
 }
 

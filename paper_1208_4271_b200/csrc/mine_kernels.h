@@ -121,8 +121,9 @@ struct SubDebug {
 // Must run once per device (under a lock) before any launch.
 cudaError_t init_kernel_attributes(int device);
 void launch_check_finite(const double* v, long long count, int* flag, cudaStream_t s);
-// K1: k_sort_vars (on chip, O(n^2) ranking) up to kRadixSortN samples, a
-// segmented radix sort above (scratch: sort_scratch_bytes, 0 below the limit)
+// K1: k_sort_bitonic / k_sort_vars (on chip) up to kRadixSortN samples, the
+// chunked bitonic sort k_sort_big through an HBM scratch above (scratch:
+// sort_scratch_bytes, 0 below the limit; MINE_B200_RADIX_SORT=1 forces it)
 constexpr int kRadixSortN = 16384;
 size_t sort_scratch_bytes(int V, int n);
 cudaError_t launch_sort_vars(const VarSet& vs, void* scratch, cudaStream_t s);

@@ -671,6 +671,49 @@ def test_bitonic_sort_same_bits(tmp_path):
     assert_bit_equal(outs[1], outs[0], "bitonic sort vs ranking")
 
 
+def test_big_sort_same_bits(tmp_path):
+    """K1's large-n sort k_sort_big (chunked bitonic through an HBM scratch,
+    n > 16384 by default) forced at smaller n (MINE_B200_RADIX_SORT=1) gives
+    the on-chip sorts' bits: one chunk (n = 65, 1000), two chunks with the
+    in-place long-distance passes (n = 8193, 12000); ties, -0.0 against +0.0,
+    huge and tiny magnitudes, constant variables."""
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "run.py"
+    script.write_text(
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        "from paper_1208_4271_b200 import Engine, Parameters\n"
+        "rng = np.random.default_rng(9)\n"
+        "e = Engine(0)\n"
+        "out = []\n"
+        "for n, alpha in ((65, 0.6), (1000, 0.6), (8193, 0.45), (12000, 0.45)):\n"
+        "    V = rng.standard_normal((8, n))\n"
+        "    V[1] = np.round(V[1] * 2)\n"
+        "    V[2, ::3] = -0.0\n"
+        "    V[2, 1::3] = 0.0\n"
+        "    V[3] = 7.0\n"
+        "    V[4] *= 1e300\n"
+        "    V[5] *= 1e-300\n"
+        "    V[6] = rng.integers(0, 3, n)\n"
+        "    r = e.pairwise(V, Parameters(alpha, 15.0, 1))\n"
+        "    out += [np.stack([r[k] for k in ('mic', 'mas', 'mev', 'mcn', 'mic_e', 'tic')]).ravel()]\n"
+        "    d = e.debug_subproblem(V[1], V[6], 2, 5, 30)\n"
+        "    out += [np.asarray(d['bounds'], float), np.asarray(d['q_x'], float)]\n"
+        "np.save(sys.argv[1], np.concatenate(out))\n")
+    outs = []
+    for flag in (None, "1"):
+        out = tmp_path / f"o{flag}.npy"
+        env = dict(os.environ)
+        env.pop("MINE_B200_RADIX_SORT", None)
+        if flag:
+            env["MINE_B200_RADIX_SORT"] = flag
+        subprocess.run([sys.executable, str(script), str(out)], env=env, check=True, timeout=600)
+        outs.append(np.load(out))
+    assert_bit_equal(outs[1], outs[0], "k_sort_big vs the on-chip sorts")
+
+
 def test_device_plog_span_terms_same_bits(tmp_path):
     """MINE_B200_SPAN_LOG=1: span terms of three or more rows compute
     p*log(p) with the device replay of the host libm's log (plog.cuh),
