@@ -11,10 +11,8 @@
 // formats that block instead (no MINE statistic gets there).
 //
 //   k_rec_len   one thread per record: its byte length (and the fallback flag)
-//   (exclusive scan of the lengths, cub)
+//   k_scan_*    exclusive scan of the lengths (tile sums, their scan, tile scans)
 //   k_rec_write one thread per record: the bytes at its offset
-#include <cub/device/device_scan.cuh>
-
 #include "device_common.cuh"
 #include "mine_kernels.h"
 
@@ -187,6 +185,82 @@ __global__ void k_format_values(const double* v, long long n, char* out, int* le
   for (int k = 0; k < l; ++k) out[i * 24 + k] = buf[k];
 }
 
+// Exclusive scan of m 64-bit lengths in tiles of kScanTile: per-tile sums, a
+// one-CTA scan of the tile sums (m <= 2^31: at most 2^18 tiles), then each
+// tile's own scan from its offset.  Three launches, ~3 passes over 8 m bytes.
+constexpr int kScanThreads = 1024, kScanPer = 8, kScanTile = kScanThreads * kScanPer;
+
+__device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long long v,
+                                                                  unsigned long long* total) {
+  __shared__ unsigned long long wsum[32];
+  __shared__ unsigned long long btot;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  unsigned long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();  // wsum / btot of a previous call are no longer read
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    unsigned long long t = lane < nw ? wsum[lane] : 0ull, u = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, u, o);
+      if (lane >= o) u += y;
+    }
+    if (lane < nw) wsum[lane] = u - t;
+    if (lane == 31) btot = u;
+  }
+  __syncthreads();
+  if (total) *total = btot;
+  return x - v + wsum[w];
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_tile_sums(const unsigned long long* in, long long m,
+                                                                 unsigned long long* tile_sum) {
+  const long long base = (long long)blockIdx.x * kScanTile + (long long)threadIdx.x * kScanPer;
+  unsigned long long v = 0;
+#pragma unroll
+  for (int i = 0; i < kScanPer; ++i)
+    if (base + i < m) v += in[base + i];
+  unsigned long long tot;
+  block_excl_scan_u64(v, &tot);
+  if (threadIdx.x == 0) tile_sum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_tile_offsets(unsigned long long* tile_sum, int tiles) {
+  unsigned long long carry = 0;
+  for (int t0 = 0; t0 < tiles; t0 += kScanThreads) {
+    const int t = t0 + threadIdx.x;
+    const unsigned long long v = t < tiles ? tile_sum[t] : 0ull;
+    unsigned long long tot;
+    const unsigned long long ex = block_excl_scan_u64(v, &tot);
+    if (t < tiles) tile_sum[t] = carry + ex;
+    carry += tot;
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const unsigned long long* in, long long m,
+                                                             const unsigned long long* tile_off,
+                                                             unsigned long long* out) {
+  const long long base = (long long)blockIdx.x * kScanTile + (long long)threadIdx.x * kScanPer;
+  unsigned long long x[kScanPer], v = 0;
+#pragma unroll
+  for (int i = 0; i < kScanPer; ++i) {
+    x[i] = base + i < m ? in[base + i] : 0ull;
+    v += x[i];
+  }
+  unsigned long long run = tile_off[blockIdx.x] + block_excl_scan_u64(v, nullptr);
+#pragma unroll
+  for (int i = 0; i < kScanPer; ++i) {
+    if (base + i < m) out[base + i] = run;
+    run += x[i];
+  }
+}
+
 }  // namespace
 
 cudaError_t format_values_device(const double* v, long long n, char* out, int* len, cudaStream_t s) {
@@ -195,10 +269,8 @@ cudaError_t format_values_device(const double* v, long long n, char* out, int* l
 }
 
 size_t format_scratch_bytes(long long count) {
-  size_t tmp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp, (unsigned long long*)nullptr,
-                                (unsigned long long*)nullptr, (int)count + 1);
-  return tmp + 2 * sizeof(unsigned long long) * (size_t)(count + 1) + 256;
+  const size_t tiles = (size_t)(count + 1 + kScanTile - 1) / kScanTile;
+  return sizeof(unsigned long long) * (2 * (size_t)(count + 1) + tiles) + 256;
 }
 
 // Formats records [0, count) of the pair space; returns the text size in
@@ -215,15 +287,17 @@ cudaError_t launch_format_records(const PairSpace& ps, const double* const stat[
   a.count = count;
   auto* len = static_cast<unsigned long long*>(scratch);
   auto* off = len + (count + 1);
-  void* cub_tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(off + (count + 1)) + 255) &
-                                          ~uintptr_t(255));
-  size_t cub_bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, len, off, (int)count + 1, s);
+  auto* tile_sum = reinterpret_cast<unsigned long long*>(
+      (reinterpret_cast<uintptr_t>(off + (count + 1)) + 255) & ~uintptr_t(255));
+  const long long m = count + 1;
+  const int tiles = (int)((m + kScanTile - 1) / kScanTile);
   cudaMemsetAsync(d_flag, 0, sizeof(int), s);
   cudaMemsetAsync(len + count, 0, sizeof(unsigned long long), s);
   const unsigned blocks = (unsigned)((count + 255) / 256);
   k_rec_len<<<blocks, 256, 0, s>>>(a, len, d_flag);
-  cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, len, off, (int)count + 1, s);
+  k_scan_tile_sums<<<tiles, kScanThreads, 0, s>>>(len, m, tile_sum);
+  k_scan_tile_offsets<<<1, kScanThreads, 0, s>>>(tile_sum, tiles);
+  k_scan_tiles<<<tiles, kScanThreads, 0, s>>>(len, m, tile_sum, off);
   unsigned long long total = 0;
   cudaMemcpyAsync(&total, off + count, sizeof total, cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(h_fallback, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s);

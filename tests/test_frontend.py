@@ -142,6 +142,25 @@ def test_results_file_matches_reference(tmp_path, monkeypatch, engine, reference
 
 
 @pytest.mark.gpu
+def test_results_file_many_records(tmp_path, monkeypatch, engine, reference):
+    """44,850 records (300 c1 variables): the device formatter's offset scan
+    spans several 8192-record tiles (k_scan_tile_sums / _offsets / _tiles);
+    the file equals the reference's byte for byte."""
+    monkeypatch.delenv("MINE_B200_HOST_FORMAT", raising=False)
+    w = datagen.make(1)
+    V = np.array(w.X[:300])
+    V[7] = 1.25
+    names = [f"v{i}" for i in range(300)]
+    src = _dataset_csv(tmp_path / "in.csv", names, V)
+    ref_out, our_out = str(tmp_path / "ref.csv"), str(tmp_path / "ours.csv")
+    n_ref = reference.analysis_file(src, ref_out, 0, 0, 0, 0.6, 15.0, None, workers=8)
+    rnames, rvalues = read_dataset(src)
+    n_ours = engine.run_analysis(rnames, rvalues, our_out, mode="all_pairs", params=Parameters(0.6, 15.0))
+    assert n_ours == n_ref == 300 * 299 // 2
+    assert open(our_out, "rb").read() == open(ref_out, "rb").read()
+
+
+@pytest.mark.gpu
 def test_variance_filter_matches_reference(engine, reference):
     rng = np.random.default_rng(11)
     V = rng.normal(scale=rng.uniform(0.2, 2.0, size=(30, 1)), size=(30, 25))
