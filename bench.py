@@ -21,7 +21,7 @@ from /root/reference/proj/src) with all host threads: whole c1 steps (all
 9.59M pairs each), at most 1 warm-up + 3 timed steps so the arm ends in
 about a minute.
 The default line also carries `secondary`: the other BASELINE configs (c0 all
-256 pairs, c2 a 20k-pair window, c3 a 4k-pair window, c4 32 pairs) with
+256 pairs, c2 a 20k-pair window, c3 a 4k-pair window, c4 148 pairs) with
 device and end-to-end pairs/s, SURVEY 8(d)'s roofline, the reference engine's
 CPU rate on a sample and a bit-exact-on-sample flag.
 """
