@@ -397,7 +397,15 @@ def run_ours(args, world, rank, local):
             traffic = int(t["dram_bytes_read"] + t["dram_bytes_write"])
         except Exception:
             pass
-        roof = {"bound": "lsu", "achieved": achieved, "peak": lds / 1e9 if lds else None,
+        ncu_pipe = None
+        try:
+            pp = json.load(open(os.path.join(ROOT, "profiles", "ncu_pipes.json")))["c1"]
+            ncu_pipe = {"limiting_pipe": pp.get("limiting_pipe"), "pct_of_peak": pp.get("limiting_pipe_pct"),
+                        "pipes_pct_of_peak": pp["pipes_pct_of_peak"], "capture": pp.get("capture"),
+                        "source": "profiles/ncu_pipes.json (ncu --set full, committed capture; not this run)"}
+        except Exception:
+            pass
+        roof = {"bound": "lsu", "ncu_limiting_pipe": ncu_pipe, "achieved": achieved, "peak": lds / 1e9 if lds else None,
                 "unit": "Ggather/s", "frac": achieved / (lds / 1e9) if lds else None,
                 "traffic": traffic,
                 "traffic_source": "profiles/ncu_traffic.json (dram read+write bytes per launch, ncu)",
